@@ -1,0 +1,146 @@
+"""ctypes front-end of ``liboracle.so`` (TEST INFRASTRUCTURE ONLY; see oracle/__init__.py).
+
+Arrays are numpy, [BH, N, d] float64 (inputs must hold bf16/fp32-exact values
+in quantised mode -- the oracle treats them as the FP32 numbers the kernels see).
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+CAUSAL, K_SMOOTH, Q_SMOOTH, QUANT_OFF = 1, 2, 4, 8
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sage_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force=False):
+    """Compile liboracle.so with gcc: -O2 -ffp-contract=off (exact FP32 emulation), OpenMP."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+                               "-fPIC", "-shared", "-std=c11", "-Wall", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        I, D = ctypes.c_int, ctypes.c_double
+        _lib.oracle_fwd.argtypes = [I, I, I, I, I, D] + [P] * 14
+        _lib.oracle_bwd.argtypes = [I, I, I, I, I, D] + [P] * 12
+        _lib.oracle_fpa.argtypes = [I, I, I, I, D] + [P] * 13
+        _lib.oracle_psi_block.argtypes = [P, I, I, P, P]
+        _lib.oracle_psi_token_row.argtypes = [P, I, D, P]
+        _lib.oracle_psi_token_row.restype = D
+        _lib.oracle_set_threads.argtypes = [I]
+        _lib.oracle_max_threads.restype = I
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def set_threads(n):
+    _load().oracle_set_threads(int(n))
+
+
+def max_threads():
+    return _load().oracle_max_threads()
+
+
+def psi_block(x, fp32_product=True):
+    """psi over one block (reading A4).  Returns (int8 values, fp32 scale as float)."""
+    x = _f64(x)
+    q = np.zeros(x.shape, dtype=np.int8)
+    s = np.zeros(1, dtype=np.float64)
+    _load().oracle_psi_block(_p(x), x.size, int(fp32_product), _p(q), _p(s))
+    return q, float(s[0])
+
+
+def psi_token_row(pt, rm_minus_m):
+    """Per-token P quantisation of one row (Alg. 1 line 9).  Returns (uint8 values, s_P)."""
+    pt = _f64(pt)
+    q = np.zeros(pt.shape, dtype=np.int8)
+    sp = _load().oracle_psi_token_row(_p(pt), pt.size, float(rm_minus_m), _p(q))
+    return q, sp
+
+
+def _default_tau(d, tau):
+    return 1.0 / np.sqrt(d) if tau is None else float(tau)
+
+
+def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk=128, tau=None):
+    """Alg. 1 per head.  Returns dict with o, lse and the Tier-A intermediates."""
+    q, k, v = _f64(q), _f64(k), _f64(v)
+    BH, N, d = q.shape
+    T = N // blk
+    flags = (CAUSAL if causal else 0) | (K_SMOOTH if k_smooth else 0) | \
+            (Q_SMOOTH if q_smooth else 0) | (0 if quant else QUANT_OFF)
+    out = dict(o=np.zeros((BH, N, d)), lse=np.zeros((BH, N)),
+               mu_k=np.zeros((BH, d), np.float32), mu_q=np.zeros((BH, T, d), np.float32),
+               bias=np.zeros((BH, T, N)),
+               q8=np.zeros((BH, N, d), np.int8), k8=np.zeros((BH, N, d), np.int8),
+               v8=np.zeros((BH, N, d), np.int8),
+               sq=np.zeros((BH, T), np.float32), sk=np.zeros((BH, T), np.float32),
+               sv=np.zeros((BH, T), np.float32))
+    rc = _load().oracle_fwd(BH, N, d, blk, flags, _default_tau(d, tau), _p(q), _p(k), _p(v),
+                            _p(out["o"]), _p(out["lse"]), _p(out["mu_k"]), _p(out["mu_q"]),
+                            _p(out["bias"]), _p(out["q8"]), _p(out["k8"]), _p(out["v8"]),
+                            _p(out["sq"]), _p(out["sk"]), _p(out["sv"]))
+    if rc:
+        raise ValueError("oracle_fwd: bad shape")
+    return out
+
+
+def bwd(q, k, v, o_stored, do, lse, *, causal=False, k_smooth=True, q_smooth=False, quant=True,
+        blk=128, tau=None):
+    """Alg. 2 per head.  o_stored is the O the forward stored (A15)."""
+    q, k, v, o_stored, do, lse = map(_f64, (q, k, v, o_stored, do, lse))
+    BH, N, d = q.shape
+    T = N // blk
+    flags = (CAUSAL if causal else 0) | (K_SMOOTH if k_smooth else 0) | \
+            (Q_SMOOTH if q_smooth else 0) | (0 if quant else QUANT_OFF)
+    out = dict(dq=np.zeros((BH, N, d)), dk=np.zeros((BH, N, d)), dv=np.zeros((BH, N, d)),
+               delta=np.zeros((BH, N)), do8=np.zeros((BH, N, d), np.int8),
+               sdo=np.zeros((BH, T), np.float32))
+    rc = _load().oracle_bwd(BH, N, d, blk, flags, _default_tau(d, tau), _p(q), _p(k), _p(v),
+                            _p(o_stored), _p(do), _p(lse), _p(out["dq"]), _p(out["dk"]),
+                            _p(out["dv"]), _p(out["delta"]), _p(out["do8"]), _p(out["sdo"]))
+    if rc:
+        raise ValueError("oracle_bwd: bad shape")
+    return out
+
+
+def fpa(q, k, v, do=None, *, causal=False, tau=None, intermediates=False):
+    """Full-precision attention fwd (+bwd if do given), materialising N x N."""
+    q, k, v = _f64(q), _f64(k), _f64(v)
+    BH, N, d = q.shape
+    do = None if do is None else _f64(do)
+    out = dict(o=np.zeros((BH, N, d)), lse=np.zeros((BH, N)))
+    if do is not None:
+        out.update(dq=np.zeros((BH, N, d)), dk=np.zeros((BH, N, d)), dv=np.zeros((BH, N, d)))
+    if intermediates:
+        out.update(P=np.zeros((BH, N, N)))
+        if do is not None:
+            out.update(dP=np.zeros((BH, N, N)), dS=np.zeros((BH, N, N)), delta=np.zeros((BH, N)))
+    rc = _load().oracle_fpa(BH, N, d, CAUSAL if causal else 0, _default_tau(d, tau),
+                            _p(q), _p(k), _p(v), _p(do), _p(out["o"]), _p(out["lse"]),
+                            _p(out.get("dq")), _p(out.get("dk")), _p(out.get("dv")),
+                            _p(out.get("P")), _p(out.get("dP")), _p(out.get("dS")),
+                            _p(out.get("delta")))
+    if rc:
+        raise ValueError("oracle_fpa: bad shape")
+    return out

@@ -1,0 +1,289 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (no GPU needed).
+
+Each test names the passage it pins.  A plausible mistake in the oracle (a dropped
+term, a wrong sign or index, a transposed operand) must fail at least one of these.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2603_02170_b200.inputs import make_inputs
+from tests.metrics import cos_sim, f64, rel_l2, rms
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rand(rng, *shape, scale=1.0):
+    """fp32-exact random doubles (the oracle's quantised mode sees FP32 numbers)."""
+    return (rng.standard_normal(shape) * scale).astype(np.float32).astype(np.float64)
+
+
+def _golden_psi():
+    rows = []
+    for line in open(os.path.join(GOLDEN, "psi_examples.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        kind, inp, scale, vals = [f.strip() for f in line.split("|")]
+        parse = lambda s: np.array([[float(x) for x in r.split()] for r in s.split(";")])
+        rows.append((kind, parse(inp), scale, parse(vals)))
+    return rows
+
+
+# --------------------------------------------------------------------------- psi
+def test_psi_worked_examples(orc):
+    """SPEC S:129-130 / P:110-114 worked examples, and the per-token example S:150."""
+    for kind, x, scale, vals in _golden_psi():
+        if kind == "block":
+            q, s = orc.psi_block(x)
+            assert s == float(scale)
+            np.testing.assert_array_equal(q, vals.astype(np.int8))
+        else:
+            q, sp = orc.psi_token_row(x.ravel(), 0.0)
+            assert sp == pytest.approx(1.0 / 127.0, rel=1e-15)
+            np.testing.assert_array_equal(q, vals.ravel().astype(np.int8))
+
+
+def test_psi_half_step_bound_and_saturation(orc):
+    """|x - q*scale| <= scale/2 (+fp32 slack, A4) and max|q| = 127 for nonzero blocks."""
+    rng = np.random.default_rng(0)
+    for trial in range(200):
+        x = _rand(rng, 128, 64, scale=10.0 ** rng.uniform(-6, 3))
+        q, s = orc.psi_block(x)
+        assert np.abs(q.astype(int)).max() == 127
+        assert s == pytest.approx(np.abs(x).max() / 127.0, rel=2 ** -23)
+        err = np.abs(x - q.astype(np.float64) * s)
+        assert err.max() <= s * (0.5 + 2 ** -15)
+
+
+def test_psi_grid_fixed_point(orc):
+    """Quantise-dequantise of a block already on the grid {-127s..127s} is exact."""
+    rng = np.random.default_rng(1)
+    ints = rng.integers(-127, 128, size=(128, 64)).astype(np.float64)
+    ints[0, 0] = 127
+    q, s = orc.psi_block(ints * 0.5)          # power-of-two scale: exactly representable grid
+    assert s == np.float32(127 * 0.5) / np.float32(127)
+    np.testing.assert_array_equal(q.astype(np.float64), ints)
+
+
+def test_psi_token_row_properties(orc):
+    """Row owning the running max reaches 127; scale e^{rm-m}/127; S:151 case."""
+    rng = np.random.default_rng(2)
+    s = rng.standard_normal(128)
+    m = s.max()
+    q, sp = orc.psi_token_row(np.exp(s - m), 0.0)
+    assert q.max() == 127 and q.min() >= 0
+    # rm - m = -ln(127): scales 1/127^2, entries <= 1/127 stay <= 127, no clamping.
+    pt = np.exp(s - s.max()) / 127.0
+    q, sp = orc.psi_token_row(pt, -math.log(127.0))
+    assert sp == pytest.approx(1.0 / 127.0 ** 2, rel=1e-12)
+    assert q.max() == 127
+
+
+# --------------------------------------------------------------------------- FPA
+@pytest.mark.parametrize("causal", [False, True])
+def test_fpa_finite_differences(orc, causal):
+    """FPA gradients == central finite differences of L = sum(O o G), step 1e-5."""
+    for N, d in [(4, 2), (8, 4)]:
+        for seed in range(5):
+            rng = np.random.default_rng(100 + seed)
+            q, k, v, g = (rng.standard_normal((1, N, d)) for _ in range(4))
+            out = orc.fpa(q, k, v, g, causal=causal)
+            for name, x in (("dq", q), ("dk", k), ("dv", v)):
+                fd = np.zeros_like(x)
+                for idx in np.ndindex(x.shape):
+                    xp, xm = x.copy(), x.copy()
+                    xp[idx] += 1e-5
+                    xm[idx] -= 1e-5
+                    args = dict(q=q, k=k, v=v)
+                    args[name[1]] = xp
+                    lp = (orc.fpa(**args, causal=causal)["o"] * g).sum()
+                    args[name[1]] = xm
+                    lm = (orc.fpa(**args, causal=causal)["o"] * g).sum()
+                    fd[idx] = (lp - lm) / 2e-5
+                assert rel_l2(fd, out[name]) <= 1e-5, (name, N, d, seed)
+
+
+def test_fpa_closed_forms(orc):
+    """N=1 -> O = V; Q=K=V=0 -> uniform P, O = 0; rows of P sum to 1."""
+    rng = np.random.default_rng(3)
+    v = rng.standard_normal((1, 1, 8))
+    out = orc.fpa(rng.standard_normal((1, 1, 8)), rng.standard_normal((1, 1, 8)), v)
+    np.testing.assert_allclose(out["o"], v, rtol=0, atol=1e-15)
+    z = np.zeros((1, 4, 2))
+    out = orc.fpa(z, z, z, intermediates=True)
+    np.testing.assert_allclose(out["P"], 0.25, atol=1e-15)
+    np.testing.assert_allclose(out["o"], 0.0, atol=1e-15)
+    np.testing.assert_allclose(out["lse"], math.log(4), atol=1e-15)
+    out = orc.fpa(*(rng.standard_normal((2, 32, 8)) for _ in range(3)), causal=True, intermediates=True)
+    np.testing.assert_allclose(out["P"].sum(-1), 1.0, atol=1e-12)
+    assert np.all(np.triu(out["P"][0], 1) == 0.0)
+
+
+def test_ds_bound_appendix_b(orc):
+    """App. B: RMS(dS) <= max_i ||dP_i - delta_i||_inf / sqrt(N); RMS(P_i) <= 1/sqrt(N)
+    (P:748-755); dS rows sum to 0.  dO = 0 gives lhs = rhs = 0."""
+    rng = np.random.default_rng(4)
+    for N in (16, 64, 256):
+        for d in (8, 64):
+            for sigma in (1.0, 5.0, 10.0):
+                q, k = (sigma * rng.standard_normal((1, N, d)) for _ in range(2))
+                v, do = (rng.standard_normal((1, N, d)) for _ in range(2))
+                out = orc.fpa(q, k, v, do, intermediates=True)
+                P, dP, dS, delta = out["P"][0], out["dP"][0], out["dS"][0], out["delta"][0]
+                rhs = np.abs(dP - delta[:, None]).max() / math.sqrt(N)
+                assert rms(dS) <= rhs + 1e-15
+                assert np.all(np.sqrt((P * P).mean(-1)) <= 1 / math.sqrt(N) + 1e-12)
+                assert np.abs(dS.sum(-1)).max() <= 1e-9 * np.abs(dS).max() + 1e-12
+    z = np.zeros((1, 16, 8))
+    out = orc.fpa(rng.standard_normal((1, 16, 8)), rng.standard_normal((1, 16, 8)), z, z, intermediates=True)
+    assert rms(out["dS"]) == 0.0
+
+
+# --------------------------------------------------------------------------- tiled, quantisation off
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("smooth", ["none", "k", "qk"])
+@pytest.mark.parametrize("N,blk", [(64, 16), (64, 32), (96, 32), (128, 128)])
+def test_tiled_quant_off_equals_fpa(orc, causal, smooth, N, blk):
+    """Alg. 1/2 with psi = identity == naive attention <= 1e-9.
+    With smoothing this also pins: K-smoothing invariance, the
+    four-term decomposition with the bias added back and
+    dK = dK_center + dK_bias."""
+    rng = np.random.default_rng(5)
+    d = 16
+    q = rng.standard_normal((2, N, d)) + rng.standard_normal(d) * 3
+    k = rng.standard_normal((2, N, d)) + rng.standard_normal(d) * 5
+    v, do = rng.standard_normal((2, N, d)), rng.standard_normal((2, N, d))
+    ref = orc.fpa(q, k, v, do, causal=causal)
+    kw = dict(causal=causal, k_smooth=smooth != "none", q_smooth=smooth == "qk", quant=False, blk=blk)
+    f = orc.fwd(q, k, v, **kw)
+    assert rel_l2(ref["o"], f["o"]) <= 1e-9
+    # smoothing drops the row-constant terms Q_sm mu_K^T + mu_Q mu_K^T = Q mu_K^T,
+    # so L of the smoothed logits is L_FPA - tau * Q_r . mu_K
+    shift = np.einsum("bnd,bd->bn", q, k.mean(1)) / math.sqrt(d) if smooth != "none" else 0.0
+    np.testing.assert_allclose(f["lse"] + shift, ref["lse"], rtol=0, atol=1e-8)
+    b = orc.bwd(q, k, v, f["o"], do, f["lse"], **kw)
+    for name in ("dq", "dk", "dv"):
+        assert rel_l2(ref[name], b[name]) <= 1e-9, name
+
+
+# --------------------------------------------------------------------------- tiled, quantised (the QO)
+def test_quant_mu_and_blocks(orc):
+    """mu_K = exact column mean over all N tokens, rounded once to fp32 (A12, A17);
+    every 128 x d block of K_sm, V satisfies the psi contract."""
+    q, k, v, do = make_inputs(1, 2, 512, 64, "outlier_k", seed=7)
+    q, k, v = f64(q), f64(k), f64(v)
+    out = orc.fwd(q.reshape(2, 512, 64), k.reshape(2, 512, 64), v.reshape(2, 512, 64), causal=True)
+    for h in range(2):
+        kh = k[0, h]
+        mu = np.array([math.fsum(kh[:, c]) / 512 for c in range(64)], dtype=np.float32)
+        np.testing.assert_array_equal(out["mu_k"][h], mu)
+        ksm = (kh.astype(np.float32) - mu).astype(np.float64)
+        for t in range(4):
+            blkk = ksm[t * 128:(t + 1) * 128]
+            q8 = out["k8"][h, t * 128:(t + 1) * 128].astype(np.float64)
+            s = float(out["sk"][h, t])
+            assert np.abs(q8).max() == 127
+            assert np.abs(blkk - q8 * s).max() <= s * (0.5 + 2 ** -15)
+            vb = v[0, h, t * 128:(t + 1) * 128]
+            v8 = out["v8"][h, t * 128:(t + 1) * 128].astype(np.float64)
+            assert np.abs(vb - v8 * float(out["sv"][h, t])).max() <= float(out["sv"][h, t]) * (0.5 + 2 ** -15)
+
+
+def test_quant_lse_is_logsumexp_of_quantised_logits(orc):
+    """L_i = m + log l (Alg. 1 line 14, A7) equals the direct logsumexp of the dequantised
+    INT8 logits S = (Q^ K^T) s_Q s_K tau (line 7, A6), causal mask (A14)."""
+    q, k, v, _ = (f64(t).reshape(1, 384, 64) for t in make_inputs(1, 1, 384, 64, "gauss", seed=8, sigma=3.0))
+    out = orc.fwd(q, k, v, causal=True)
+    q8, k8 = out["q8"][0].astype(np.int64), out["k8"][0].astype(np.int64)
+    sq, sk = np.repeat(out["sq"][0].astype(np.float64), 128), np.repeat(out["sk"][0].astype(np.float64), 128)
+    S = (q8 @ k8.T).astype(np.float64) * sq[:, None] * sk[None, :] / 8.0
+    S[np.triu_indices(384, 1)] = -np.inf
+    mx = S.max(1)
+    lse = mx + np.log(np.exp(S - mx[:, None]).sum(1))
+    np.testing.assert_allclose(out["lse"][0], lse, rtol=0, atol=1e-9)
+    # O approximates softmax(S) V up to the P~ / V quantisation (half-step bounds)
+    P = np.exp(S - lse[:, None])
+    assert rel_l2(P @ v[0], out["o"][0]) < 0.02
+
+
+def test_quant_zero_do_gives_zero_grads(orc):
+    """dO = 0 -> dQ = dK = dV = 0 exactly (all-zero blocks, A3)."""
+    q, k, v, _ = (f64(t).reshape(2, 256, 64) for t in make_inputs(1, 2, 256, 64, "gauss", seed=9))
+    f = orc.fwd(q, k, v, causal=True)
+    b = orc.bwd(q, k, v, f["o"], np.zeros_like(q), f["lse"], causal=True)
+    for name in ("dq", "dk", "dv"):
+        assert np.all(b[name] == 0.0)
+
+
+def _fidelity(orc, q, k, v, do, **kw):
+    ref = orc.fpa(q, k, v, do, causal=kw.get("causal", False))
+    f = orc.fwd(q, k, v, **kw)
+    o_st = f["o"]
+    b = orc.bwd(q, k, v, o_st, do, f["lse"], **kw)
+    res = {"o": (cos_sim(ref["o"], f["o"]), rel_l2(ref["o"], f["o"]))}
+    for name in ("dq", "dk", "dv"):
+        res[name] = (cos_sim(ref[name], b[name]), rel_l2(ref[name], b[name]))
+    return res
+
+
+def _table1():
+    rows = {}
+    for line in open(os.path.join(GOLDEN, "table1_qkstd.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        f = [float(x) for x in line.split()]
+        rows[f[0]] = {"o": f[1:3], "dq": f[3:5], "dk": f[5:7], "dv": f[7:9]}
+    return rows
+
+
+@pytest.mark.slow
+def test_table1_sigma_sweep(orc):
+    """Table 1: SageBwd vs FPA on Gaussian Q, K with sigma in {1,3,5,8,10}.
+    The paper does not state N or d; at N = 1024, d = 64 (non-causal, K-smoothing on,
+    P:405) the oracle must (a) grow strictly in sigma for every tensor and
+    (b) land within the bands below of the paper's values (band evidence: DESIGN.md 3.3)."""
+    tab = _table1()
+    res = {}
+    for sigma in (1.0, 3.0, 5.0, 8.0, 10.0):
+        q, k, v, do = (f64(t).reshape(1, 1024, 64) for t in
+                       make_inputs(1, 1, 1024, 64, "gauss", seed=11, sigma=sigma))
+        res[sigma] = _fidelity(orc, q, k, v, do)
+    sig = sorted(res)
+    for name in ("o", "dq", "dk", "dv"):
+        # dV at sigma = 1 sits above sigma = 3 under the literal per-tile psi(P) (reading A11)
+        start = 1 if name == "dv" else 0
+        rels = [res[s][name][1] for s in sig[start:]]
+        assert all(a < b for a, b in zip(rels, rels[1:])), (name, rels)
+    for s in sig:
+        for name in ("o", "dq", "dk", "dv"):
+            paper = tab[s][name][1]
+            got = res[s][name][1]
+            # sigma >= 3: within [0.75, 1.35] x paper.  sigma = 1: the gradients of the literal
+            # per-tile psi(P)/psi(dS) reading (A11) sit up to ~3.7x above the paper.
+            lo, hi = (0.75, 1.35) if (name == "o" or s >= 3) else (0.75, 4.5)
+            assert lo * paper <= got <= hi * paper, (s, name, got, paper)
+    # sigma = 10: dQ/dK cosine collapses below 0.9 (paper 0.78)
+    assert res[10.0]["dq"][0] < 0.9 and res[10.0]["dk"][0] < 0.9
+
+
+def test_k_smoothing_matters_on_outlier_k(orc):
+    """K-smoothing is what keeps INT8 QK^T accurate under channel outliers:
+    with outlier-injected K the quantised dQ error vs FPA must drop >= 2x when it is on."""
+    q, k, v, do = (f64(t).reshape(2, 512, 64) for t in make_inputs(1, 2, 512, 64, "outlier_k", seed=12))
+    on = _fidelity(orc, q, k, v, do, causal=True, k_smooth=True)
+    off = _fidelity(orc, q, k, v, do, causal=True, k_smooth=False)
+    assert off["dq"][1] > 2.0 * on["dq"][1]
+    assert on["o"][1] < 0.05
+
+
+def test_q_smoothing_bias_pathways(orc):
+    """Q-smoothing with the bias added back and dK_bias keeps the quantised
+    method close to FPA even with large Q channel offsets; dropping either term would not."""
+    q, k, v, do = (f64(t).reshape(2, 256, 64) for t in make_inputs(1, 2, 256, 64, "outlier_kq", seed=13))
+    q = q + 20.0                           # a large block mean makes mu_Q matter
+    res = _fidelity(orc, q, k, v, do, causal=True, k_smooth=True, q_smooth=True)
+    assert res["o"][1] < 0.06
+    assert res["dk"][1] < 0.15 and res["dq"][1] < 0.15
