@@ -1,0 +1,136 @@
+/*
+ * sage.h -- C ABI of libsage.so: SageBwd trainable INT8 attention (arXiv 2603.02170)
+ * forward and backward, hand-written for sm_100a (B200).
+ *
+ * The operations (PAPER.md line numbers, section/algorithm in brackets):
+ *   sage_fwd  Alg. 1, P:638-671 [App. A "Forward pass of the 8-bit attention"]:
+ *             K-smoothing K <- K - mean_row(K), optional block-wise
+ *             Q-smoothing with the low-rank bias added back, per-block INT8
+ *             psi of Q, K, V (Alg. 1 line 3), INT8 S = Q^K^T (line 7),
+ *             online softmax (line 8), per-token INT8 P~ (line 9), INT8 P^V^ (line 10),
+ *             O and logsumexp L (lines 13-14).
+ *   sage_bwd  Alg. 2, P:674-708 [App. A "Backward pass of the 8-bit attention"]:
+ *             delta = rowsum(dO o O) (line 2), INT8 S recompute and P = exp(S - L) (line 5),
+ *             psi(P), psi(dO) (line 6), INT8 dV (line 7), dP = dO V^T unquantised in
+ *             BF16 with FP32 accumulation (line 8), dS = P o (dP - delta) and
+ *             psi(dS) (line 9), INT8 dQ (line 10), INT8 dK (line 11) plus the Q-smoothing
+ *             dK bias branch.
+ * Readings of ambiguous passages (tile size 128, softmax scale 1/sqrt(d), rounding,
+ * all-zero blocks, causal masking, ...) are listed in DESIGN.md section 3.
+ *
+ * Conventions
+ *   - Tensors Q, K, V, O, dO, dQ, dK, dV: bf16, contiguous [B, H, N, d] (d innermost),
+ *     16-byte aligned device pointers.  N % 128 == 0, d in {64, 128}.
+ *   - lse: fp32 [B, H, N], natural log (Alg. 1 line 14).
+ *   - Ownership: the caller allocates every buffer (device memory), including the
+ *     forward->backward context `ctx` (sage_ctx_bytes) and the scratch workspace
+ *     (sage_workspace_bytes).  The library never allocates or frees device memory.
+ *   - Execution: every call only enqueues kernels on `stream` and returns; errors in
+ *     arguments are reported before anything is launched (nothing is written).
+ *     Asynchronous device faults surface at the caller's next synchronisation.
+ *   - There is no CPU fallback: without an sm_100 device the calls return SAGE_ERR_ARCH.
+ */
+#ifndef SAGE_H_
+#define SAGE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SAGE_API __attribute__((visibility("default")))
+#else
+#define SAGE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SAGE_OK = 0,
+  SAGE_ERR_INVALID_VALUE = 1, /* null pointer, bad shape/flags, N % 128 != 0, d not in {64,128} */
+  SAGE_ERR_UNSUPPORTED = 2,   /* valid but not implemented combination */
+  SAGE_ERR_MISALIGNED = 3,    /* a pointer is not 16-byte aligned */
+  SAGE_ERR_WORKSPACE = 4,     /* ctx or workspace smaller than required */
+  SAGE_ERR_CUDA = 5,          /* a CUDA runtime call or launch failed (see sage_last_cuda_error) */
+  SAGE_ERR_ARCH = 6           /* current device is not sm_100 */
+} sage_status;
+
+/* sage_params.flags */
+enum {
+  SAGE_CAUSAL = 1u << 0,   /* mask key n > query r (reading A14) */
+  SAGE_K_SMOOTH = 1u << 1, /* K-smoothing, P:136-147 (the paper's default) */
+  SAGE_Q_SMOOTH = 1u << 2  /* block-wise Q-smoothing + bias */
+};
+
+typedef struct {
+  int32_t batch, heads, seqlen, head_dim; /* B, H, N, d */
+  uint32_t flags;                         /* SAGE_* bit set */
+  float softmax_scale;                    /* tau; 0 => 1/sqrt(d) (reading A6) */
+} sage_params;
+
+/* Bytes of the forward->backward context: int8 Q^, K^ [B,H,N,d]; fp32 s_Q, s_K
+ * [B,H,N/128]; mu_K [B,H,d]; and with SAGE_Q_SMOOTH mu_Q [B,H,N/128,d] and the
+ * bias [B,H,N/128,N] (Alg. 2 line 1 inputs).  0 on invalid params. */
+SAGE_API size_t sage_ctx_bytes(const sage_params* p);
+
+/* Bytes of scratch for sage_fwd (backward = 0: V^, s_V, partial sums) or sage_bwd
+ * (backward = 1: dO^, s_dO, delta, L*log2(e), fp32 dQ accumulator). 0 on invalid params. */
+SAGE_API size_t sage_workspace_bytes(const sage_params* p, int backward);
+
+/* Forward (Alg. 1).  Reads q, k, v; writes o, lse and the context ctx.
+ * ws must hold sage_workspace_bytes(p, 0) bytes.  stream: a cudaStream_t (NULL = legacy). */
+SAGE_API sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const void* v, void* o, float* lse,
+                     void* ctx, size_t ctx_bytes, void* ws, size_t ws_bytes, void* stream);
+
+/* Backward (Alg. 2).  Reads v, the o and lse written by sage_fwd, dO and ctx; writes
+ * dq, dk, dv.  ws must hold sage_workspace_bytes(p, 1) bytes. */
+SAGE_API sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const float* lse, const void* dO,
+                     const void* ctx, size_t ctx_bytes, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
+                     void* stream);
+
+/* Device pointers into a context / workspace buffer (for tests and tracing; no launch). */
+typedef struct {
+  int8_t *q_i8, *k_i8;        /* [B,H,N,d] psi(Q_sm or Q), psi(K_sm) */
+  float *q_scale, *k_scale;   /* [B,H,N/128] */
+  float* mu_k;                /* [B,H,d] */
+  float* mu_q;                /* [B,H,N/128,d] or NULL */
+  float* bias;                /* [B,H,N/128,N] or NULL: bias_i[n] = mu_Qi . K_sm[n] */
+} sage_ctx_view;
+SAGE_API sage_status sage_ctx_get_view(const sage_params* p, void* ctx, sage_ctx_view* out);
+
+typedef struct {
+  int8_t* v_i8;   /* fwd: [B,H,N,d] psi(V) */
+  float* v_scale; /* fwd: [B,H,N/128] */
+  int8_t* do_i8;  /* bwd: [B,H,N,d] psi(dO) */
+  float* do_scale;/* bwd: [B,H,N/128] */
+  float* delta;   /* bwd: [B,H,N] rowsum(dO o O) */
+  float* dq_acc;  /* bwd: [B,H,N,d] fp32 dQ accumulator */
+} sage_ws_view;
+SAGE_API sage_status sage_ws_get_view(const sage_params* p, int backward, void* ws, sage_ws_view* out);
+
+/* Test entry (Tier B parity): one 128 x N UMMA tile through the same descriptor and
+ * TMEM code the fused kernels use.  mode 0: int32 D = A[128][K] . B[N][K]^T with both
+ * operands K-major (K in {64,128}, N = 128);  mode 1: A K-major [128][128] written by
+ * threads (P^ path), B MN-major [128][N] (N in {64,128}); mode 2: A MN-major [K=128][M=128],
+ * B MN-major [128][N]; mode 3: fp32 D = A . B^T, bf16 K-major operands [128][K], [128][K].
+ * a, b, d: device pointers to row-major host-order arrays as described (int8/bf16 in, int32/fp32 out). */
+SAGE_API sage_status sage_debug_umma(int mode, int K, int N, const void* a, const void* b, void* d, void* stream);
+
+/* Optional instrumentation (calling thread only).  While enabled, sage_fwd / sage_bwd record
+ * a CUDA event pair around their fused kernel (K2 / K4) and count every kernel they launch.
+ * sage_profile_read synchronises on the recorded events, returns the summed K2 and K4 device
+ * times (ms), the number of K2 / K4 launches and of all library kernel launches since the last
+ * read, and resets the counters.  Disabled by default: zero cost on the normal path. */
+SAGE_API sage_status sage_profile_enable(int enable);
+SAGE_API sage_status sage_profile_read(double* fwd_kernel_ms, double* bwd_kernel_ms, int64_t* n_fwd, int64_t* n_bwd,
+                                       int64_t* n_launches);
+
+SAGE_API const char* sage_status_string(sage_status s);
+SAGE_API int sage_last_cuda_error(void); /* cudaError_t of the last SAGE_ERR_CUDA (per thread) */
+SAGE_API int sage_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAGE_H_ */

@@ -1,0 +1,433 @@
+// sage_api.cu -- the extern "C" boundary of libsage.so (include/sage.h): argument
+// validation, carving of the caller-owned ctx / workspace buffers, TMA tensor-map
+// encoding and the kernel launch sequence of sage_fwd (K0, K1, [bias], K2) and
+// sage_bwd (K3, K4, K5).  No device memory is allocated here.
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <utility>
+#include <vector>
+
+#include "../../include/sage.h"
+#include "sage_internal.h"
+
+namespace sage {
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+
+sage_status cuda_fail(cudaError_t e) {
+  g_last_cuda_error = (int)e;
+  return SAGE_ERR_CUDA;
+}
+
+// ---- cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// Per-device arch check (sm_100 only; there is no fallback path).  Also clears a stale
+// error another library left in this thread's runtime state, so that the
+// cudaGetLastError() after each of our launches reports only our own launches.
+sage_status check_arch() {
+  (void)cudaGetLastError();
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e);
+  int major = 0, minor = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+    return SAGE_ERR_ARCH;
+  return (major == 10 && minor == 0) ? SAGE_OK : SAGE_ERR_ARCH;
+}
+
+constexpr size_t kAlign = 256;
+size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Dims {
+  size_t BH, N, d, T;
+  bool causal, ks, qs;
+  float tau;
+};
+
+bool dims_of(const sage_params* p, Dims* o) {
+  if (!p) return false;
+  if (p->batch <= 0 || p->heads <= 0 || p->seqlen <= 0) return false;
+  if (p->head_dim != 64 && p->head_dim != 128) return false;
+  if (p->seqlen % kBlk) return false;
+  if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH)) return false;
+  if (!(p->softmax_scale >= 0.f) || std::isinf(p->softmax_scale)) return false;
+  const size_t BH = (size_t)p->batch * p->heads;
+  if (BH * p->seqlen > (size_t)INT32_MAX / 2) return false;  // TMA row coordinates are int32
+  o->BH = BH;
+  o->N = p->seqlen;
+  o->d = p->head_dim;
+  o->T = o->N / kBlk;
+  o->causal = p->flags & SAGE_CAUSAL;
+  o->ks = p->flags & SAGE_K_SMOOTH;
+  o->qs = p->flags & SAGE_Q_SMOOTH;
+  o->tau = p->softmax_scale > 0.f ? p->softmax_scale : 1.f / std::sqrt((float)p->head_dim);
+  return true;
+}
+
+// ---- carving.  ctx: q_i8, k_i8, q_scale, k_scale, mu_k, [mu_q, bias]
+struct CtxLayout {
+  size_t q8, k8, sq, sk, muk, muq, bias, total;
+};
+CtxLayout ctx_layout(const Dims& D) {
+  CtxLayout L{};
+  size_t off = 0, nd = D.BH * D.N * D.d;
+  L.q8 = off; off += up(nd);
+  L.k8 = off; off += up(nd);
+  L.sq = off; off += up(D.BH * D.T * 4);
+  L.sk = off; off += up(D.BH * D.T * 4);
+  L.muk = off; off += up(D.BH * D.d * 4);
+  L.muq = off; off += D.qs ? up(D.BH * D.T * D.d * 4) : 0;
+  L.bias = off; off += D.qs ? up(D.BH * D.T * D.N * 4) : 0;
+  L.total = off;
+  return L;
+}
+// fwd ws: v_i8, v_scale, colsum partials (K [, Q])
+struct FwdWs {
+  size_t v8, sv, partk, partq, total;
+};
+FwdWs fwd_ws(const Dims& D) {
+  FwdWs W{};
+  size_t off = 0, nd = D.BH * D.N * D.d;
+  W.v8 = off; off += up(nd);
+  W.sv = off; off += up(D.BH * D.T * 4);
+  W.partk = off; off += up(D.BH * D.T * D.d * 8);
+  W.partq = off; off += D.qs ? up(D.BH * D.T * D.d * 8) : 0;
+  W.total = off;
+  return W;
+}
+// bwd ws: do_i8, do_scale, delta, l2, dq_acc
+struct BwdWs {
+  size_t do8, sdo, delta, l2, dq, total;
+};
+BwdWs bwd_ws(const Dims& D) {
+  BwdWs W{};
+  size_t off = 0, nd = D.BH * D.N * D.d;
+  W.do8 = off; off += up(nd);
+  W.sdo = off; off += up(D.BH * D.T * 4);
+  W.delta = off; off += up(D.BH * D.N * 4);
+  W.l2 = off; off += up(D.BH * D.N * 4);
+  W.dq = off; off += up(nd * 4);
+  W.total = off;
+  return W;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---- optional instrumentation (sage_profile_enable / sage_profile_read), per thread
+struct Prof {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[2];  // [0] K2, [1] K4
+  std::vector<cudaEvent_t> pool;
+  int64_t launches = 0;
+  cudaEvent_t get() {
+    cudaEvent_t e = nullptr;
+    if (!pool.empty()) {
+      e = pool.back();
+      pool.pop_back();
+    } else if (cudaEventCreate(&e) != cudaSuccess) {
+      e = nullptr;
+    }
+    return e;
+  }
+};
+thread_local Prof g_prof;
+
+// Launch `fn` (the fused kernel) bracketed by events when profiling.
+template <typename F>
+cudaError_t timed(int which, cudaStream_t s, F&& fn) {
+  if (!g_prof.on) return fn();
+  cudaEvent_t a = g_prof.get(), b = g_prof.get();
+  if (a) cudaEventRecord(a, s);
+  cudaError_t e = fn();
+  if (b) cudaEventRecord(b, s);
+  if (a && b) g_prof.ev[which].emplace_back(a, b);
+  return e;
+}
+
+template <typename T>
+T* at(void* base, size_t off) {
+  return reinterpret_cast<T*>(static_cast<uint8_t*>(base) + off);
+}
+
+}  // namespace
+
+bool make_tmap_2d(CUtensorMap* m, const void* base, bool bf16, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                  uint32_t box_cols) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  const uint32_t esz = bf16 ? 2 : 1;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * esz};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  const uint32_t row_bytes = box_cols * esz;
+  CUtensorMapSwizzle sw = row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace sage
+
+using namespace sage;
+
+extern "C" {
+
+int sage_version(void) { return 1; }
+
+const char* sage_status_string(sage_status s) {
+  switch (s) {
+    case SAGE_OK: return "SAGE_OK";
+    case SAGE_ERR_INVALID_VALUE: return "SAGE_ERR_INVALID_VALUE";
+    case SAGE_ERR_UNSUPPORTED: return "SAGE_ERR_UNSUPPORTED";
+    case SAGE_ERR_MISALIGNED: return "SAGE_ERR_MISALIGNED";
+    case SAGE_ERR_WORKSPACE: return "SAGE_ERR_WORKSPACE";
+    case SAGE_ERR_CUDA: return "SAGE_ERR_CUDA";
+    case SAGE_ERR_ARCH: return "SAGE_ERR_ARCH";
+  }
+  return "SAGE_ERR_UNKNOWN";
+}
+
+int sage_last_cuda_error(void) { return g_last_cuda_error; }
+
+sage_status sage_profile_enable(int enable) {
+  g_prof.on = enable != 0;
+  return SAGE_OK;
+}
+
+sage_status sage_profile_read(double* fwd_kernel_ms, double* bwd_kernel_ms, int64_t* n_fwd, int64_t* n_bwd,
+                              int64_t* n_launches) {
+  double ms[2] = {0.0, 0.0};
+  int64_t n[2] = {0, 0};
+  cudaError_t err = cudaSuccess;
+  for (int w = 0; w < 2; ++w) {
+    for (auto& pr : g_prof.ev[w]) {
+      float t = 0.f;
+      cudaError_t e = cudaEventSynchronize(pr.second);
+      if (e == cudaSuccess) e = cudaEventElapsedTime(&t, pr.first, pr.second);
+      if (e != cudaSuccess) err = e;
+      ms[w] += t;
+      ++n[w];
+      g_prof.pool.push_back(pr.first);
+      g_prof.pool.push_back(pr.second);
+    }
+    g_prof.ev[w].clear();
+  }
+  if (fwd_kernel_ms) *fwd_kernel_ms = ms[0];
+  if (bwd_kernel_ms) *bwd_kernel_ms = ms[1];
+  if (n_fwd) *n_fwd = n[0];
+  if (n_bwd) *n_bwd = n[1];
+  if (n_launches) *n_launches = g_prof.launches;
+  g_prof.launches = 0;
+  return err == cudaSuccess ? SAGE_OK : cuda_fail(err);
+}
+
+size_t sage_ctx_bytes(const sage_params* p) {
+  Dims D;
+  return dims_of(p, &D) ? ctx_layout(D).total : 0;
+}
+
+size_t sage_workspace_bytes(const sage_params* p, int backward) {
+  Dims D;
+  if (!dims_of(p, &D)) return 0;
+  return backward ? bwd_ws(D).total : fwd_ws(D).total;
+}
+
+sage_status sage_ctx_get_view(const sage_params* p, void* ctx, sage_ctx_view* out) {
+  Dims D;
+  if (!dims_of(p, &D) || !ctx || !out) return SAGE_ERR_INVALID_VALUE;
+  CtxLayout L = ctx_layout(D);
+  out->q_i8 = at<int8_t>(ctx, L.q8);
+  out->k_i8 = at<int8_t>(ctx, L.k8);
+  out->q_scale = at<float>(ctx, L.sq);
+  out->k_scale = at<float>(ctx, L.sk);
+  out->mu_k = at<float>(ctx, L.muk);
+  out->mu_q = D.qs ? at<float>(ctx, L.muq) : nullptr;
+  out->bias = D.qs ? at<float>(ctx, L.bias) : nullptr;
+  return SAGE_OK;
+}
+
+sage_status sage_ws_get_view(const sage_params* p, int backward, void* ws, sage_ws_view* out) {
+  Dims D;
+  if (!dims_of(p, &D) || !ws || !out) return SAGE_ERR_INVALID_VALUE;
+  std::memset(out, 0, sizeof(*out));
+  if (backward) {
+    BwdWs W = bwd_ws(D);
+    out->do_i8 = at<int8_t>(ws, W.do8);
+    out->do_scale = at<float>(ws, W.sdo);
+    out->delta = at<float>(ws, W.delta);
+    out->dq_acc = at<float>(ws, W.dq);
+  } else {
+    FwdWs W = fwd_ws(D);
+    out->v_i8 = at<int8_t>(ws, W.v8);
+    out->v_scale = at<float>(ws, W.sv);
+  }
+  return SAGE_OK;
+}
+
+sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const void* v, void* o, float* lse,
+                     void* ctx, size_t ctx_bytes, void* ws, size_t ws_bytes, void* stream) {
+  Dims D;
+  if (!dims_of(p, &D) || !q || !k || !v || !o || !lse || !ctx || !ws) return SAGE_ERR_INVALID_VALUE;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(lse) || !aligned16(ctx) ||
+      !aligned16(ws))
+    return SAGE_ERR_MISALIGNED;
+  const CtxLayout C = ctx_layout(D);
+  const FwdWs W = fwd_ws(D);
+  if (ctx_bytes < C.total || ws_bytes < W.total) return SAGE_ERR_WORKSPACE;
+  sage_status st = check_arch();
+  if (st != SAGE_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int BH = (int)D.BH, N = (int)D.N, d = (int)D.d;
+  const auto* qb = static_cast<const __nv_bfloat16*>(q);
+  const auto* kb = static_cast<const __nv_bfloat16*>(k);
+  const auto* vb = static_cast<const __nv_bfloat16*>(v);
+  int8_t *q8 = at<int8_t>(ctx, C.q8), *k8 = at<int8_t>(ctx, C.k8), *v8 = at<int8_t>(ws, W.v8);
+  float *sq = at<float>(ctx, C.sq), *sk = at<float>(ctx, C.sk), *sv = at<float>(ws, W.sv);
+  float* muk = at<float>(ctx, C.muk);
+  float* muq = D.qs ? at<float>(ctx, C.muq) : nullptr;
+  float* bias = D.qs ? at<float>(ctx, C.bias) : nullptr;
+  double* partk = at<double>(ws, W.partk);
+  double* partq = D.qs ? at<double>(ws, W.partq) : nullptr;
+
+  FwdArgs a{};
+  const uint64_t rows = D.BH * D.N;
+  if (!make_tmap_2d(&a.tm_q, q8, false, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_k, k8, false, rows, d, kBlk, d) ||
+      !make_tmap_2d(&a.tm_v, v8, false, rows, d, kBlk, d))
+    return cuda_fail(cudaErrorInvalidValue);
+
+  cudaError_t e = cudaSuccess;
+  // K0: smoothing statistics
+  if (D.ks) {
+    if ((e = launch_colsum(kb, partk, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = launch_colmean(partk, muk, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+  }
+  if (D.qs) {
+    if ((e = launch_colsum(qb, partq, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = launch_blockmean(partq, muq, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+  }
+  // K1: per-block psi (Alg. 1 line 3)
+  if ((e = launch_quantize(qb, muq, D.qs ? 2 : 0, q8, sq, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+  if ((e = launch_quantize(kb, muk, D.ks ? 1 : 0, k8, sk, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+  if ((e = launch_quantize(vb, nullptr, 0, v8, sv, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+  // mu_K is all-zero when K-smoothing is off (ctx is caller memory: make it so)
+  if (!D.ks && (e = launch_fill(muk, D.BH * D.d, 0.f, s)) != cudaSuccess) return cuda_fail(e);
+  if (D.qs && (e = launch_qsmooth_bias(kb, muk, muq, bias, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+  // K2: fused INT8 forward (Alg. 1 lines 4-14)
+  a.q_scale = sq;
+  a.k_scale = sk;
+  a.v_scale = sv;
+  a.bias = bias;
+  a.o = static_cast<__nv_bfloat16*>(o);
+  a.lse = lse;
+  a.BH = BH;
+  a.N = N;
+  a.d = d;
+  a.tau = D.tau;
+  a.causal = D.causal;
+  a.qsmooth = D.qs;
+  if ((e = timed(0, s, [&] { return launch_fwd(a, s); })) != cudaSuccess) return cuda_fail(e);
+  if (g_prof.on) g_prof.launches += (D.ks ? 2 : 1) + (D.qs ? 3 : 0) + 3 + 1;
+  return SAGE_OK;
+}
+
+sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const float* lse, const void* dO,
+                     const void* ctx, size_t ctx_bytes, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
+                     void* stream) {
+  Dims D;
+  if (!dims_of(p, &D) || !v || !o || !lse || !dO || !ctx || !dq || !dk || !dv || !ws) return SAGE_ERR_INVALID_VALUE;
+  if (!aligned16(v) || !aligned16(o) || !aligned16(lse) || !aligned16(dO) || !aligned16(ctx) || !aligned16(dq) ||
+      !aligned16(dk) || !aligned16(dv) || !aligned16(ws))
+    return SAGE_ERR_MISALIGNED;
+  const CtxLayout C = ctx_layout(D);
+  const BwdWs W = bwd_ws(D);
+  if (ctx_bytes < C.total || ws_bytes < W.total) return SAGE_ERR_WORKSPACE;
+  sage_status st = check_arch();
+  if (st != SAGE_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int BH = (int)D.BH, N = (int)D.N, d = (int)D.d;
+  void* cx = const_cast<void*>(ctx);
+  int8_t *q8 = at<int8_t>(cx, C.q8), *k8 = at<int8_t>(cx, C.k8), *do8 = at<int8_t>(ws, W.do8);
+  float *sq = at<float>(cx, C.sq), *sk = at<float>(cx, C.sk), *sdo = at<float>(ws, W.sdo);
+  float *delta = at<float>(ws, W.delta), *l2 = at<float>(ws, W.l2), *dqacc = at<float>(ws, W.dq);
+
+  BwdArgs a{};
+  const uint64_t rows = D.BH * D.N;
+  if (!make_tmap_2d(&a.tm_q, q8, false, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_k, k8, false, rows, d, kBlk, d) ||
+      !make_tmap_2d(&a.tm_doq, do8, false, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_v, v, true, rows, d, kBlk, 64) ||
+      !make_tmap_2d(&a.tm_do, dO, true, rows, d, kBlk, 64))
+    return cuda_fail(cudaErrorInvalidValue);
+  cudaError_t e;
+  // K3: delta, psi(dO), L*log2(e), zero dQ accumulator (Alg. 2 lines 2, 6)
+  if ((e = launch_bwd_prep(static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dO), lse, delta,
+                           l2, do8, sdo, dqacc, BH, N, d, s)) != cudaSuccess)
+    return cuda_fail(e);
+  // K4: fused INT8 backward (Alg. 2 lines 3-11)
+  a.q_scale = sq;
+  a.k_scale = sk;
+  a.do_scale = sdo;
+  a.l2 = l2;
+  a.delta = delta;
+  a.bias = D.qs ? at<float>(cx, C.bias) : nullptr;
+  a.mu_q = D.qs ? at<float>(cx, C.muq) : nullptr;
+  a.dq_acc = dqacc;
+  a.dk = static_cast<__nv_bfloat16*>(dk);
+  a.dv = static_cast<__nv_bfloat16*>(dv);
+  a.BH = BH;
+  a.N = N;
+  a.d = d;
+  a.tau = D.tau;
+  a.causal = D.causal;
+  a.qsmooth = D.qs;
+  if ((e = timed(1, s, [&] { return launch_bwd(a, s); })) != cudaSuccess) return cuda_fail(e);
+  if (g_prof.on) g_prof.launches += 3;
+  // K5
+  if ((e = launch_dq_finalize(dqacc, static_cast<__nv_bfloat16*>(dq), D.BH * D.N * D.d, s)) != cudaSuccess)
+    return cuda_fail(e);
+  return SAGE_OK;
+}
+
+sage_status sage_debug_umma(int mode, int K, int N, const void* a, const void* b, void* d, void* stream) {
+  if (mode < 0 || mode > 3 || !a || !b || !d) return SAGE_ERR_INVALID_VALUE;
+  if ((mode == 0 || mode == 3) && K != 64 && K != 128) return SAGE_ERR_INVALID_VALUE;
+  if ((mode == 1 || mode == 2) && N != 64 && N != 128) return SAGE_ERR_INVALID_VALUE;
+  if (!aligned16(a) || !aligned16(b) || !aligned16(d)) return SAGE_ERR_MISALIGNED;
+  sage_status st = check_arch();
+  if (st != SAGE_OK) return st;
+  CUtensorMap ta{}, tb{};
+  bool ok = true;
+  if (mode == 0) {
+    ok = make_tmap_2d(&ta, a, false, 128, K, 128, K) && make_tmap_2d(&tb, b, false, 128, K, 128, K);
+  } else if (mode == 3) {
+    ok = make_tmap_2d(&ta, a, true, 128, K, 128, 64) && make_tmap_2d(&tb, b, true, 128, K, 128, 64);
+  } else {
+    ok = make_tmap_2d(&tb, b, false, 128, N, 128, N);
+    ta = tb;
+  }
+  if (!ok) return cuda_fail(cudaErrorInvalidValue);
+  cudaError_t e = launch_debug_umma(mode, K, N, &ta, &tb, a, d, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SAGE_OK : cuda_fail(e);
+}
+
+}  // extern "C"

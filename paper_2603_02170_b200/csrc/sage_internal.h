@@ -1,0 +1,71 @@
+// sage_internal.h -- host-side declarations shared by the libsage translation units.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace sage {
+
+constexpr int kBlk = 128;  // B_q = B_kv = 128 (reading A5): tcgen05 M = 128 tiles
+
+// ---- memory-bound passes (sage_prep.cu) ----
+// K0: per-(head, 128-row chunk) column sums in double, fixed order (reading A17).
+cudaError_t launch_colsum(const __nv_bfloat16* x, double* part, int BH, int N, int d, cudaStream_t s);
+// K0b: mu[bh][c] = fl32(sum_t part[bh][t][c] / N)  (mu_K).
+cudaError_t launch_colmean(const double* part, float* mu, int BH, int N, int d, cudaStream_t s);
+// K0c: mu_Q[bh][t][c] = fl32(part[bh][t][c] / 128)  (block-wise mu_Qi).
+cudaError_t launch_blockmean(const double* part, float* mu_q, int BH, int N, int d, cudaStream_t s);
+// K1: per-block psi of x - mu (mu per column: mu_mode 0 none, 1 per head [BH][d], 2 per block [BH][T][d]).
+cudaError_t launch_quantize(const __nv_bfloat16* x, const float* mu, int mu_mode, int8_t* xq, float* scale, int BH,
+                            int N, int d, cudaStream_t s);
+// Q-smoothing bias_i[n] = mu_Qi . (K[n] - mu_K)  (reading A13), fp32.
+cudaError_t launch_qsmooth_bias(const __nv_bfloat16* k, const float* mu_k, const float* mu_q, float* bias, int BH,
+                                int N, int d, cudaStream_t s);
+// K3: delta = rowsum(dO o O) (Alg. 2 line 2), psi(dO) (line 6, reading A22), l2 = lse*log2(e),
+//     dq_acc = 0.
+cudaError_t launch_bwd_prep(const __nv_bfloat16* o, const __nv_bfloat16* dO, const float* lse, float* delta,
+                            float* l2, int8_t* do_q, float* do_scale, float* dq_acc, int BH, int N, int d,
+                            cudaStream_t s);
+cudaError_t launch_fill(float* x, size_t n, float v, cudaStream_t s);
+// K5: dQ fp32 -> bf16.
+cudaError_t launch_dq_finalize(const float* dq_acc, __nv_bfloat16* dq, size_t n, cudaStream_t s);
+
+// ---- fused tensor-core kernels ----
+struct FwdArgs {
+  CUtensorMap tm_q, tm_k, tm_v;  // int8 [BH*N][d], box [128][d]
+  const float *q_scale, *k_scale, *v_scale;
+  const float* bias;  // [BH][T][N] or null
+  __nv_bfloat16* o;
+  float* lse;
+  int BH, N, d;
+  float tau;
+  bool causal, qsmooth;
+};
+cudaError_t launch_fwd(const FwdArgs& a, cudaStream_t s);
+
+struct BwdArgs {
+  CUtensorMap tm_q, tm_k, tm_doq;  // int8 [BH*N][d], box [128][d]
+  CUtensorMap tm_v, tm_do;         // bf16 [BH*N][d], box [128][64]
+  const float *q_scale, *k_scale, *do_scale;
+  const float *l2, *delta;         // [BH][N]
+  const float* bias;               // [BH][T][N] or null
+  const float* mu_q;               // [BH][T][d] or null
+  float* dq_acc;                   // [BH][N][d]
+  __nv_bfloat16 *dk, *dv;
+  int BH, N, d;
+  float tau;
+  bool causal, qsmooth;
+};
+cudaError_t launch_bwd(const BwdArgs& a, cudaStream_t s);
+
+// UMMA tile test (sage_debug_umma)
+cudaError_t launch_debug_umma(int mode, int K, int N, const CUtensorMap* tma, const CUtensorMap* tmb,
+                              const void* a, void* d, cudaStream_t s);
+
+// Tensor-map helpers (sage_api.cu)
+bool make_tmap_2d(CUtensorMap* m, const void* base, bool bf16, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                  uint32_t box_cols);
+
+}  // namespace sage

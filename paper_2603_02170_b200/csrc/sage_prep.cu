@@ -1,0 +1,311 @@
+// sage_prep.cu -- the HBM-bound passes around the fused kernels:
+//   K0  smoothing statistics mu_K, mu_Q   (fixed-order fp64 sums, reading A17)
+//   K1  per-block INT8 psi of Q(-mu_Q), K-mu_K, V  (Alg. 1 line 3)
+//   Q-smoothing bias mu_Qi . K_sm^T       (reading A13)
+//   K3  backward prep: delta, psi(dO), L*log2(e), zero dQ accumulator  (Alg. 2 lines 2, 6)
+//   K5  dQ fp32 -> bf16
+// Built without --use_fast_math; every FP32 op that decides a bit-exact INT8 value
+// is an explicit round-to-nearest intrinsic (__fsub_rn, __fmul_rn, __fdiv_rn) so
+// nvcc cannot contract it (reading A4).
+#include "sage_internal.h"
+
+namespace sage {
+namespace {
+
+constexpr int kVec = 8;  // bf16 elements per 16-byte vector
+
+__device__ __forceinline__ void load_bf16x8(const __nv_bfloat16* p, float (&f)[8]) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    float2 t = __bfloat1622float2(h[e]);
+    f[2 * e] = t.x;
+    f[2 * e + 1] = t.y;
+  }
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ---------------------------------------------------------------- K0: column sums
+// part[bh][t][c] = sum_{r=0..127} x[bh][128t + r][c], sequential in r, in double (A17).
+// One thread owns 8 consecutive columns of one chunk; 16-byte loads.
+__global__ void colsum_kernel(const __nv_bfloat16* __restrict__ x, double* __restrict__ part, int N, int d,
+                              int n_items) {
+  int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= n_items) return;
+  int groups = d / kVec;
+  int g = item % groups;
+  long long chunk = item / groups;  // = bh * T + t
+  const __nv_bfloat16* p = x + chunk * kBlk * d + g * kVec;
+  double acc[kVec];
+#pragma unroll
+  for (int e = 0; e < kVec; ++e) acc[e] = 0.0;
+#pragma unroll 4
+  for (int r = 0; r < kBlk; ++r) {
+    float f[kVec];
+    load_bf16x8(p + (size_t)r * d, f);
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) acc[e] += (double)f[e];
+  }
+  double* out = part + chunk * d + g * kVec;
+#pragma unroll
+  for (int e = 0; e < kVec; ++e) out[e] = acc[e];
+}
+
+// mu[bh][c] = fl32((sum over chunks, sequential in t) / N)
+__global__ void colmean_kernel(const double* __restrict__ part, float* __restrict__ mu, int N, int d, int BH) {
+  int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= BH * d) return;
+  int bh = item / d, c = item % d, T = N / kBlk;
+  const double* p = part + (size_t)bh * T * d + c;
+  double total = 0.0;
+  for (int t = 0; t < T; ++t) total += p[(size_t)t * d];
+  mu[item] = __double2float_rn(total / (double)N);
+}
+
+__global__ void blockmean_kernel(const double* __restrict__ part, float* __restrict__ mu_q, size_t n) {
+  size_t item = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= n) return;
+  mu_q[item] = __double2float_rn(part[item] / (double)kBlk);
+}
+
+// ---------------------------------------------------------------- K1: psi
+// One CTA quantises one 128 x d block: x_sm = fl32(x - mu); amax; scale = fl32(amax/127);
+// inv = fl32(127/amax) (0 for an all-zero block, A3); q = clamp(RNE(fl32(x_sm*inv)), +-127).
+template <int D>
+__global__ void __launch_bounds__(256) quantize_kernel(const __nv_bfloat16* __restrict__ x,
+                                                       const float* __restrict__ mu, int mu_mode,
+                                                       int8_t* __restrict__ xq, float* __restrict__ scale, int T) {
+  constexpr int kPerThread = kBlk * D / 256;      // 64 (D=128) or 32 (D=64)
+  constexpr int kIters = kPerThread / kVec;       // 8 or 4
+  constexpr int kGroups = D / kVec;               // 16 or 8 column groups per row
+  constexpr int kRowsPerPass = 256 / kGroups;     // 16 or 32
+  __shared__ float red[8];
+  const long long blk = blockIdx.x;               // bh * T + t
+  const int bh = (int)(blk / T), t = (int)(blk % T);
+  const int g = threadIdx.x % kGroups, r0 = threadIdx.x / kGroups;
+  const __nv_bfloat16* xb = x + blk * kBlk * D;
+  float m[kVec];
+#pragma unroll
+  for (int e = 0; e < kVec; ++e) {
+    int c = g * kVec + e;
+    m[e] = mu_mode == 0 ? 0.f : (mu_mode == 1 ? mu[(size_t)bh * D + c] : mu[((size_t)bh * T + t) * D + c]);
+  }
+  float v[kIters][kVec];
+  float amax = 0.f;
+#pragma unroll
+  for (int it = 0; it < kIters; ++it) {
+    int r = r0 + it * kRowsPerPass;
+    load_bf16x8(xb + (size_t)r * D + g * kVec, v[it]);
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) {
+      v[it][e] = __fsub_rn(v[it][e], m[e]);
+      amax = fmaxf(amax, fabsf(v[it][e]));
+    }
+  }
+  amax = warp_max(amax);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  amax = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) amax = fmaxf(amax, red[w]);
+  const float sc = __fdiv_rn(amax, 127.f);
+  const float inv = amax > 0.f ? __fdiv_rn(127.f, amax) : 0.f;
+  if (threadIdx.x == 0) scale[blk] = sc;
+  int8_t* qb = xq + blk * kBlk * D;
+#pragma unroll
+  for (int it = 0; it < kIters; ++it) {
+    int r = r0 + it * kRowsPerPass;
+    uint32_t w[2] = {0u, 0u};
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) {
+      int qv = __float2int_rn(__fmul_rn(v[it][e], inv));
+      qv = max(-127, min(127, qv));
+      w[e / 4] |= (uint32_t)(qv & 0xFF) << (8 * (e % 4));
+    }
+    *reinterpret_cast<uint2*>(qb + (size_t)r * D + g * kVec) = make_uint2(w[0], w[1]);
+  }
+}
+
+// ---------------------------------------------------------------- Q-smoothing bias
+// bias[bh][i][n] = sum_c mu_Q[bh][i][c] * fl32(K[n][c] - mu_K[c]), fp32 in fixed c order.
+// One CTA per (bh, 128-key block); K_sm staged in smem (padded rows).
+template <int D>
+__global__ void __launch_bounds__(128) qsmooth_bias_kernel(const __nv_bfloat16* __restrict__ k,
+                                                           const float* __restrict__ mu_k,
+                                                           const float* __restrict__ mu_q, float* __restrict__ bias,
+                                                           int N) {
+  extern __shared__ float sm[];
+  float* ks = sm;                      // [128][D+1]
+  float* mq = sm + kBlk * (D + 1);     // [D]
+  const int T = N / kBlk;
+  const long long blk = blockIdx.x;    // bh * T + jn
+  const int bh = (int)(blk / T), jn = (int)(blk % T);
+  const __nv_bfloat16* kb = k + blk * kBlk * D;
+  for (int e = threadIdx.x; e < kBlk * D; e += blockDim.x) {
+    int r = e / D, c = e % D;
+    ks[r * (D + 1) + c] = __fsub_rn(__bfloat162float(kb[e]), mu_k[(size_t)bh * D + c]);
+  }
+  __syncthreads();
+  const int n = threadIdx.x;
+  for (int i = 0; i < T; ++i) {
+    for (int c = threadIdx.x; c < D; c += blockDim.x) mq[c] = mu_q[((size_t)bh * T + i) * D + c];
+    __syncthreads();
+    float acc = 0.f;
+#pragma unroll 8
+    for (int c = 0; c < D; ++c) acc = fmaf(mq[c], ks[n * (D + 1) + c], acc);
+    bias[((size_t)bh * T + i) * N + (size_t)jn * kBlk + n] = acc;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- K3: backward prep
+template <int D>
+__global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
+                                                       const __nv_bfloat16* __restrict__ dO,
+                                                       const float* __restrict__ lse, float* __restrict__ delta,
+                                                       float* __restrict__ l2, int8_t* __restrict__ do_q,
+                                                       float* __restrict__ do_scale, float* __restrict__ dq_acc) {
+  constexpr int kGroups = D / kVec;            // threads per row
+  constexpr int kRowsPerPass = 256 / kGroups;
+  constexpr int kIters = kBlk / kRowsPerPass;
+  __shared__ float red[8];
+  const long long blk = blockIdx.x;
+  const int g = threadIdx.x % kGroups, r0 = threadIdx.x / kGroups;
+  const size_t base = (size_t)blk * kBlk * D;
+  float v[kIters][kVec];
+  float amax = 0.f;
+#pragma unroll
+  for (int it = 0; it < kIters; ++it) {
+    const int r = r0 + it * kRowsPerPass;
+    const size_t off = base + (size_t)r * D + g * kVec;
+    float fo[kVec];
+    load_bf16x8(dO + off, v[it]);
+    load_bf16x8(o + off, fo);
+    float dot = 0.f;
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) {
+      dot = fmaf(v[it][e], fo[e], dot);
+      amax = fmaxf(amax, fabsf(v[it][e]));
+    }
+#pragma unroll
+    for (int s = kGroups / 2; s; s >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, s);
+    if (g == 0) {
+      const size_t row = (size_t)blk * kBlk + r;
+      delta[row] = dot;
+      l2[row] = lse[row] * 1.4426950408889634f;
+    }
+    *reinterpret_cast<float4*>(dq_acc + off) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(dq_acc + off + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  amax = warp_max(amax);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  amax = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) amax = fmaxf(amax, red[w]);
+  const float sc = __fdiv_rn(amax, 127.f);
+  const float inv = amax > 0.f ? __fdiv_rn(127.f, amax) : 0.f;
+  if (threadIdx.x == 0) do_scale[blk] = sc;
+#pragma unroll
+  for (int it = 0; it < kIters; ++it) {
+    const int r = r0 + it * kRowsPerPass;
+    uint32_t w[2] = {0u, 0u};
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) {
+      int qv = __float2int_rn(__fmul_rn(v[it][e], inv));
+      qv = max(-127, min(127, qv));
+      w[e / 4] |= (uint32_t)(qv & 0xFF) << (8 * (e % 4));
+    }
+    *reinterpret_cast<uint2*>(do_q + base + (size_t)r * D + g * kVec) = make_uint2(w[0], w[1]);
+  }
+}
+
+__global__ void fill_kernel(float* __restrict__ x, size_t n, float v) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = v;
+}
+
+__global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq, size_t n8) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n8) return;
+  float4 a = reinterpret_cast<const float4*>(acc)[2 * i];
+  float4 b = reinterpret_cast<const float4*>(acc)[2 * i + 1];
+  __nv_bfloat162 h[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
+                         __floats2bfloat162_rn(b.x, b.y), __floats2bfloat162_rn(b.z, b.w)};
+  reinterpret_cast<uint4*>(dq)[i] = *reinterpret_cast<uint4*>(h);
+}
+
+}  // namespace
+
+cudaError_t launch_colsum(const __nv_bfloat16* x, double* part, int BH, int N, int d, cudaStream_t s) {
+  int n_items = BH * (N / kBlk) * (d / kVec);
+  colsum_kernel<<<(n_items + 127) / 128, 128, 0, s>>>(x, part, N, d, n_items);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colmean(const double* part, float* mu, int BH, int N, int d, cudaStream_t s) {
+  int n = BH * d;
+  colmean_kernel<<<(n + 127) / 128, 128, 0, s>>>(part, mu, N, d, BH);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blockmean(const double* part, float* mu_q, int BH, int N, int d, cudaStream_t s) {
+  size_t n = (size_t)BH * (N / kBlk) * d;
+  blockmean_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(part, mu_q, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quantize(const __nv_bfloat16* x, const float* mu, int mu_mode, int8_t* xq, float* scale, int BH,
+                            int N, int d, cudaStream_t s) {
+  int T = N / kBlk;
+  unsigned grid = (unsigned)(BH * T);
+  if (d == 128)
+    quantize_kernel<128><<<grid, 256, 0, s>>>(x, mu, mu_mode, xq, scale, T);
+  else
+    quantize_kernel<64><<<grid, 256, 0, s>>>(x, mu, mu_mode, xq, scale, T);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_qsmooth_bias(const __nv_bfloat16* k, const float* mu_k, const float* mu_q, float* bias, int BH,
+                                int N, int d, cudaStream_t s) {
+  unsigned grid = (unsigned)(BH * (N / kBlk));
+  size_t smem = (size_t)(kBlk * (d + 1) + d) * sizeof(float);
+  if (d == 128) {
+    cudaFuncSetAttribute(qsmooth_bias_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    qsmooth_bias_kernel<128><<<grid, 128, smem, s>>>(k, mu_k, mu_q, bias, N);
+  } else {
+    cudaFuncSetAttribute(qsmooth_bias_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    qsmooth_bias_kernel<64><<<grid, 128, smem, s>>>(k, mu_k, mu_q, bias, N);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_prep(const __nv_bfloat16* o, const __nv_bfloat16* dO, const float* lse, float* delta,
+                            float* l2, int8_t* do_q, float* do_scale, float* dq_acc, int BH, int N, int d,
+                            cudaStream_t s) {
+  unsigned grid = (unsigned)(BH * (N / kBlk));
+  if (d == 128)
+    bwd_prep_kernel<128><<<grid, 256, 0, s>>>(o, dO, lse, delta, l2, do_q, do_scale, dq_acc);
+  else
+    bwd_prep_kernel<64><<<grid, 256, 0, s>>>(o, dO, lse, delta, l2, do_q, do_scale, dq_acc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(float* x, size_t n, float v, cudaStream_t s) {
+  fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, n, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dq_finalize(const float* dq_acc, __nv_bfloat16* dq, size_t n, cudaStream_t s) {
+  size_t n8 = n / 8;
+  dq_finalize_kernel<<<(unsigned)((n8 + 255) / 256), 256, 0, s>>>(dq_acc, dq, n8);
+  return cudaGetLastError();
+}
+
+}  // namespace sage

@@ -1,0 +1,89 @@
+"""The C-ABI library loads, exports every symbol include/sage.h declares, and rejects bad
+arguments before launching anything (runs without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2603_02170_b200 import build, sage
+    build.build()
+    return sage.lib()
+
+
+def test_exports_match_header(L):
+    from paper_2603_02170_b200 import sage
+    hdr = open(os.path.join(ROOT, "include", "sage.h")).read()
+    declared = set(re.findall(r"SAGE_API\s+[\w\s\*]+?\b(sage_\w+)\s*\(", hdr))
+    assert declared == set(sage.SYMBOLS)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.sage_version() == 1
+    assert L.sage_status_string(4) == b"SAGE_ERR_WORKSPACE"
+
+
+def test_sizes_and_invalid_params(L):
+    from paper_2603_02170_b200.sage import make_params
+    p = make_params(2, 3, 256, 64, causal=True)
+    nctx = L.sage_ctx_bytes(ctypes.byref(p))
+    # q_i8 + k_i8 + 2 scale arrays + mu_K, 256-byte aligned
+    assert nctx >= 2 * 2 * 3 * 256 * 64 + 2 * 2 * 3 * 2 * 4 + 2 * 3 * 64 * 4
+    pq = make_params(2, 3, 256, 64, q_smooth=True)
+    assert L.sage_ctx_bytes(ctypes.byref(pq)) > nctx  # + mu_Q and the bias
+    assert L.sage_workspace_bytes(ctypes.byref(p), 1) >= 2 * 3 * 256 * 64 * 4  # fp32 dQ accumulator
+    for bad in (make_params(1, 1, 100, 64), make_params(1, 1, 128, 96), make_params(0, 1, 128, 64),
+                make_params(1, 1, 128, 64, softmax_scale=-1.0)):
+        assert L.sage_ctx_bytes(ctypes.byref(bad)) == 0
+        assert L.sage_workspace_bytes(ctypes.byref(bad), 0) == 0
+    bad = make_params(1, 1, 128, 64)
+    bad.flags = 1 << 7
+    assert L.sage_ctx_bytes(ctypes.byref(bad)) == 0
+
+
+def test_error_paths_do_not_launch(L):
+    """Validation happens before any device access: fake (never dereferenced) pointers."""
+    from paper_2603_02170_b200.sage import make_params
+    p = make_params(1, 2, 256, 64)
+    nctx = L.sage_ctx_bytes(ctypes.byref(p))
+    nws = L.sage_workspace_bytes(ctypes.byref(p), 0)
+    A = ctypes.c_void_p(0x10000)
+    mis = ctypes.c_void_p(0x10008)
+    z = ctypes.c_void_p(0)
+    S = ctypes.c_size_t
+    bad = make_params(1, 2, 200, 64)
+    assert L.sage_fwd(ctypes.byref(bad), A, A, A, A, A, A, S(nctx), A, S(nws), z) == 1
+    assert L.sage_fwd(ctypes.byref(p), z, A, A, A, A, A, S(nctx), A, S(nws), z) == 1
+    assert L.sage_fwd(ctypes.byref(p), mis, A, A, A, A, A, S(nctx), A, S(nws), z) == 3
+    assert L.sage_fwd(ctypes.byref(p), A, A, A, A, A, A, S(nctx - 1), A, S(nws), z) == 4
+    assert L.sage_fwd(ctypes.byref(p), A, A, A, A, A, A, S(nctx), A, S(nws - 1), z) == 4
+    nwb = L.sage_workspace_bytes(ctypes.byref(p), 1)
+    assert L.sage_bwd(ctypes.byref(p), A, A, A, A, A, S(nctx), A, A, A, A, S(nwb - 1), z) == 4
+    assert L.sage_bwd(ctypes.byref(p), A, A, A, A, A, S(nctx), A, A, mis, A, S(nwb), z) == 3
+    assert L.sage_debug_umma(7, 64, 128, A, A, A, z) == 1
+    assert L.sage_debug_umma(1, 128, 96, A, A, A, z) == 1
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_gpu_no_fallback(L):
+    """Valid arguments on a machine without an sm_100 device: an error status, never a CPU result."""
+    from paper_2603_02170_b200.sage import make_params
+    p = make_params(1, 2, 256, 64)
+    A = ctypes.c_void_p(0x10000)
+    S = ctypes.c_size_t
+    st = L.sage_fwd(ctypes.byref(p), A, A, A, A, A, A, S(1 << 30), A, S(1 << 30), ctypes.c_void_p(0))
+    assert st in (5, 6)  # SAGE_ERR_CUDA / SAGE_ERR_ARCH
+
+
+def test_product_does_not_import_oracle():
+    """The product package never references oracle/ (the oracle is test infrastructure)."""
+    pkg = os.path.join(ROOT, "paper_2603_02170_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src and "liboracle" not in src, f

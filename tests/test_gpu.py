@@ -1,0 +1,209 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Tier A (bit-exact): mu_K, mu_Q, Q^, K^, V^, dO^ and their fp32 scales.
+Tier B (bit-exact): int32 UMMA tiles for every operand configuration the kernels use.
+Outputs O, dQ, dK, dV: rel-L2 <= 2e-3 and cos >= 0.9999 against the quantised oracle,
+both sides rounded to bf16 (BASELINE.json north_star tolerance; reading A18).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2603_02170_b200 import sage
+from paper_2603_02170_b200.inputs import CONFIGS, make_inputs
+from tests.metrics import cos_sim, f64, rel_l2, round_bf16
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL, COS_TOL = 2e-3, 0.9999
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    assert torch.cuda.is_available(), "gpu tests need an sm_100 device"
+    assert torch.cuda.get_device_capability() == (10, 0), torch.cuda.get_device_capability()
+    sage.lib()
+    oracle.build()
+
+
+def _run(q, k, v, do, causal, k_smooth, q_smooth):
+    dev = "cuda"
+    qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
+    o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth)
+    dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
+    torch.cuda.synchronize()
+    return dict(o=o, lse=lse, dq=dq, dk=dk, dv=dv, ctx=ctx)
+
+
+def _oracle(q, k, v, do, heads, causal, k_smooth, q_smooth):
+    """Oracle on the selected flattened heads; O is stored as bf16 before the backward (A15)."""
+    B, H, N, d = q.shape
+    sel = lambda t: f64(t).reshape(B * H, N, d)[heads]
+    qn, kn, vn, don = map(sel, (q, k, v, do))
+    kw = dict(causal=causal, k_smooth=k_smooth, q_smooth=q_smooth)
+    f = oracle.fwd(qn, kn, vn, **kw)
+    o_st = round_bf16(f["o"])
+    b = oracle.bwd(qn, kn, vn, o_st, don, f["lse"], **kw)
+    return f, b
+
+
+def _compare(gpu, f, b, heads, B, H, N, d):
+    flat = lambda t: f64(t).reshape(B * H, N, d)[heads]
+    res = {}
+    for name, ref in (("o", f["o"]), ("dq", b["dq"]), ("dk", b["dk"]), ("dv", b["dv"])):
+        got = flat(gpu[name])
+        ref = round_bf16(ref)
+        res[name] = (rel_l2(ref, got), cos_sim(ref, got))
+    lse = f64(gpu["lse"]).reshape(B * H, N)[heads]
+    res["lse"] = float(np.abs(lse - f["lse"]).max())
+    return res
+
+
+def _assert_ok(res, what):
+    for name in ("o", "dq", "dk", "dv"):
+        rl, cs = res[name]
+        assert rl <= REL_TOL and cs >= COS_TOL, (what, name, rl, cs, res)
+    assert res["lse"] <= 1e-4, (what, res)
+
+
+# ------------------------------------------------------------------ Tier B: UMMA tiles
+@pytest.mark.parametrize("K", [64, 128])
+def test_umma_s_tile_kmajor(K):
+    g = torch.Generator().manual_seed(K)
+    a = torch.randint(-127, 128, (128, K), generator=g, dtype=torch.int8)
+    b = torch.randint(-127, 128, (128, K), generator=g, dtype=torch.int8)
+    d = sage.debug_umma(0, a.cuda(), b.cuda()).cpu().numpy()
+    np.testing.assert_array_equal(d, a.numpy().astype(np.int64) @ b.numpy().astype(np.int64).T)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("N", [64, 128])
+def test_umma_mn_major(mode, N):
+    g = torch.Generator().manual_seed(10 * mode + N)
+    lo = 0 if mode == 1 else -127          # mode 1 is the P^ path (values in [0, 127])
+    a = torch.randint(lo, 128, (128, 128), generator=g, dtype=torch.int8)
+    b = torch.randint(-127, 128, (128, N), generator=g, dtype=torch.int8)
+    d = sage.debug_umma(mode, a.cuda(), b.cuda()).cpu().numpy()
+    A = a.numpy().astype(np.int64)
+    if mode == 2:                           # a holds A^T ([K][M], the dS^^T tile)
+        A = A.T
+    np.testing.assert_array_equal(d, A @ b.numpy().astype(np.int64))
+
+
+@pytest.mark.parametrize("K", [64, 128])
+def test_umma_bf16_dp_tile(K):
+    g = torch.Generator().manual_seed(K + 1)
+    a = torch.randn(128, K, generator=g).to(torch.bfloat16)
+    b = torch.randn(128, K, generator=g).to(torch.bfloat16)
+    d = sage.debug_umma(3, a.cuda(), b.cuda()).cpu().numpy()
+    ref = f64(a) @ f64(b).T
+    assert np.abs(d - ref).max() <= 1e-4 * np.abs(ref).max()
+
+
+# ------------------------------------------------------------------ Tier A: quantised inputs
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("q_smooth", [False, True])
+def test_tier_a_bit_exact(d, q_smooth):
+    B, H, N = 1, 2, 384
+    q, k, v, do = make_inputs(B, H, N, d, "outlier_kq", seed=21 + d)
+    gpu = _run(q, k, v, do, True, True, q_smooth)
+    view = gpu["ctx"].view()
+    f, b = _oracle(q, k, v, do, list(range(B * H)), True, True, q_smooth)
+    T = N // 128
+    np.testing.assert_array_equal(view["mu_k"].cpu().numpy().reshape(B * H, d), f["mu_k"])
+    np.testing.assert_array_equal(view["q_i8"].cpu().numpy().reshape(B * H, N, d), f["q8"])
+    np.testing.assert_array_equal(view["k_i8"].cpu().numpy().reshape(B * H, N, d), f["k8"])
+    np.testing.assert_array_equal(view["q_scale"].cpu().numpy().reshape(B * H, T), f["sq"])
+    np.testing.assert_array_equal(view["k_scale"].cpu().numpy().reshape(B * H, T), f["sk"])
+    if q_smooth:
+        np.testing.assert_array_equal(view["mu_q"].cpu().numpy().reshape(B * H, T, d), f["mu_q"])
+        bias = view["bias"].cpu().numpy().reshape(B * H, T, N).astype(np.float64)
+        assert np.abs(bias - f["bias"]).max() <= 1e-5 * np.abs(f["bias"]).max()
+    # V^ and dO^ live in the workspaces
+    p = gpu["ctx"].params
+    wsf = sage._ws.get(p, False, torch.device("cuda"))
+    wv = sage.ws_view(p, False, wsf)
+    base = wsf.data_ptr()
+    v8 = wsf[wv.v_i8 - base: wv.v_i8 - base + B * H * N * d].view(torch.int8).cpu().numpy()
+    sv = wsf[wv.v_scale - base: wv.v_scale - base + B * H * T * 4].view(torch.float32).cpu().numpy()
+    np.testing.assert_array_equal(v8.reshape(B * H, N, d), f["v8"])
+    np.testing.assert_array_equal(sv.reshape(B * H, T), f["sv"])
+    wsb = sage._ws.get(p, True, torch.device("cuda"))
+    wb = sage.ws_view(p, True, wsb)
+    base = wsb.data_ptr()
+    do8 = wsb[wb.do_i8 - base: wb.do_i8 - base + B * H * N * d].view(torch.int8).cpu().numpy()
+    sdo = wsb[wb.do_scale - base: wb.do_scale - base + B * H * T * 4].view(torch.float32).cpu().numpy()
+    np.testing.assert_array_equal(do8.reshape(B * H, N, d), b["do8"])
+    np.testing.assert_array_equal(sdo.reshape(B * H, T), b["sdo"])
+    delta = wsb[wb.delta - base: wb.delta - base + B * H * N * 4].view(torch.float32).cpu().numpy()
+    # delta from the GPU's own bf16 O; the oracle's from its own O: compare loosely
+    assert rel_l2(b["delta"], delta.reshape(B * H, N)) < 1e-2
+
+
+# ------------------------------------------------------------------ fused fwd + bwd parity
+SMALL = [
+    # (B, H, N, d, causal, k_smooth, q_smooth, recipe)
+    (1, 2, 128, 64, True, True, False, "outlier_k"),      # C1 (BASELINE.json configs[0])
+    (1, 2, 128, 64, True, True, False, "gauss"),
+    (1, 2, 256, 64, False, True, False, "qknorm"),
+    (1, 2, 384, 64, True, True, False, "qknorm"),
+    (1, 2, 512, 128, True, True, False, "qknorm"),
+    (1, 2, 384, 128, False, True, False, "outlier_k"),
+    (1, 2, 384, 128, True, False, False, "gauss"),
+    (1, 2, 512, 64, True, True, True, "outlier_kq"),
+    (1, 2, 384, 128, True, True, True, "outlier_kq"),
+    (2, 1, 256, 128, False, True, True, "outlier_kq"),
+]
+
+
+@pytest.mark.parametrize("B,H,N,d,causal,ks,qs,recipe", SMALL)
+def test_fwd_bwd_parity_small(B, H, N, d, causal, ks, qs, recipe):
+    q, k, v, do = make_inputs(B, H, N, d, recipe, seed=100 + N + d)
+    gpu = _run(q, k, v, do, causal, ks, qs)
+    heads = list(range(B * H))
+    f, b = _oracle(q, k, v, do, heads, causal, ks, qs)
+    _assert_ok(_compare(gpu, f, b, heads, B, H, N, d), (B, H, N, d, causal, ks, qs, recipe))
+
+
+def test_zero_do_gives_zero_grads():
+    """dO = 0: every dS tile is all-zero, scale 0 (reading A3) -> exact zeros."""
+    q, k, v, do = make_inputs(1, 2, 256, 64, "gauss", seed=5)
+    gpu = _run(q, k, v, torch.zeros_like(do), True, True, False)
+    for name in ("dq", "dk", "dv"):
+        assert torch.count_nonzero(gpu[name]).item() == 0
+
+
+def test_autograd_function():
+    q, k, v, do = (t.cuda() for t in make_inputs(1, 2, 256, 64, "qknorm", seed=6))
+    q.requires_grad_(True)
+    k.requires_grad_(True)
+    v.requires_grad_(True)
+    o = sage.sage_attention(q, k, v, causal=True)
+    o.backward(do)
+    o2, lse, ctx = sage.forward(q.detach(), k.detach(), v.detach(), causal=True)
+    dq, dk, dv = sage.backward(ctx, v.detach(), o2, lse, do)
+    assert torch.equal(o, o2)
+    for g1, g2 in ((q.grad, dq), (k.grad, dk), (v.grad, dv)):
+        assert rel_l2(f64(g2), f64(g1)) < 1e-3  # dQ reduction order differs run to run
+
+
+# ------------------------------------------------------------------ full BASELINE sizes, sampled heads
+@pytest.mark.parametrize("cfg,heads", [("C2", [0, 77, 127]), ("C3", [5, 126])])
+def test_full_size_sampled_heads(cfg, heads):
+    c = CONFIGS[cfg]
+    q, k, v, do = make_inputs(c.batch, c.heads, c.seqlen, c.head_dim, c.recipe, seed=c.seed)
+    gpu = _run(q, k, v, do, c.causal, c.k_smooth, c.q_smooth)
+    oracle.set_threads(max(1, len(heads)))
+    f, b = _oracle(q, k, v, do, heads, c.causal, c.k_smooth, c.q_smooth)
+    _assert_ok(_compare(gpu, f, b, heads, c.batch, c.heads, c.seqlen, c.head_dim), cfg)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,heads", [("C5", [3]), ("C4", [40])])
+def test_full_size_long_sampled_head(cfg, heads):
+    c = CONFIGS[cfg]
+    q, k, v, do = make_inputs(c.batch, c.heads, c.seqlen, c.head_dim, c.recipe, seed=c.seed)
+    gpu = _run(q, k, v, do, c.causal, c.k_smooth, c.q_smooth)
+    f, b = _oracle(q, k, v, do, heads, c.causal, c.k_smooth, c.q_smooth)
+    _assert_ok(_compare(gpu, f, b, heads, c.batch, c.heads, c.seqlen, c.head_dim), cfg)
