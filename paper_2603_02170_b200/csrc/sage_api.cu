@@ -3,6 +3,8 @@
 // encoding and the kernel launch sequence of sage_fwd (K0, K1, [bias], K2) and
 // sage_bwd (K3, K4, K5).  No device memory is allocated here.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <utility>
@@ -16,10 +18,13 @@ namespace {
 
 thread_local int g_last_cuda_error = 0;
 
-sage_status cuda_fail(cudaError_t e) {
+sage_status cuda_fail_at(cudaError_t e, int line) {
   g_last_cuda_error = (int)e;
+  if (std::getenv("SAGE_DEBUG"))
+    std::fprintf(stderr, "[libsage] cuda error %d (%s) at sage_api.cu:%d\n", (int)e, cudaGetErrorString(e), line);
   return SAGE_ERR_CUDA;
 }
+#define cuda_fail(e) cuda_fail_at((e), __LINE__)
 
 // ---- cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
