@@ -281,8 +281,10 @@ def main():
     if dist is not None:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     nbytes = sum(h.numel() * h.element_size() for h in host)
-    e2e = {"value": ops_of(c) * world / (float(te.item()) * 1e-3) / 1e12, "unit": "TOPS",
-           "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
+    e2e = None
+    if e2e_ms:
+        e2e = {"value": ops_of(c) * world / (float(te.item()) * 1e-3) / 1e12, "unit": "TOPS",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
 
     if rank == 0:
         pk = peaks()

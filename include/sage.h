@@ -117,6 +117,10 @@ SAGE_API sage_status sage_ws_get_view(const sage_params* p, int backward, void* 
  * a, b, d: device pointers to row-major host-order arrays as described (int8/bf16 in, int32/fp32 out). */
 SAGE_API sage_status sage_debug_umma(int mode, int K, int N, const void* a, const void* b, void* d, void* stream);
 
+/* Profiling only: copy the K4 pipeline timeline (clock64 stamps of 16 events x 64 tiles x 4 CTAs,
+ * uint64, recorded when the environment variable SAGE_ABLATE has bit 8 set) to host memory. */
+SAGE_API sage_status sage_debug_trace(void* host_out, size_t bytes);
+
 /* Optional instrumentation (calling thread only).  While enabled, sage_fwd / sage_bwd record
  * a CUDA event pair around their fused kernel (K2 / K4) and count every kernel they launch.
  * sage_profile_read synchronises on the recorded events, returns the summed K2 and K4 device

@@ -51,6 +51,9 @@ sage_status check_arch() {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e);
+  // Bind the device's primary context to this thread (e.g. torch's autograd worker thread):
+  // cuTensorMapEncodeTiled needs a current context.
+  if ((e = cudaSetDevice(dev)) != cudaSuccess) return cuda_fail(e);
   int major = 0, minor = 0;
   if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
@@ -71,7 +74,7 @@ bool dims_of(const sage_params* p, Dims* o) {
   if (!p) return false;
   if (p->batch <= 0 || p->heads <= 0 || p->seqlen <= 0) return false;
   if (p->head_dim != 64 && p->head_dim != 128) return false;
-  if (p->seqlen % kBlk) return false;
+  if (p->seqlen % kBlk || p->seqlen > kMaxSeqLen) return false;
   if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH)) return false;
   if (!(p->softmax_scale >= 0.f) || std::isinf(p->softmax_scale)) return false;
   const size_t BH = (size_t)p->batch * p->heads;
@@ -167,6 +170,15 @@ cudaError_t timed(int which, cudaStream_t s, F&& fn) {
   return e;
 }
 
+// Profiling-only ablation switch for K4 (SAGE_ABLATE=<bits>), read once; 0 in normal use.
+int ablate_flags() {
+  static int v = [] {
+    const char* e = std::getenv("SAGE_ABLATE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <typename T>
 T* at(void* base, size_t off) {
   return reinterpret_cast<T*>(static_cast<uint8_t*>(base) + off);
@@ -190,6 +202,9 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, bool bf16, uint64_t rows, ui
   CUresult r = enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && std::getenv("SAGE_DEBUG"))
+    std::fprintf(stderr, "[libsage] cuTensorMapEncodeTiled -> %d (base %p rows %llu cols %llu box %u x %u)\n", (int)r,
+                 base, (unsigned long long)rows, (unsigned long long)cols, box_rows, box_cols);
   return r == CUDA_SUCCESS;
 }
 
@@ -405,12 +420,19 @@ sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const f
   a.tau = D.tau;
   a.causal = D.causal;
   a.qsmooth = D.qs;
+  a.ablate = ablate_flags();
   if ((e = timed(1, s, [&] { return launch_bwd(a, s); })) != cudaSuccess) return cuda_fail(e);
   if (g_prof.on) g_prof.launches += 3;
   // K5
   if ((e = launch_dq_finalize(dqacc, static_cast<__nv_bfloat16*>(dq), D.BH * D.N * D.d, s)) != cudaSuccess)
     return cuda_fail(e);
   return SAGE_OK;
+}
+
+sage_status sage_debug_trace(void* host_out, size_t bytes) {
+  if (!host_out) return SAGE_ERR_INVALID_VALUE;
+  cudaError_t e = read_bwd_trace(host_out, bytes);
+  return e == cudaSuccess ? SAGE_OK : cuda_fail(e);
 }
 
 sage_status sage_debug_umma(int mode, int K, int N, const void* a, const void* b, void* d, void* stream) {

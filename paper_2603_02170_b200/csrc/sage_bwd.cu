@@ -3,30 +3,43 @@
 // order: j outer, i inner).  Everything is computed transposed so that
 // TMEM lanes are key rows:
 //   S^T   = MM(K^_j, Q^_i)          kind::i8   A K^_j K-major, B Q^_i K-major     (line 5)
-//   P     = exp(S - L_i);  psi(P) over the 128x128 tile (reading A11)               (line 5-6)
+//   P     = exp(S - L_i);  psi(P) over the 128x128 tile (reading A11)               (lines 5-6)
 //   dP^T  = V_j dO_i^T               kind::f16  bf16 operands, fp32 accumulation     (line 8)
 //   dS    = P o (dP - D_i);  psi(dS) over the tile                                   (line 9)
 //   dV_j += MM(P^^T, dO^_i) s_P s_dO    A P^^T smem K-major, B dO^_i MN-major        (line 7)
 //   dK_j += MM(dS^^T, Q^_i) s_dS s_Q tau  (+ tau s_dS colsum(dS^) mu_Qi)  (line 11)
 //   dQ_i += MM(dS^, K^_j) s_dS s_K tau    A dS^ (the dS^^T tile read MN-major), B K^_j MN-major (line 10)
-// dV_j, dK_j accumulate in fp32 registers (the per-tile scales forbid int32
-// accumulation across tiles); dQ_i is reduced across key blocks with fp32
-// red.global.add into a [B,H,N,d] accumulator (finalised to bf16 by K5).
-// Roles: warps 0-3 / 4-7 = two compute warpgroups (query columns 0-63 / 64-127 of
-// each tile, and d columns [0,d/2) / [d/2,d) of every drain), warp 8 = TMA
-// producer, warp 9 = TMEM allocator + MMA issuer.
+//
+// Warp roles (512 threads, register budgets re-balanced with setmaxnreg):
+//   warp 0        TMA producer: K^_j, V_j once; per i a stage {Q^_i, dO_i, dO^_i, L_i, delta_i}
+//   warp 1        TMEM allocator + MMA issuer (one thread)
+//   warps 4-11    two compute warpgroups, query columns [0,64) / [64,128) of every tile.
+//                 Single pass: S^T and dP^T are read from TMEM once into a 64-float register
+//                 tile (t -> P -> dS in place), so their TMEM columns free up immediately and
+//                 the next tile's MMAs overlap this tile's softmax / quantisation.
+//   warps 12-15   drain warpgroup: the per-tile scales forbid int32 accumulation across
+//                 tiles, so every dV/dK/dQ int32 tile is converted and scaled here while the
+//                 compute warpgroups already work on the next tile.  dK_j (and dV_j for d=64)
+//                 accumulate in fp32 registers; for d=128 dV_j accumulates in fp32 TMEM.
+//                 dQ_i is reduced across key blocks with fp32 red.global.add (finalised by K5).
+// TMEM (512 columns):  d=64 : S 0 | dP 128 | dV 256 | dK 320 | dQ 384
+//                      d=128: S/dV 0 | dP/dK 128 | dQ 256 | dV fp32 accumulator 384
+//   (d=128 aliases the dV tile onto S and the dK tile onto dP; the MMA issuer orders them.)
 #include "sage_internal.h"
 #include "sm100.cuh"
 
 namespace sage {
 namespace {
 
-constexpr int kThreads = 320;
-constexpr int kStages = 2;
+constexpr int kThreads = 512;
+constexpr int kComputeWarps = 8;
+constexpr int kDrainWarps = 4;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kMaxT = kMaxSeqLen / kBlk;
 
 template <int D>
 struct BwdSmem {
+  static constexpr int kStages = D == 64 ? 3 : 2;
   static constexpr int kTile = kBlk * D;           // int8 [128][D]
   static constexpr int kK = 0;                     // K^_j
   static constexpr int kV = kK + kTile;            // V_j bf16: D/64 panels of [128][64]
@@ -35,15 +48,28 @@ struct BwdSmem {
   static constexpr int kStageBytes = 4 * kTile + 1024;
   static constexpr int kPt = kStage + kStages * kStageBytes;  // P^^T [128 kv][128 q]
   static constexpr int kDSt = kPt + kBlk * kBlk;              // dS^^T [128 kv][128 q]
-  static constexpr int kRed = kDSt + kBlk * kBlk;             // 2 x 8 floats
-  static constexpr int kRowSum = kRed + 64;                   // [2][128] int
-  static constexpr int kBar = kRowSum + 2 * kBlk * 4;
-  static constexpr int kNumBars = 1 + 2 * kStages + 10;
+  static constexpr int kRed = kDSt + kBlk * kBlk;             // [2][8] floats (cross-warp max)
+  static constexpr int kScl = kRed + 64;                      // [4][2] floats {s_P, s_dS} per tile slot
+  static constexpr int kRowSum = kScl + 32;                   // [2 slots][2 wg][128] int (Q-smoothing colsum of dS^)
+  static constexpr int kScQ = kRowSum + 4 * kBlk * 4;          // s_Q[bh][0..T), s_dO[bh][0..T) (T <= kMaxT)
+  static constexpr int kScDO = kScQ + kMaxT * 4;
+  static constexpr int kBar = kScDO + kMaxT * 4;
+  static constexpr int kNumBars = 1 + 2 * kStages + 8;
   static constexpr int kTmemSlot = kBar + kNumBars * 8;
   static constexpr int kBytes = kTmemSlot + 16;
   static constexpr int kAlloc = kBytes + 1024;
   static constexpr uint32_t kStageTx = 4 * kTile + 1024;
 };
+
+// Profiling-only timeline (SAGE_ABLATE bit 8): clock64 stamps of pipeline events for the
+// first kTrCtas CTAs, read back with sage_debug_trace().  One predicated branch per event.
+constexpr int kTrCtas = 4, kTrTiles = 64, kTrEvents = 24;
+__device__ unsigned long long g_trace[kTrCtas * kTrTiles * kTrEvents];
+#define TR(ev, it)                                                                  \
+  do {                                                                              \
+    if ((ablate & 8) && blockIdx.x < kTrCtas && (it) < kTrTiles)                    \
+      g_trace[(blockIdx.x * kTrTiles + (it)) * kTrEvents + (ev)] = clock64();       \
+  } while (0)
 
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
@@ -51,15 +77,15 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-// max over the 256 compute threads (warps 0-7), named barrier 1
-__device__ __forceinline__ float block_max256(float v, float* red, int warp) {
+// max over the 256 compute threads (warps 4-11), named barrier `id`
+__device__ __forceinline__ float compute_max(float v, float* red, int cw, int id) {
   v = warp_max(v);
-  if ((threadIdx.x & 31) == 0) red[warp] = v;
-  named_bar_sync(1, 256);
-  float r = red[0];
-#pragma unroll
-  for (int w = 1; w < 8; ++w) r = fmaxf(r, red[w]);
-  return r;
+  if ((threadIdx.x & 31) == 0) red[cw] = v;
+  named_bar_sync(id, 256);
+  float r = fmax3(red[0], red[1], red[2]);
+  r = fmax3(r, red[3], red[4]);
+  r = fmax3(r, red[5], red[6]);
+  return fmaxf(r, red[7]);
 }
 
 template <int D, bool CAUSAL, bool QSMOOTH>
@@ -70,33 +96,44 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* __restrict__ k_scale, const float* __restrict__ do_scale,
                     const float* __restrict__ l2g, const float* __restrict__ deltag, const float* __restrict__ bias,
                     const float* __restrict__ mu_q, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dk,
-                    __nv_bfloat16* __restrict__ dv, int N, int BH, float tau) {
+                    __nv_bfloat16* __restrict__ dv, int N, int BH, float tau, int ablate) {
   using L = BwdSmem<D>;
+  constexpr int kStages = L::kStages;
+  constexpr bool kAlias = D == 128;
+  // setmaxnreg budgets (x128 threads each; sum = 512 regs/thread-slot = the 64K register file)
+  constexpr uint32_t kRegProducer = 56, kRegCompute = D == 64 ? 136 : 128, kRegDrain = D == 64 ? 184 : 200;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* kv_full = bars;
-  uint64_t* q_full = bars + 1;              // [kStages]
-  uint64_t* q_empty = q_full + kStages;     // [kStages]
-  uint64_t* s_full = q_empty + kStages;
-  uint64_t* dp_full = s_full + 1;
-  uint64_t* dv_full = s_full + 2;
-  uint64_t* dk_full = s_full + 3;
-  uint64_t* dq_full = s_full + 4;
-  uint64_t* s_free = s_full + 5;            // 256 arrivals each
-  uint64_t* dp_free = s_full + 6;
-  uint64_t* ds_ready = s_full + 7;
-  uint64_t* dk_free = s_full + 8;
-  uint64_t* dq_free = s_full + 9;
+  uint64_t* q_full = bars + 1;             // [kStages]
+  uint64_t* q_empty = q_full + kStages;    // [kStages]
+  uint64_t* b0 = q_empty + kStages;
+  // MMA -> compute / drain (tcgen05.commit).  dv_full also tells the compute warps that P^^T
+  // may be overwritten, dkq_full that dS^^T may be; each completes once per tile and no waiter
+  // can fall a full phase behind (checked per wait below), so one barrier serves both.
+  uint64_t* s_full = b0 + 0;
+  uint64_t* dp_full = b0 + 1;
+  uint64_t* dv_full = b0 + 2;
+  uint64_t* dkq_full = b0 + 3;
+  uint64_t* p_ready = b0 + 4;      // compute -> MMA (8 warps): P^^T written, S^T read
+  uint64_t* ds_ready = b0 + 5;     // compute -> MMA (8 warps): dS^^T written, dP^T read
+  uint64_t* dv_drained = b0 + 6;   // drain -> MMA (4 warps)
+  uint64_t* dkq_drained = b0 + 7;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
   float* red = reinterpret_cast<float*>(smem + L::kRed);
+  float* scl = reinterpret_cast<float*>(smem + L::kScl);
+  float* sc_q = reinterpret_cast<float*>(smem + L::kScQ);
+  float* sc_do = reinterpret_cast<float*>(smem + L::kScDO);
   int* rowsum_s = reinterpret_cast<int*>(smem + L::kRowSum);
 
   const int T = N / kBlk;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tile = blockIdx.x;
-  const int j = tile / BH;  // causal: low j has the most query blocks -> scheduled first
-  const int bh = tile % BH;
+  // head-major order: the T CTAs of one head run together and share its Q^/dO/dO^ tiles and
+  // its dQ accumulator through L2; within a head, low j (most query blocks when causal) first.
+  const int bh = tile / T;
+  const int j = tile % T;
   const int i0 = CAUSAL ? j : 0;
   const int n_it = T - i0;
   const int krow = bh * N + j * kBlk;
@@ -107,296 +144,483 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(q_full + s, 1);
       mbar_init(q_empty + s, 1);
     }
-    for (int b = 0; b < 5; ++b) mbar_init(s_full + b, 1);
-    for (int b = 5; b < 10; ++b) mbar_init(s_full + b, 256);
+    for (int b = 0; b < 4; ++b) mbar_init(b0 + b, 1);
+    for (int b = 4; b < 6; ++b) mbar_init(b0 + b, kComputeWarps);
+    for (int b = 6; b < 8; ++b) mbar_init(b0 + b, kDrainWarps);
     fence_mbar_init();
   }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  for (int t = threadIdx.x; t < T; t += kThreads) {
+    sc_q[t] = q_scale[(size_t)bh * T + t];
+    sc_do[t] = do_scale[(size_t)bh * T + t];
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem;         // S^T   cols [0,128)   int32  (lanes = key rows)
-  const uint32_t tDP = tmem + 128;  // dP^T  cols [128,256) fp32 -> dS fp32 -> dV tile int32 [0,D)
-  const uint32_t tDK = tmem + 256;  // dK tile int32 [0,D)
-  const uint32_t tDQ = tmem + 384;  // dQ tile int32 [0,D)  (lanes = query rows)
+  const uint32_t tS = tmem;
+  const uint32_t tDP = tmem + 128;
+  const uint32_t tDV = kAlias ? tmem : tmem + 256;
+  const uint32_t tDK = kAlias ? tmem + 128 : tmem + 256 + D;
+  const uint32_t tDQ = kAlias ? tmem + 256 : tmem + 256 + 2 * D;
+  const uint32_t tDVacc = tmem + 384;  // d=128 only
 
-  if (warp == 8) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_doq);
-      tma_prefetch(&tm_v);
-      tma_prefetch(&tm_do);
-      mbar_expect_tx(kv_full, 3 * L::kTile);
-      tma_load_2d(smem + L::kK, &tm_k, kv_full, 0, krow);
+  if (warp < 4) {
+    reg_dealloc<kRegProducer>();
+    if (warp == 0) {
+      // ---------------------------------------------------------- TMA producer (one elected lane)
+      if (elect_one()) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_doq);
+        tma_prefetch(&tm_v);
+        tma_prefetch(&tm_do);
+        mbar_expect_tx(kv_full, 3 * L::kTile);
+        tma_load_2d(smem + L::kK, &tm_k, kv_full, 0, krow);
 #pragma unroll
-      for (int p = 0; p < D / 64; ++p) tma_load_2d(smem + L::kV + p * 16384, &tm_v, kv_full, p * 64, krow);
+        for (int p = 0; p < D / 64; ++p) tma_load_2d(smem + L::kV + p * 16384, &tm_v, kv_full, p * 64, krow);
+      }
+      __syncwarp();
       for (int it = 0; it < n_it; ++it) {
         const int s = it % kStages, i = i0 + it;
         const int qrow = bh * N + i * kBlk;
         uint8_t* st = smem + L::kStage + s * L::kStageBytes;
         mbar_wait(q_empty + s, ((it / kStages) & 1) ^ 1);
-        mbar_expect_tx(q_full + s, L::kStageTx);
-        tma_load_2d(st + L::kSQ, &tm_q, q_full + s, 0, qrow);
+        if (elect_one()) {
+          TR(14, it);
+          mbar_expect_tx(q_full + s, L::kStageTx);
+          tma_load_2d(st + L::kSQ, &tm_q, q_full + s, 0, qrow);
 #pragma unroll
-        for (int p = 0; p < D / 64; ++p) tma_load_2d(st + L::kSDO + p * 16384, &tm_do, q_full + s, p * 64, qrow);
-        tma_load_2d(st + L::kSDOQ, &tm_doq, q_full + s, 0, qrow);
-        bulk_load(st + L::kSL, l2g + qrow, 512, q_full + s);
-        bulk_load(st + L::kSDelta, deltag + qrow, 512, q_full + s);
+          for (int p = 0; p < D / 64; ++p) tma_load_2d(st + L::kSDO + p * 16384, &tm_do, q_full + s, p * 64, qrow);
+          tma_load_2d(st + L::kSDOQ, &tm_doq, q_full + s, 0, qrow);
+          bulk_load(st + L::kSL, l2g + qrow, 512, q_full + s);
+          bulk_load(st + L::kSDelta, deltag + qrow, 512, q_full + s);
+        }
+        __syncwarp();
       }
-    }
-  } else if (warp == 9) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    } else if (warp == 1) {
+      // ---------------------------------------------------------- MMA issuer (whole warp, one elected lane issues)
       constexpr uint32_t kIdS = idesc_i8(128, 128, false, false);     // S^T
       constexpr uint32_t kIdDP = idesc_bf16(128, 128, false, false);  // dP^T
       constexpr uint32_t kIdDV = idesc_i8(128, D, false, true);       // dV, dK (B MN-major)
       constexpr uint32_t kIdDQ = idesc_i8(128, D, true, true);        // dQ (A, B MN-major)
+      // smem operand addresses; descriptors are formed at issue time (cheap uniform-datapath ALU)
+      const uint32_t st0 = smem_u32(smem + L::kStage);
       const uint32_t k_addr = smem_u32(smem + L::kK);
       const uint32_t v_addr = smem_u32(smem + L::kV);
       const uint32_t pt_addr = smem_u32(smem + L::kPt);
       const uint32_t dst_addr = smem_u32(smem + L::kDSt);
-      auto stage_addr = [&](int it) { return smem_u32(smem + L::kStage + (it % kStages) * L::kStageBytes); };
+      auto soff = [&](int it) { return (uint32_t)((it % kStages) * L::kStageBytes); };
       auto issue_s = [&](int it) {
         mbar_wait(q_full + it % kStages, (it / kStages) & 1);
         tc_fence_after();
-        const uint32_t q_addr = stage_addr(it) + L::kSQ;
+        if (elect_one()) {
+          TR(22, it);
+          const uint32_t q_addr = st0 + soff(it) + L::kSQ;
 #pragma unroll
-        for (int kk = 0; kk < D / 32; ++kk)
-          mma_i8(tS, desc_kmajor(k_addr, D, kk * 32), desc_kmajor(q_addr, D, kk * 32), kIdS, kk > 0);
-        mma_commit(s_full);
-      };
-      auto issue_dp = [&](int it) {
-        const uint32_t do_addr = stage_addr(it) + L::kSDO;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t po = (kk / 4) * 16384, ko = (kk % 4) * 32;
-          mma_bf16(tDP, desc_kmajor(v_addr + po, 128, ko), desc_kmajor(do_addr + po, 128, ko), kIdDP, kk > 0);
+          for (int kk = 0; kk < D / 32; ++kk)
+            mma_i8(tS, desc_kmajor(k_addr, D, kk * 32), desc_kmajor(q_addr, D, kk * 32), kIdS, kk > 0);
+          mma_commit(s_full);
+          TR(0, it);
         }
-        mma_commit(dp_full);
+        __syncwarp();
+      };
+      auto issue_dp = [&](int it) {  // stage `it` was already waited for by issue_s(it)
+        if (elect_one()) {
+          const uint32_t do_addr = st0 + soff(it) + L::kSDO;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * 16384 + (kk % 4) * 32;
+            mma_bf16(tDP, desc_kmajor(v_addr + off, 128, 0), desc_kmajor(do_addr + off, 128, 0), kIdDP, kk > 0);
+          }
+          mma_commit(dp_full);
+          TR(2, it);
+        }
+        __syncwarp();
+      };
+      auto issue_dv = [&](int it) {
+        if (elect_one()) {
+          const uint32_t doq_addr = st0 + soff(it) + L::kSDOQ;
+#pragma unroll
+          for (int kk = 0; kk < kBlk / 32; ++kk)
+            mma_i8(tDV, desc_kmajor(pt_addr, 128, kk * 32), desc_mnmajor(doq_addr, D, kk * 32), kIdDV, kk > 0);
+          mma_commit(dv_full);
+          TR(1, it);
+        }
+        __syncwarp();
+      };
+      auto issue_dkdq = [&](int it) {
+        if (elect_one()) {
+          const uint32_t q_addr = st0 + soff(it) + L::kSQ;
+#pragma unroll
+          for (int kk = 0; kk < kBlk / 32; ++kk)
+            mma_i8(tDK, desc_kmajor(dst_addr, 128, kk * 32), desc_mnmajor(q_addr, D, kk * 32), kIdDV, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < kBlk / 32; ++kk)
+            mma_i8(tDQ, desc_mnmajor(dst_addr, 128, kk * 32), desc_mnmajor(k_addr, D, kk * 32), kIdDQ, kk > 0);
+          mma_commit(dkq_full);
+          mma_commit(q_empty + it % kStages);
+          TR(3, it);
+        }
+        __syncwarp();
       };
       mbar_wait(kv_full, 0);
       issue_s(0);
       issue_dp(0);
       for (int it = 0; it < n_it; ++it) {
-        const uint32_t ph = it & 1;
-        if (it + 1 < n_it) {
-          mbar_wait(s_free, ph);  // pass 2 of `it` has consumed S^T
-          issue_s(it + 1);
-        }
-        mbar_wait(ds_ready, ph);
-        mbar_wait(dk_free, ph ^ 1);
-        mbar_wait(dq_free, ph ^ 1);
-        tc_fence_after();
-        const uint32_t q_addr = stage_addr(it) + L::kSQ;
-        const uint32_t doq_addr = stage_addr(it) + L::kSDOQ;
-#pragma unroll
-        for (int kk = 0; kk < kBlk / 32; ++kk)
-          mma_i8(tDP, desc_kmajor(pt_addr, 128, kk * 32), desc_mnmajor(doq_addr, D, kk * 32), kIdDV, kk > 0);
-        mma_commit(dv_full);
-#pragma unroll
-        for (int kk = 0; kk < kBlk / 32; ++kk)
-          mma_i8(tDK, desc_kmajor(dst_addr, 128, kk * 32), desc_mnmajor(q_addr, D, kk * 32), kIdDV, kk > 0);
-        mma_commit(dk_full);
-#pragma unroll
-        for (int kk = 0; kk < kBlk / 32; ++kk)
-          mma_i8(tDQ, desc_mnmajor(dst_addr, 128, kk * 32), desc_mnmajor(k_addr, D, kk * 32), kIdDQ, kk > 0);
-        mma_commit(dq_full);
-        mma_commit(q_empty + it % kStages);
-        if (it + 1 < n_it) {
-          mbar_wait(dp_free, ph);  // dV tile of `it` drained out of the dP columns
+        const uint32_t ph = it & 1, pph = ph ^ 1;
+        const bool more = it + 1 < n_it;
+        if constexpr (!kAlias) {
+          // compute events per tile: p_ready (S^T, dP^T read; P^^T written) < ds_ready (dS^^T
+          // written).  S_{i+1} and dP_{i+1} ride behind dV_i.
+          mbar_wait(p_ready, ph);
+          if (it > 0) mbar_wait(dv_drained, pph);
+          if (lane == 0) TR(17, it);
           tc_fence_after();
-          issue_dp(it + 1);
+          issue_dv(it);
+          if (more) {
+            issue_s(it + 1);
+            issue_dp(it + 1);
+          }
+          mbar_wait(ds_ready, ph);
+          if (it > 0) mbar_wait(dkq_drained, pph);
+          if (lane == 0) TR(20, it);
+          tc_fence_after();
+          issue_dkdq(it);
+        } else {
+          // d=128: dV_i lands on S's columns, dK_i on dP's (both read by p_ready); S_{i+1} /
+          // dP_{i+1} wait until those tiles are drained.
+          mbar_wait(p_ready, ph);
+          tc_fence_after();
+          issue_dv(it);
+          if (more) {
+            mbar_wait(dv_drained, ph);
+            tc_fence_after();
+            issue_s(it + 1);
+          }
+          mbar_wait(ds_ready, ph);
+          if (it > 0) mbar_wait(dkq_drained, pph);
+          tc_fence_after();
+          issue_dkdq(it);
+          if (more) {
+            mbar_wait(dkq_drained, ph);
+            tc_fence_after();
+            issue_dp(it + 1);
+          }
         }
       }
     }
-  } else {
+  } else if (warp < 4 + kComputeWarps) {
+    reg_alloc<kRegCompute>();
     // ------------------------------------------------------------ compute warpgroups (256 threads)
-    const int wg = warp / 4;
-    const int r = (warp % 4) * 32 + lane;  // TMEM lane: key row (S, dP, dV, dK) or query row (dQ)
+    const int cw = warp - 4;                 // compute warp 0..7
+    const int wg = cw / 4;
+    const int r = (warp % 4) * 32 + lane;    // TMEM lane = key row of S^T / dP^T
     const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
-    const int qc0 = wg * 64;               // this warpgroup's query columns of the tile
-    constexpr int kHalf = D / 2;           // this warpgroup's d columns of every drain
-    const int dc0 = wg * kHalf;
+    const int qc0 = wg * 64;                 // this warpgroup's query columns of the tile
     const float tau2 = tau * kLog2e;
     const float sk = k_scale[(size_t)bh * T + j];
-    float dv_acc[kHalf], dk_acc[kHalf];
-#pragma unroll
-    for (int c = 0; c < kHalf; ++c) dv_acc[c] = dk_acc[c] = 0.f;
+    uint8_t* pt = smem + L::kPt;
+    uint8_t* dst = smem + L::kDSt;
 
     for (int it = 0; it < n_it; ++it) {
       const int i = i0 + it, s = it % kStages;
-      const uint32_t ph = it & 1;
+      const uint32_t ph = it & 1, pph = ph ^ 1;
       const uint8_t* st = smem + L::kStage + s * L::kStageBytes;
-      const float* Ls = reinterpret_cast<const float*>(st + L::kSL);
-      const float* Ds = reinterpret_cast<const float*>(st + L::kSDelta);
-      const float sq = q_scale[(size_t)bh * T + i];
-      const float sdo = do_scale[(size_t)bh * T + i];
-      const float c2 = sq * sk * tau2;
+      const float4* Ls4 = reinterpret_cast<const float4*>(st + L::kSL) + qc0 / 4;
+      const float4* Ds4 = reinterpret_cast<const float4*>(st + L::kSDelta) + qc0 / 4;
+      const float c2 = sc_q[i] * sk * tau2;  // int32 -> log2-domain logit
       const float b2 = QSMOOTH ? bias[((size_t)bh * T + i) * N + (size_t)j * kBlk + r] * tau2 : 0.f;
       const bool diag = CAUSAL && (i == j);
+      const bool cm = !(ablate & 2);
+      float t[64];
+#pragma unroll
+      for (int e = 0; e < 64; ++e) t[e] = 0.f;
+
+      // -- step 1: t = log2 P = S*c2 + b2 - L2[q]  (Alg. 2 line 5), tile max of t
       mbar_wait(q_full + s, (it / kStages) & 1);
       mbar_wait(s_full, ph);
       tc_fence_after();
-      // pass 1: max over the tile of t = log2 P = S*c2 + b2 - L2[q]
+      if (threadIdx.x == 128) TR(5, it);
       float tmax = -INFINITY;
-#pragma unroll 1
-      for (int cc = 0; cc < 64; cc += 32) {
+if (cm) {
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
         uint32_t v[32];
-        tmem_ld32(tS + qc0 + cc + lane_off, v);
+        tmem_ld32(tS + qc0 + cc * 32 + lane_off, v);
         tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int q = qc0 + cc + e;
-          const float t = fmaf(__int2float_rn((int)v[e]), c2, b2 - Ls[q]);
-          if (!diag || r <= q) tmax = fmaxf(tmax, t);
+        for (int e4 = 0; e4 < 8; ++e4) {
+          float4 l4 = Ls4[cc * 8 + e4];
+          float2 a = make_float2(__int2float_rn((int)v[4 * e4]), __int2float_rn((int)v[4 * e4 + 1]));
+          float2 b = make_float2(__int2float_rn((int)v[4 * e4 + 2]), __int2float_rn((int)v[4 * e4 + 3]));
+          float2 na = make_float2(-l4.x, -l4.y), nb = make_float2(-l4.z, -l4.w);
+          if constexpr (QSMOOTH) {
+            na = fadd2(na, make_float2(b2, b2));
+            nb = fadd2(nb, make_float2(b2, b2));
+          }
+          a = ffma2(a, make_float2(c2, c2), na);
+          b = ffma2(b, make_float2(c2, c2), nb);
+          const int e = cc * 32 + 4 * e4;
+          t[e] = a.x;
+          t[e + 1] = a.y;
+          t[e + 2] = b.x;
+          t[e + 3] = b.y;
         }
       }
-      const float amax_p = ex2(block_max256(tmax, red, warp));
+}
+      tc_fence_before();
+      if (diag) {  // causal: key r attends query q only if r <= q (reading A14)
+#pragma unroll
+        for (int e = 0; e < 64; ++e)
+          if (r > qc0 + e) t[e] = -INFINITY;
+      }
+#pragma unroll
+      for (int e = 0; e < 64; e += 4) tmax = fmaxf(tmax, fmax3(t[e], t[e + 1], fmaxf(t[e + 2], t[e + 3])));
+
+      // -- step 2: psi(P) scale over the tile: amax = max P = 2^max(t)  (line 6, reading A11)
+      const float amax_p = ex2(compute_max(tmax, red, cw, 1));
       const float inv_p = amax_p > 0.f ? __fdiv_rn(127.f, amax_p) : 0.f;
-      const float s_p = amax_p * (1.f / 127.f);
+      // tile scales for the drain warpgroup (4 slots: it cannot run 4 tiles ahead of the drain)
+      if (threadIdx.x == 128) scl[(it & 3) * 2] = __fdiv_rn(amax_p, 127.f);
+
+      // -- step 3: P = 2^t, P^ = RNE(P * inv) -> P^^T smem (A of dV, K-major);
+      //            dS = P o (dP - delta) (lines 8-9) in the same pass, tile max |dS|
+      if (it > 0) mbar_wait(dv_full, pph);  // dV_{i-1} has read P^^T (its commit = dv_full)
       mbar_wait(dp_full, ph);
       tc_fence_after();
-      // pass 2: P, psi(P) -> P^^T smem; dS = P (dP - delta) -> back into the dP columns
-      uint8_t* pt = smem + L::kPt;
+      if (threadIdx.x == 128) TR(15, it);
       float dsmax = 0.f;
-#pragma unroll 1
-      for (int cc = 0; cc < 64; cc += 16) {
-        uint32_t sv[16], dpv[16];
-        tmem_ld16(tS + qc0 + cc + lane_off, sv);
-        tmem_ld16(tDP + qc0 + cc + lane_off, dpv);
+if (cm) {
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tDP + qc0 + cc * 32 + lane_off, v);
         tmem_wait_ld();
-        uint32_t pk[4];
 #pragma unroll
-        for (int e4 = 0; e4 < 4; ++e4) {
-          uint32_t w = 0;
+        for (int c16 = 0; c16 < 2; ++c16) {
+          uint32_t w[4];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int e = e4 * 4 + t, q = qc0 + cc + e;
-            float p = ex2(fmaf(__int2float_rn((int)sv[e]), c2, b2 - Ls[q]));
-            if (diag && r > q) p = 0.f;
-            w |= rne_small(fminf(p * inv_p, 127.f)) << (8 * t);
-            const float ds = p * (__uint_as_float(dpv[e]) - Ds[q]);
-            dsmax = fmaxf(dsmax, fabsf(ds));
-            dpv[e] = __float_as_uint(ds);
+          for (int e4 = 0; e4 < 4; ++e4) {
+            const int ev = c16 * 16 + e4 * 4;  // index into v
+            const int e = cc * 32 + ev;        // index into t
+            const float4 d4 = Ds4[e / 4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) t[e + u] = ex2(t[e + u]);
+            float2 qa = ffma2(make_float2(t[e], t[e + 1]), make_float2(inv_p, inv_p), make_float2(kMagic, kMagic));
+            float2 qb = ffma2(make_float2(t[e + 2], t[e + 3]), make_float2(inv_p, inv_p), make_float2(kMagic, kMagic));
+            w[e4] = pack4_magic(qa.x, qa.y, qb.x, qb.y);
+            float2 a = fadd2(make_float2(__uint_as_float(v[ev]), __uint_as_float(v[ev + 1])), make_float2(-d4.x, -d4.y));
+            float2 b = fadd2(make_float2(__uint_as_float(v[ev + 2]), __uint_as_float(v[ev + 3])), make_float2(-d4.z, -d4.w));
+            a = fmul2(a, make_float2(t[e], t[e + 1]));
+            b = fmul2(b, make_float2(t[e + 2], t[e + 3]));
+            t[e] = a.x;
+            t[e + 1] = a.y;
+            t[e + 2] = b.x;
+            t[e + 3] = b.y;
+            dsmax = fmax3(dsmax, fabsf(a.x), fmax3(fabsf(a.y), fabsf(b.x), fabsf(b.y)));
           }
-          pk[e4] = w;
+          *reinterpret_cast<uint4*>(pt + sw_offset(r, (qc0 + cc * 32) / 16 + c16, 128)) =
+              make_uint4(w[0], w[1], w[2], w[3]);
         }
-        tmem_st16(tDP + qc0 + cc + lane_off, dpv);
-        *reinterpret_cast<uint4*>(pt + sw_offset(r, (qc0 + cc) / 16, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(s_free);
-      const float amax_ds = block_max256(dsmax, red + 8, warp);
-      const float inv_ds = amax_ds > 0.f ? __fdiv_rn(127.f, amax_ds) : 0.f;
-      const float s_ds = amax_ds * (1.f / 127.f);
-      // pass 3: psi(dS) -> dS^^T smem (K-major for dK, read MN-major for dQ)
-      uint8_t* dst = smem + L::kDSt;
-      int rsum = 0;
-#pragma unroll 1
-      for (int cc = 0; cc < 64; cc += 16) {
-        uint32_t dsv[16];
-        tmem_ld16(tDP + qc0 + cc + lane_off, dsv);
-        tmem_wait_ld();
-        uint32_t pk[4];
-#pragma unroll
-        for (int e4 = 0; e4 < 4; ++e4) {
-          uint32_t w = 0;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            float x = fminf(fmaxf(__uint_as_float(dsv[e4 * 4 + t]) * inv_ds, -127.f), 127.f);
-            const uint32_t qb = rne_small(x);
-            if (QSMOOTH) rsum += (int)(int8_t)(qb & 0xFF);
-            w |= (qb & 0xFFu) << (8 * t);
-          }
-          pk[e4] = w;
-        }
-        *reinterpret_cast<uint4*>(dst + sw_offset(r, (qc0 + cc) / 16, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-      }
-      if (QSMOOTH) rowsum_s[wg * kBlk + r] = rsum;
+}
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(ds_ready);
-      if (QSMOOTH) named_bar_sync(2, 256);
-      // drain dV tile: dV_j += tile * s_P * s_dO_i  (Alg. 2 line 7)
+      warp_arrive(p_ready);  // P^^T written; S^T and dP^T read (their TMEM columns may be reused)
+      if (threadIdx.x == 128) TR(6, it);
+
+      // -- step 5: psi(dS) scale over the tile
+      const float amax_ds = compute_max(dsmax, red + 8, cw, 2);
+      const float inv_ds = amax_ds > 0.f ? __fdiv_rn(127.f, amax_ds) : 0.f;
+      if (threadIdx.x == 128) scl[(it & 3) * 2 + 1] = __fdiv_rn(amax_ds, 127.f);
+
+      // -- step 6: dS^ = RNE(dS * inv) -> dS^^T smem (A of dK K-major, A of dQ MN-major)
+      if (it > 0) mbar_wait(dkq_full, pph);  // dK_{i-1}, dQ_{i-1} have read dS^^T
+      if (threadIdx.x == 128) TR(9, it);
+      int rsum = 0;
+if (cm) {
+#pragma unroll
+      for (int c16 = 0; c16 < 4; ++c16) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) {
+          const int e = c16 * 16 + e4 * 4;
+          float2 qa = ffma2(make_float2(t[e], t[e + 1]), make_float2(inv_ds, inv_ds), make_float2(kMagic, kMagic));
+          float2 qb = ffma2(make_float2(t[e + 2], t[e + 3]), make_float2(inv_ds, inv_ds), make_float2(kMagic, kMagic));
+          w[e4] = pack4_magic(qa.x, qa.y, qb.x, qb.y);
+          if constexpr (QSMOOTH) rsum = __dp4a((int)w[e4], 0x01010101, rsum);
+        }
+        *reinterpret_cast<uint4*>(dst + sw_offset(r, qc0 / 16 + c16, 128)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+}
+      if constexpr (QSMOOTH) rowsum_s[(it & 1) * kBlk * 2 + wg * kBlk + r] = rsum;
+      fence_proxy_async_smem();
+      tc_fence_before();
+      warp_arrive(ds_ready);
+      if (threadIdx.x == 128) TR(8, it);
+    }
+  } else {
+    reg_alloc<kRegDrain>();
+    // ------------------------------------------------------------ drain warpgroup (128 threads)
+    const int r = (warp % 4) * 32 + lane;  // TMEM lane: key row (dV, dK) or query row (dQ)
+    const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
+    const float sk = k_scale[(size_t)bh * T + j];
+    constexpr int kRegV = kAlias ? 1 : D;  // dV_j in registers (d=64) or in TMEM (d=128)
+    float dv_acc[kRegV];
+    float dk_acc[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) dk_acc[c] = 0.f;
+#pragma unroll
+    for (int c = 0; c < kRegV; ++c) dv_acc[c] = 0.f;
+
+    for (int it = 0; it < n_it; ++it) {
+      const int i = i0 + it;
+      const uint32_t ph = it & 1;
+      const float sq = sc_q[i];
+      const float sdo = sc_do[i];
+
+      // dV_j += tile * s_P * s_dO_i  (Alg. 2 line 7)
       mbar_wait(dv_full, ph);
       tc_fence_after();
-      {
-        const float f = s_p * sdo;
+      if (threadIdx.x == 384) TR(10, it);
+      if (!(ablate & 1)) {
+        const float s_p = scl[(it & 3) * 2];
+        const float2 f = make_float2(s_p * sdo, s_p * sdo);
+        if constexpr (kAlias) {
+          // fp32 accumulator in TMEM: 16-column chunks keep the drain within its register budget
 #pragma unroll
-        for (int c0 = 0; c0 < kHalf; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tDP + dc0 + c0 + lane_off, v);
-          tmem_wait_ld();
+          for (int c0 = 0; c0 < D; c0 += 16) {
+            uint32_t v[16], a[16];
+            tmem_ld16(tDV + c0 + lane_off, v);
+            tmem_ld16(tDVacc + c0 + lane_off, a);
+            tmem_wait_ld();
+            if (it == 0) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) dv_acc[c0 + e] = fmaf(__int2float_rn((int)v[e]), f, dv_acc[c0 + e]);
+              for (int e = 0; e < 16; ++e) a[e] = 0u;
+            }
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              float2 x = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f,
+                               make_float2(__uint_as_float(a[e]), __uint_as_float(a[e + 1])));
+              a[e] = __float_as_uint(x.x);
+              a[e + 1] = __float_as_uint(x.y);
+            }
+            tmem_st16(tDVacc + c0 + lane_off, a);
+          }
+        } else {
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tDV + c0 + lane_off, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              float2 x = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f,
+                               make_float2(dv_acc[c0 + e], dv_acc[c0 + e + 1]));
+              dv_acc[c0 + e] = x.x;
+              dv_acc[c0 + e + 1] = x.y;
+            }
+          }
         }
+        if constexpr (kAlias) tmem_wait_st();
       }
       tc_fence_before();
-      mbar_arrive(dp_free);
-      // drain dK tile: dK_j += tile * s_dS * s_Q * tau (+ Q-smoothing bias branch)  (line 11)
-      mbar_wait(dk_full, ph);
+      warp_arrive(dv_drained);
+
+      // dK_j += tile * s_dS * s_Q * tau (+ Q-smoothing bias branch)  (line 11)
+      mbar_wait(dkq_full, ph);
       tc_fence_after();
-      {
-        const float f = s_ds * sq * tau;
-        const float fb = QSMOOTH ? tau * s_ds * (float)(rowsum_s[r] + rowsum_s[kBlk + r]) : 0.f;
-        const float* muq = QSMOOTH ? mu_q + ((size_t)bh * T + i) * D + dc0 : nullptr;
+      if (threadIdx.x == 384) TR(11, it);
+      if (!(ablate & 1)) {
+        const float s_ds = scl[(it & 3) * 2 + 1];
+        const float2 f = make_float2(s_ds * sq * tau, s_ds * sq * tau);
+        float fb = 0.f;
+        const float* muq = nullptr;
+        if constexpr (QSMOOTH) {
+          const int* rs = rowsum_s + (it & 1) * kBlk * 2;
+          fb = tau * s_ds * (float)(rs[r] + rs[kBlk + r]);
+          muq = mu_q + ((size_t)bh * T + i) * D;
+        }
 #pragma unroll
-        for (int c0 = 0; c0 < kHalf; c0 += 32) {
+        for (int c0 = 0; c0 < D; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(tDK + dc0 + c0 + lane_off, v);
+          tmem_ld32(tDK + c0 + lane_off, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            float add = __int2float_rn((int)v[e]) * f;
-            if (QSMOOTH) add = fmaf(fb, muq[c0 + e], add);
-            dk_acc[c0 + e] += add;
+          for (int e = 0; e < 32; e += 2) {
+            float2 acc = make_float2(dk_acc[c0 + e], dk_acc[c0 + e + 1]);
+            if constexpr (QSMOOTH) {
+              const float2 m2 = *reinterpret_cast<const float2*>(muq + c0 + e);
+              acc = ffma2(make_float2(fb, fb), m2, acc);
+            }
+            float2 x = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f, acc);
+            dk_acc[c0 + e] = x.x;
+            dk_acc[c0 + e + 1] = x.y;
           }
         }
       }
       tc_fence_before();
-      mbar_arrive(dk_free);
-      // drain dQ tile: dQ_i += tile * s_dS * s_K * tau, fp32 reduction across key blocks (line 10)
-      mbar_wait(dq_full, ph);
-      tc_fence_after();
-      {
-        const float f = s_ds * sk * tau;
-        float* grow = dq_acc + ((size_t)bh * N + (size_t)i * kBlk + r) * D + dc0;
+
+      // dQ_i += tile * s_dS * s_K * tau, fp32 reduction across key blocks (line 10)
+      if (threadIdx.x == 384) TR(12, it);
+      if (!(ablate & 1)) {
+        const float s_ds = scl[(it & 3) * 2 + 1];
+        const float2 f = make_float2(s_ds * sk * tau, s_ds * sk * tau);
+        float* grow = dq_acc + ((size_t)bh * N + (size_t)i * kBlk + r) * D;
 #pragma unroll
-        for (int c0 = 0; c0 < kHalf; c0 += 32) {
+        for (int c0 = 0; c0 < D; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(tDQ + dc0 + c0 + lane_off, v);
+          tmem_ld32(tDQ + c0 + lane_off, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            red_add_v4(grow + c0 + e, __int2float_rn((int)v[e]) * f, __int2float_rn((int)v[e + 1]) * f,
-                       __int2float_rn((int)v[e + 2]) * f, __int2float_rn((int)v[e + 3]) * f);
+          for (int e = 0; e < 32; e += 4) {
+            float2 a = fmul2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f);
+            float2 b = fmul2(make_float2(__int2float_rn((int)v[e + 2]), __int2float_rn((int)v[e + 3])), f);
+            if (!(ablate & 4)) red_add_v4(grow + c0 + e, a.x, a.y, b.x, b.y);
+          }
         }
       }
       tc_fence_before();
-      mbar_arrive(dq_free);
+      warp_arrive(dkq_drained);
+      if (threadIdx.x == 384) TR(13, it);
     }
     // epilogue: dK_j, dV_j rows -> bf16
-    const size_t orow = ((size_t)krow + r) * D + dc0;
+    const size_t orow = ((size_t)krow + r) * D;
 #pragma unroll
-    for (int c0 = 0; c0 < kHalf; c0 += 8) {
-      __nv_bfloat162 hk[4], hv[4];
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      float vv[32];
+      if constexpr (kAlias) {
+        uint32_t a[16], b[16];
+        tmem_ld16(tDVacc + c0 + lane_off, a);
+        tmem_ld16(tDVacc + c0 + 16 + lane_off, b);
+        tmem_wait_ld();
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        hk[e] = __floats2bfloat162_rn(dk_acc[c0 + 2 * e], dk_acc[c0 + 2 * e + 1]);
-        hv[e] = __floats2bfloat162_rn(dv_acc[c0 + 2 * e], dv_acc[c0 + 2 * e + 1]);
+        for (int e = 0; e < 16; ++e) {
+          vv[e] = __uint_as_float(a[e]);
+          vv[16 + e] = __uint_as_float(b[e]);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) vv[e] = dv_acc[c0 + e];
       }
-      *reinterpret_cast<uint4*>(dk + orow + c0) = *reinterpret_cast<uint4*>(hk);
-      *reinterpret_cast<uint4*>(dv + orow + c0) = *reinterpret_cast<uint4*>(hv);
+#pragma unroll
+      for (int e8 = 0; e8 < 32; e8 += 8) {
+        __nv_bfloat162 hk[4], hv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          hk[e] = __floats2bfloat162_rn(dk_acc[c0 + e8 + 2 * e], dk_acc[c0 + e8 + 2 * e + 1]);
+          hv[e] = __floats2bfloat162_rn(vv[e8 + 2 * e], vv[e8 + 2 * e + 1]);
+        }
+        *reinterpret_cast<uint4*>(dk + orow + c0 + e8) = *reinterpret_cast<uint4*>(hk);
+        *reinterpret_cast<uint4*>(dv + orow + c0 + e8) = *reinterpret_cast<uint4*>(hv);
+      }
     }
   }
   __syncwarp();
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -410,11 +634,16 @@ cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
   const int T = a.N / kBlk;
   kern<<<a.BH * T, kThreads, BwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_doq, a.tm_v, a.tm_do, a.q_scale,
                                                        a.k_scale, a.do_scale, a.l2, a.delta, a.bias, a.mu_q,
-                                                       a.dq_acc, a.dk, a.dv, a.N, a.BH, a.tau);
+                                                       a.dq_acc, a.dk, a.dv, a.N, a.BH, a.tau, a.ablate);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+cudaError_t read_bwd_trace(void* host, size_t bytes) {
+  if (bytes > sizeof(g_trace)) bytes = sizeof(g_trace);
+  return cudaMemcpyFromSymbol(host, g_trace, bytes);
+}
 
 cudaError_t launch_bwd(const BwdArgs& a, cudaStream_t s) {
   if (a.d == 128) {

@@ -66,8 +66,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // Longest-first order for causal: high query blocks have the most kv tiles.
   const int tile = blockIdx.x;
-  const int i = CAUSAL ? (T - 1 - tile / BH) : (tile / BH);
-  const int bh = tile % BH;
+  // head-major order (the CTAs of one head share K^/V^ through L2); causal: longest (high i) first
+  const int bh = tile / T;
+  const int i = CAUSAL ? (T - 1 - tile % T) : (tile % T);
   const int nj = CAUSAL ? i + 1 : T;
   const int row0 = bh * N + i * kBlk;  // first global row of this q block
 

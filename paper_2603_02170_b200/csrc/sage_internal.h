@@ -9,6 +9,7 @@
 namespace sage {
 
 constexpr int kBlk = 128;  // B_q = B_kv = 128 (reading A5): tcgen05 M = 128 tiles
+constexpr int kMaxSeqLen = 32768;  // per-head scale rows are staged in shared memory (T <= 256)
 
 // ---- memory-bound passes (sage_prep.cu) ----
 // K0: per-(head, 128-row chunk) column sums in double, fixed order (reading A17).
@@ -57,8 +58,10 @@ struct BwdArgs {
   int BH, N, d;
   float tau;
   bool causal, qsmooth;
+  int ablate;  // profiling only (SAGE_ABLATE): 1 drain math off, 2 compute math off, 4 dQ reduction off
 };
 cudaError_t launch_bwd(const BwdArgs& a, cudaStream_t s);
+cudaError_t read_bwd_trace(void* host, size_t bytes);  // profiling: K4 event timeline
 
 // UMMA tile test (sage_debug_umma)
 cudaError_t launch_debug_umma(int mode, int K, int N, const CUtensorMap* tma, const CUtensorMap* tmb,

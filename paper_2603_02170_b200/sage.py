@@ -19,7 +19,7 @@ _STATUS = {0: "SAGE_OK", 1: "SAGE_ERR_INVALID_VALUE", 2: "SAGE_ERR_UNSUPPORTED",
 
 # exported symbols of include/sage.h
 SYMBOLS = ("sage_ctx_bytes", "sage_workspace_bytes", "sage_fwd", "sage_bwd", "sage_ctx_get_view",
-           "sage_ws_get_view", "sage_debug_umma", "sage_profile_enable", "sage_profile_read",
+           "sage_ws_get_view", "sage_debug_umma", "sage_debug_trace", "sage_profile_enable", "sage_profile_read",
            "sage_status_string", "sage_last_cuda_error", "sage_version")
 
 
@@ -61,6 +61,7 @@ def lib():
         L.sage_ctx_get_view.argtypes = [pp, P, ctypes.POINTER(SageCtxView)]
         L.sage_ws_get_view.argtypes = [pp, ctypes.c_int, P, ctypes.POINTER(SageWsView)]
         L.sage_debug_umma.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P]
+        L.sage_debug_trace.argtypes = [P, S]
         L.sage_profile_enable.argtypes = [ctypes.c_int]
         L.sage_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double)] * 2 + [ctypes.POINTER(ctypes.c_int64)] * 3
         L.sage_status_string.restype = ctypes.c_char_p
