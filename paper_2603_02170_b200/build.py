@@ -7,6 +7,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsage.so")
+TRACE_LIB = os.path.join(HERE, "libsage_trace.so")  # profiling build only
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 # -gencode arch=compute_100a,code=sm_100a: plain -arch=sm_100a embeds compute_100 PTX
@@ -29,25 +30,32 @@ def _stale():
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
-        return LIB
+def _link(lib, defines, verbose):
+    tag = "trace" if defines else "prod"
     objs = []
     for src in sources():
-        obj = os.path.join(CSRC, "build", os.path.basename(src) + ".o")
+        obj = os.path.join(CSRC, "build", tag, os.path.basename(src) + ".o")
         os.makedirs(os.path.dirname(obj), exist_ok=True)
-        cmd = [NVCC] + [f for f in FLAGS if f != "-shared"] + ["-dc" if False else "-c", src, "-o", obj]
+        cmd = [NVCC] + [f for f in FLAGS if f != "-shared"] + defines + ["-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
         objs.append(obj)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
                            "-Xcompiler", "-fPIC", "-o", tmp] + objs + ["-lcudart"])
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
+
+
+def build(force=False, verbose=False, trace=False):
+    """Build libsage.so; with trace=True also libsage_trace.so (K4 timeline/ablation hooks)."""
+    if force or _stale():
+        _link(LIB, [], verbose)
+    if trace:
+        _link(TRACE_LIB, ["-DSAGE_TRACE=1"], verbose)
     return LIB
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv)
     print(LIB)

@@ -186,11 +186,14 @@ T* at(void* base, size_t off) {
 
 }  // namespace
 
-bool make_tmap_2d(CUtensorMap* m, const void* base, bool bf16, uint64_t rows, uint64_t cols, uint32_t box_rows,
+bool make_tmap_2d(CUtensorMap* m, const void* base, TmapType type, uint64_t rows, uint64_t cols, uint32_t box_rows,
                   uint32_t box_cols) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
-  const uint32_t esz = bf16 ? 2 : 1;
+  const uint32_t esz = type == kF32 ? 4 : type == kBF16 ? 2 : 1;
+  const CUtensorMapDataType dt = type == kF32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : type == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * esz};
   cuuint32_t box[2] = {box_cols, box_rows};
@@ -199,8 +202,7 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, bool bf16, uint64_t rows, ui
   CUtensorMapSwizzle sw = row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                           : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                             : CU_TENSOR_MAP_SWIZZLE_NONE;
-  CUresult r = enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
-                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS && std::getenv("SAGE_DEBUG"))
     std::fprintf(stderr, "[libsage] cuTensorMapEncodeTiled -> %d (base %p rows %llu cols %llu box %u x %u)\n", (int)r,
@@ -333,8 +335,8 @@ sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const v
 
   FwdArgs a{};
   const uint64_t rows = D.BH * D.N;
-  if (!make_tmap_2d(&a.tm_q, q8, false, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_k, k8, false, rows, d, kBlk, d) ||
-      !make_tmap_2d(&a.tm_v, v8, false, rows, d, kBlk, d))
+  if (!make_tmap_2d(&a.tm_q, q8, kU8, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_k, k8, kU8, rows, d, kBlk, d) ||
+      !make_tmap_2d(&a.tm_v, v8, kU8, rows, d, kBlk, d))
     return cuda_fail(cudaErrorInvalidValue);
 
   cudaError_t e = cudaSuccess;
@@ -394,9 +396,10 @@ sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const f
 
   BwdArgs a{};
   const uint64_t rows = D.BH * D.N;
-  if (!make_tmap_2d(&a.tm_q, q8, false, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_k, k8, false, rows, d, kBlk, d) ||
-      !make_tmap_2d(&a.tm_doq, do8, false, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_v, v, true, rows, d, kBlk, 64) ||
-      !make_tmap_2d(&a.tm_do, dO, true, rows, d, kBlk, 64))
+  if (!make_tmap_2d(&a.tm_q, q8, kU8, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_k, k8, kU8, rows, d, kBlk, d) ||
+      !make_tmap_2d(&a.tm_doq, do8, kU8, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_v, v, kBF16, rows, d, kBlk, 64) ||
+      !make_tmap_2d(&a.tm_do, dO, kBF16, rows, d, kBlk, 64) ||
+      !make_tmap_2d(&a.tm_dq, dqacc, kF32, rows, d, kBlk, 32))
     return cuda_fail(cudaErrorInvalidValue);
   cudaError_t e;
   // K3: delta, psi(dO), L*log2(e), zero dQ accumulator (Alg. 2 lines 2, 6)
@@ -445,11 +448,11 @@ sage_status sage_debug_umma(int mode, int K, int N, const void* a, const void* b
   CUtensorMap ta{}, tb{};
   bool ok = true;
   if (mode == 0) {
-    ok = make_tmap_2d(&ta, a, false, 128, K, 128, K) && make_tmap_2d(&tb, b, false, 128, K, 128, K);
+    ok = make_tmap_2d(&ta, a, kU8, 128, K, 128, K) && make_tmap_2d(&tb, b, kU8, 128, K, 128, K);
   } else if (mode == 3) {
-    ok = make_tmap_2d(&ta, a, true, 128, K, 128, 64) && make_tmap_2d(&tb, b, true, 128, K, 128, 64);
+    ok = make_tmap_2d(&ta, a, kBF16, 128, K, 128, 64) && make_tmap_2d(&tb, b, kBF16, 128, K, 128, 64);
   } else {
-    ok = make_tmap_2d(&tb, b, false, 128, N, 128, N);
+    ok = make_tmap_2d(&tb, b, kU8, 128, N, 128, N);
     ta = tb;
   }
   if (!ok) return cuda_fail(cudaErrorInvalidValue);

@@ -53,7 +53,11 @@ struct BwdSmem {
   static constexpr int kRowSum = kScl + 32;                   // [2 slots][2 wg][128] int (Q-smoothing colsum of dS^)
   static constexpr int kScQ = kRowSum + 4 * kBlk * 4;          // s_Q[bh][0..T), s_dO[bh][0..T) (T <= kMaxT)
   static constexpr int kScDO = kScQ + kMaxT * 4;
-  static constexpr int kBar = kScDO + kMaxT * 4;
+  // dQ tile staging for the TMA reduce-add (d=64: 2 buffers x [2 boxes][128][32] fp32, 128B-swizzled)
+  static constexpr bool kDqTma = D == 64;
+  static constexpr int kDqBox = kBlk * 32 * 4;
+  static constexpr int kDq = (kScDO + kMaxT * 4 + 1023) / 1024 * 1024;
+  static constexpr int kBar = kDq + (kDqTma ? 2 * (D / 32) * kDqBox : 0);
   static constexpr int kNumBars = 1 + 2 * kStages + 8;
   static constexpr int kTmemSlot = kBar + kNumBars * 8;
   static constexpr int kBytes = kTmemSlot + 16;
@@ -61,13 +65,18 @@ struct BwdSmem {
   static constexpr uint32_t kStageTx = 4 * kTile + 1024;
 };
 
+// Profiling hooks (timeline + ablation switches) exist only in the SAGE_TRACE=1 build
+// (libsage_trace.so); the production library compiles them out.
+#ifndef SAGE_TRACE
+#define SAGE_TRACE 0
+#endif
 // Profiling-only timeline (SAGE_ABLATE bit 8): clock64 stamps of pipeline events for the
 // first kTrCtas CTAs, read back with sage_debug_trace().  One predicated branch per event.
 constexpr int kTrCtas = 4, kTrTiles = 64, kTrEvents = 24;
 __device__ unsigned long long g_trace[kTrCtas * kTrTiles * kTrEvents];
 #define TR(ev, it)                                                                  \
   do {                                                                              \
-    if ((ablate & 8) && blockIdx.x < kTrCtas && (it) < kTrTiles)                    \
+    if (SAGE_TRACE && (ablate & 8) && blockIdx.x < kTrCtas && (it) < kTrTiles)      \
       g_trace[(blockIdx.x * kTrTiles + (it)) * kTrEvents + (ev)] = clock64();       \
   } while (0)
 
@@ -92,18 +101,22 @@ template <int D, bool CAUSAL, bool QSMOOTH>
 __global__ void __launch_bounds__(kThreads, 1)
     sage_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_doq, const __grid_constant__ CUtensorMap tm_v,
-                    const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ q_scale,
+                    const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
+                    const float* __restrict__ q_scale,
                     const float* __restrict__ k_scale, const float* __restrict__ do_scale,
                     const float* __restrict__ l2g, const float* __restrict__ deltag, const float* __restrict__ bias,
                     const float* __restrict__ mu_q, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dk,
-                    __nv_bfloat16* __restrict__ dv, int N, int BH, float tau, int ablate) {
+                    __nv_bfloat16* __restrict__ dv, int N, int BH, float tau, int ablate_arg) {
+  const int ablate = SAGE_TRACE ? ablate_arg : 0;
   using L = BwdSmem<D>;
   constexpr int kStages = L::kStages;
   constexpr bool kAlias = D == 128;
   // setmaxnreg budgets (x128 threads each; sum = 512 regs/thread-slot = the 64K register file)
   constexpr uint32_t kRegProducer = 56, kRegCompute = D == 64 ? 136 : 128, kRegDrain = D == 64 ? 184 : 200;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment (128B swizzle atoms) by offsetting the __shared__ array itself, so every
+  // derived pointer stays in the shared window (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;             // [kStages]
@@ -349,6 +362,7 @@ if (cm) {
         uint32_t v[32];
         tmem_ld32(tS + qc0 + cc * 32 + lane_off, v);
         tmem_wait_ld();
+        if (threadIdx.x == 128 && cc == 0) TR(16, it);
 #pragma unroll
         for (int e4 = 0; e4 < 8; ++e4) {
           float4 l4 = Ls4[cc * 8 + e4];
@@ -369,6 +383,7 @@ if (cm) {
         }
       }
 }
+      if (threadIdx.x == 128) TR(18, it);
       tc_fence_before();
       if (diag) {  // causal: key r attends query q only if r <= q (reading A14)
 #pragma unroll
@@ -379,7 +394,9 @@ if (cm) {
       for (int e = 0; e < 64; e += 4) tmax = fmaxf(tmax, fmax3(t[e], t[e + 1], fmaxf(t[e + 2], t[e + 3])));
 
       // -- step 2: psi(P) scale over the tile: amax = max P = 2^max(t)  (line 6, reading A11)
+      if (threadIdx.x == 128) TR(19, it);
       const float amax_p = ex2(compute_max(tmax, red, cw, 1));
+      if (threadIdx.x == 128) TR(21, it);
       const float inv_p = amax_p > 0.f ? __fdiv_rn(127.f, amax_p) : 0.f;
       // tile scales for the drain warpgroup (4 slots: it cannot run 4 tiles ahead of the drain)
       if (threadIdx.x == 128) scl[(it & 3) * 2] = __fdiv_rn(amax_p, 127.f);
@@ -396,6 +413,9 @@ if (cm) {
       for (int cc = 0; cc < 2; ++cc) {
         uint32_t v[32];
         tmem_ld32(tDP + qc0 + cc * 32 + lane_off, v);
+        // the chunk's 32 exponentials first: back-to-back MUFU work while the TMEM load lands
+#pragma unroll
+        for (int u = 0; u < 32; ++u) t[cc * 32 + u] = ex2(t[cc * 32 + u]);
         tmem_wait_ld();
 #pragma unroll
         for (int c16 = 0; c16 < 2; ++c16) {
@@ -405,8 +425,6 @@ if (cm) {
             const int ev = c16 * 16 + e4 * 4;  // index into v
             const int e = cc * 32 + ev;        // index into t
             const float4 d4 = Ds4[e / 4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) t[e + u] = ex2(t[e + u]);
             float2 qa = ffma2(make_float2(t[e], t[e + 1]), make_float2(inv_p, inv_p), make_float2(kMagic, kMagic));
             float2 qb = ffma2(make_float2(t[e + 2], t[e + 3]), make_float2(inv_p, inv_p), make_float2(kMagic, kMagic));
             w[e4] = pack4_magic(qa.x, qa.y, qb.x, qb.y);
@@ -425,6 +443,7 @@ if (cm) {
         }
       }
 }
+      if (threadIdx.x == 128) TR(23, it);
       fence_proxy_async_smem();
       tc_fence_before();
       warp_arrive(p_ready);  // P^^T written; S^T and dP^T read (their TMEM columns may be reused)
@@ -564,7 +583,36 @@ if (cm) {
 
       // dQ_i += tile * s_dS * s_K * tau, fp32 reduction across key blocks (line 10)
       if (threadIdx.x == 384) TR(12, it);
-      if (!(ablate & 1)) {
+      if constexpr (L::kDqTma) {
+        // scaled tile -> swizzled smem staging (double-buffered) -> one TMA reduce-add per 32-col box
+        uint8_t* stage = smem + L::kDq + (it & 1) * (D / 32) * L::kDqBox;
+        if (threadIdx.x == 384 && it >= 2) bulk_wait_read<1>();  // reduce of tile it-2 has read `stage`
+        named_bar_sync(3, 128);
+        if (!(ablate & 1)) {
+          const float s_ds = scl[(it & 3) * 2 + 1];
+          const float2 f = make_float2(s_ds * sk * tau, s_ds * sk * tau);
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tDQ + c0 + lane_off, v);
+            tmem_wait_ld();
+            uint8_t* box = stage + (c0 / 32) * L::kDqBox;
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) {
+              float2 a = fmul2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f);
+              float2 b = fmul2(make_float2(__int2float_rn((int)v[e + 2]), __int2float_rn((int)v[e + 3])), f);
+              *reinterpret_cast<float4*>(box + sw_offset(r, e / 4, 128)) = make_float4(a.x, a.y, b.x, b.y);
+            }
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(3, 128);
+        if (threadIdx.x == 384 && !(ablate & 4)) {
+#pragma unroll
+          for (int b = 0; b < D / 32; ++b) tma_reduce_add_2d(&tm_dq, stage + b * L::kDqBox, b * 32, bh * N + i * kBlk);
+          bulk_commit();
+        }
+      } else if (!(ablate & 1)) {
         const float s_ds = scl[(it & 3) * 2 + 1];
         const float2 f = make_float2(s_ds * sk * tau, s_ds * sk * tau);
         float* grow = dq_acc + ((size_t)bh * N + (size_t)i * kBlk + r) * D;
@@ -584,6 +632,9 @@ if (cm) {
       tc_fence_before();
       warp_arrive(dkq_drained);
       if (threadIdx.x == 384) TR(13, it);
+    }
+    if constexpr (L::kDqTma) {
+      if (threadIdx.x == 384) bulk_wait_all();  // staging smem must outlive the in-flight reduces
     }
     // epilogue: dK_j, dV_j rows -> bf16
     const size_t orow = ((size_t)krow + r) * D;
@@ -632,7 +683,7 @@ cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem<D>::kAlloc);
   if (e != cudaSuccess) return e;
   const int T = a.N / kBlk;
-  kern<<<a.BH * T, kThreads, BwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_doq, a.tm_v, a.tm_do, a.q_scale,
+  kern<<<a.BH * T, kThreads, BwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_doq, a.tm_v, a.tm_do, a.tm_dq, a.q_scale,
                                                        a.k_scale, a.do_scale, a.l2, a.delta, a.bias, a.mu_q,
                                                        a.dq_acc, a.dk, a.dv, a.N, a.BH, a.tau, a.ablate);
   return cudaGetLastError();

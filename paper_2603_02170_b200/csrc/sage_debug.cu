@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(128, 1)
     debug_umma_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                       const int8_t* __restrict__ a_host_layout, void* __restrict__ out) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int kABytes = MODE == 3 ? 128 * K * 2 : (MODE == 0 ? 128 * K : 128 * 128);
   constexpr int kBBytes = MODE == 3 ? 128 * K * 2 : (MODE == 0 ? 128 * K : 128 * N);
   uint8_t* sa = smem;

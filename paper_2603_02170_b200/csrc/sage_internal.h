@@ -49,6 +49,7 @@ cudaError_t launch_fwd(const FwdArgs& a, cudaStream_t s);
 struct BwdArgs {
   CUtensorMap tm_q, tm_k, tm_doq;  // int8 [BH*N][d], box [128][d]
   CUtensorMap tm_v, tm_do;         // bf16 [BH*N][d], box [128][64]
+  CUtensorMap tm_dq;               // fp32 dQ accumulator [BH*N][d], box [128][32] (TMA reduce-add)
   const float *q_scale, *k_scale, *do_scale;
   const float *l2, *delta;         // [BH][N]
   const float* bias;               // [BH][T][N] or null
@@ -68,7 +69,8 @@ cudaError_t launch_debug_umma(int mode, int K, int N, const CUtensorMap* tma, co
                               const void* a, void* d, cudaStream_t s);
 
 // Tensor-map helpers (sage_api.cu)
-bool make_tmap_2d(CUtensorMap* m, const void* base, bool bf16, uint64_t rows, uint64_t cols, uint32_t box_rows,
+enum TmapType { kU8 = 0, kBF16 = 1, kF32 = 2 };
+bool make_tmap_2d(CUtensorMap* m, const void* base, TmapType type, uint64_t rows, uint64_t cols, uint32_t box_rows,
                   uint32_t box_cols);
 
 }  // namespace sage

@@ -11,7 +11,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsage.so")
+# SAGE_LIB selects the profiling build (libsage_trace.so) for scripts/trace_bwd.py only.
+LIB_PATH = os.environ.get("SAGE_LIB") or os.path.join(_HERE, "libsage.so")
 
 SAGE_CAUSAL, SAGE_K_SMOOTH, SAGE_Q_SMOOTH = 1, 2, 4
 _STATUS = {0: "SAGE_OK", 1: "SAGE_ERR_INVALID_VALUE", 2: "SAGE_ERR_UNSUPPORTED", 3: "SAGE_ERR_MISALIGNED",

@@ -4,6 +4,8 @@ clock64 event stamps per tile for one CTA (cycles relative to its first event).
   SAGE_ABLATE=8 python scripts/trace_bwd.py [C2] [cta]
 """
 import ctypes, os, sys
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ.setdefault("SAGE_LIB", os.path.join(_ROOT, "paper_2603_02170_b200", "libsage_trace.so"))
 import numpy as np
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -24,7 +26,7 @@ sage.lib().sage_debug_trace(buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes)
 tr = buf.reshape(4, 64, 24)[cta].astype(np.int64)
 names = ["S_iss", "dV_iss", "dP_iss", "dKQ_iss", "-", "c_sfull", "c_pready", "c_dpfull", "c_dsready", "c_dstfree",
          "d_dvfull", "d_dkfull", "d_dqfull", "d_dqdone", "tma_st", "c_ptfree",
-         "m_sfree", "m_pready", "m_dvdrn", "m_dpfree", "m_dsrdy", "m_dkqdrn", "m_qfull", "-"]
+         "c_ld0", "m_pready", "c_ldall", "c_tmax", "m_dsrdy", "c_bar1", "m_qfull", "c_st3"]
 base = tr[tr > 0].min()
 rows = [t for t in range(64) if tr[t].any()]
 print("tile " + " ".join(f"{n:>8s}" for n in names))
