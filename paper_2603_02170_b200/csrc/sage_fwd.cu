@@ -1,50 +1,56 @@
 // sage_fwd.cu -- K2: SageBwd forward, Alg. 1, one CTA per
-// (head, 128-query block i).  tcgen05 kind::i8 MMAs with TMEM accumulators, TMA
-// into 128B/64B-swizzled shared memory, warp-specialised roles:
+// (head, 128-query block i), two CTAs resident per SM (TMEM 256 columns, <= 113 KB smem,
+// setmaxnreg) so one CTA's softmax overlaps the other's MMAs and TMEM round trips.
+// tcgen05 kind::i8 MMAs with TMEM accumulators, TMA into 128B/64B-swizzled shared
+// memory, warp-specialised roles:
 //   warps 0-3  softmax + correction + epilogue (thread t owns query row t = TMEM lane t)
-//   warp  4    TMA producer (Q^_i once, K^_j / V^_j ring)
-//   warp  5    TMEM allocator + MMA issuer (one thread)
+//   warp  4    TMA producer (Q^_i once, K^_j / V^_j ring), one elected lane
+//   warp  5    TMEM allocator + MMA issuer, one elected lane
+//   warps 6-7  idle (they complete warpgroup 1 for setmaxnreg)
 // Per kv tile j (Alg. 1 lines 7-10, with the corrections of reading A7):
-//   S_ij   = MM(Q^_i, K^_j) s_Q s_K tau            int32 in TMEM S[j%2], scaled in fp32
+//   S_ij   = MM(Q^_i, K^_j) s_Q s_K tau            int32 in TMEM, scaled in fp32
 //   m_ij   = max(m, rowmax S_ij);  alpha = e^{m - m_ij}
 //   P~     = e^{S - m_ij} = e^{S - rowmax} e^{rowmax - m_ij}
 //   s_P    = e^{rowmax - m_ij}/127,  P^ = RNE(P~/s_P) = RNE(127 e^{S - rowmax})  in [0,127]
 //   l      = alpha l + e^{rowmax - m_ij} sum(e^{S - rowmax})
-//   O      = alpha O + MM(P^, V^_j) s_P s_V        (int32 in TMEM PV[j%2], drained to fp32 regs)
-// All exponentials are base 2 on log2(e)-prescaled logits (one MUFU.EX2 per score).
+//   O      = alpha O + MM(P^, V^_j) s_P s_V        (int32 in TMEM, drained to fp32 registers)
+// All exponentials are base 2 on log2(e)-prescaled logits (one MUFU.EX2 per score); the
+// factor 127 is folded into the exponent, p' = 2^{s - rowmax + log2 127} = 127 e^{S - rowmax}.
 #include "sage_internal.h"
 #include "sm100.cuh"
 
 namespace sage {
 namespace {
 
-constexpr int kStages = 3;
-constexpr int kThreads = 192;
+constexpr int kThreads = 256;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLog2_127 = 6.988684686772166f;
 
 template <int D>
 struct FwdSmem {
+  static constexpr int kStages = D == 64 ? 3 : 2;
   static constexpr int kTile = kBlk * D;        // bytes of an int8 [128][D] tile
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + kTile;
   static constexpr int kV = kK + kStages * kTile;
-  static constexpr int kP = kV + kStages * kTile;  // 2 x [128][128] int8
-  static constexpr int kBias = kP + 2 * kBlk * kBlk;  // 2 x 128 floats (Q-smoothing)
+  static constexpr int kP = kV + kStages * kTile;  // [128][128] int8 P^, K-major 128B-swizzled
+  static constexpr int kBias = kP + kBlk * kBlk;   // 2 x 128 floats (Q-smoothing)
   static constexpr int kBar = kBias + 2 * kBlk * 4;
-  static constexpr int kNumBars = 1 + 4 * kStages + 12;
+  static constexpr int kNumBars = 1 + 4 * kStages + 4;
   static constexpr int kTmemSlot = kBar + kNumBars * 8;
   static constexpr int kBytes = kTmemSlot + 16;
   static constexpr int kAlloc = kBytes + 1024;  // slack for 1024-byte alignment
 };
 
 template <int D, bool CAUSAL, bool QSMOOTH>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     sage_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ q_scale,
                     const float* __restrict__ k_scale, const float* __restrict__ v_scale,
                     const float* __restrict__ bias, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, int N,
                     int BH, float tau) {
   using L = FwdSmem<D>;
+  constexpr int kStages = L::kStages;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment (128B swizzle atoms) by offsetting the __shared__ array itself, so every
   // derived pointer stays in the shared window (LDS/STS, not generic LD/ST)
@@ -55,20 +61,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* k_empty = k_full + kStages;
   uint64_t* v_full = k_empty + kStages;
   uint64_t* v_empty = v_full + kStages;
-  uint64_t* s_full = v_empty + kStages;  // [2]
-  uint64_t* s_empty = s_full + 2;        // [2]
-  uint64_t* p_full = s_empty + 2;        // [2]
-  uint64_t* p_empty = p_full + 2;        // [2]
-  uint64_t* o_full = p_empty + 2;        // [2]
-  uint64_t* o_empty = o_full + 2;        // [2]
+  uint64_t* s_full = v_empty + kStages;  // MMA -> softmax: S_j in TMEM
+  uint64_t* p_full = s_full + 1;         // softmax -> MMA (4 warps): S_j read, P^_j in smem
+  uint64_t* o_full = s_full + 2;         // MMA -> softmax: PV_j in TMEM (P^_j read)
+  uint64_t* o_empty = s_full + 3;        // softmax -> MMA (4 warps): PV_j drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
   float* bias_s = reinterpret_cast<float*>(smem + L::kBias);
 
   const int T = N / kBlk;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // Longest-first order for causal: high query blocks have the most kv tiles.
-  const int tile = blockIdx.x;
+  const int warp = threadIdx.x / 32;
   // head-major order (the CTAs of one head share K^/V^ through L2); causal: longest (high i) first
+  const int tile = blockIdx.x;
   const int bh = tile / T;
   const int i = CAUSAL ? (T - 1 - tile % T) : (tile % T);
   const int nj = CAUSAL ? i + 1 : T;
@@ -82,85 +85,95 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(v_full + s, 1);
       mbar_init(v_empty + s, 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(s_full + b, 1);
-      mbar_init(s_empty + b, 128);
-      mbar_init(p_full + b, 128);
-      mbar_init(p_empty + b, 1);
-      mbar_init(o_full + b, 1);
-      mbar_init(o_empty + b, 128);
-    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(o_full, 1);
+    mbar_init(o_empty, 4);
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  if (warp == 5) tmem_alloc(tmem_slot, 256);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem;          // S[b] at columns 128*b
-  const uint32_t tPV = tmem + 256;   // PV[b] at columns 256 + D*b
+  const uint32_t tS = tmem;         // S_j   columns [0, 128)
+  const uint32_t tPV = tmem + 128;  // PV_j  columns [128, 128 + D)
 
-  if (warp == 4) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      mbar_expect_tx(q_full, L::kTile);
-      tma_load_2d(smem + L::kQ, &tm_q, q_full, 0, row0);
+  if (warp >= 4) {
+    reg_dealloc<72>();
+    if (warp == 4) {
+      // ---------------------------------------------------------- TMA producer
+      if (elect_one()) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
+        mbar_expect_tx(q_full, L::kTile);
+        tma_load_2d(smem + L::kQ, &tm_q, q_full, 0, row0);
+      }
+      __syncwarp();
       for (int j = 0; j < nj; ++j) {
         const int st = j % kStages;
         const uint32_t ph = (j / kStages) & 1;
         const int krow = bh * N + j * kBlk;
         mbar_wait(k_empty + st, ph ^ 1);
-        mbar_expect_tx(k_full + st, L::kTile);
-        tma_load_2d(smem + L::kK + st * L::kTile, &tm_k, k_full + st, 0, krow);
+        if (elect_one()) {
+          mbar_expect_tx(k_full + st, L::kTile);
+          tma_load_2d(smem + L::kK + st * L::kTile, &tm_k, k_full + st, 0, krow);
+        }
+        __syncwarp();
         mbar_wait(v_empty + st, ph ^ 1);
-        mbar_expect_tx(v_full + st, L::kTile);
-        tma_load_2d(smem + L::kV + st * L::kTile, &tm_v, v_full + st, 0, krow);
+        if (elect_one()) {
+          mbar_expect_tx(v_full + st, L::kTile);
+          tma_load_2d(smem + L::kV + st * L::kTile, &tm_v, v_full + st, 0, krow);
+        }
+        __syncwarp();
       }
-    }
-  } else if (warp == 5) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    } else if (warp == 5) {
+      // ---------------------------------------------------------- MMA issuer
       constexpr uint32_t kIdS = idesc_i8(128, 128, false, false);
       constexpr uint32_t kIdPV = idesc_i8(128, D, false, true);
       const uint32_t q_addr = smem_u32(smem + L::kQ);
-      mbar_wait(q_full, 0);
-      auto issue_s = [&](int j) {
-        const int st = j % kStages, b = j & 1;
+      const uint32_t k0 = smem_u32(smem + L::kK), v0 = smem_u32(smem + L::kV);
+      const uint32_t p_addr = smem_u32(smem + L::kP);
+      auto issue_s = [&](int j) {  // S_j = Q^_i K^_j^T (line 7)
+        const int st = j % kStages;
         mbar_wait(k_full + st, (j / kStages) & 1);
-        mbar_wait(s_empty + b, ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t k_addr = smem_u32(smem + L::kK + st * L::kTile);
+        if (elect_one()) {
+          const uint32_t k_addr = k0 + st * L::kTile;
 #pragma unroll
-        for (int kk = 0; kk < D / 32; ++kk)
-          mma_i8(tS + 128 * b, desc_kmajor(q_addr, D, kk * 32), desc_kmajor(k_addr, D, kk * 32), kIdS, kk > 0);
-        mma_commit(k_empty + st);
-        mma_commit(s_full + b);
+          for (int kk = 0; kk < D / 32; ++kk)
+            mma_i8(tS, desc_kmajor(q_addr, D, kk * 32), desc_kmajor(k_addr, D, kk * 32), kIdS, kk > 0);
+          mma_commit(k_empty + st);
+          mma_commit(s_full);
+        }
+        __syncwarp();
       };
-      auto issue_pv = [&](int j) {
-        const int st = j % kStages, b = j & 1;
-        mbar_wait(p_full + b, (j >> 1) & 1);
+      auto issue_pv = [&](int j) {  // PV_j = P^_j V^_j (line 10)
+        const int st = j % kStages;
         mbar_wait(v_full + st, (j / kStages) & 1);
-        mbar_wait(o_empty + b, ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t p_addr = smem_u32(smem + L::kP + b * kBlk * kBlk);
-        const uint32_t v_addr = smem_u32(smem + L::kV + st * L::kTile);
+        if (elect_one()) {
+          const uint32_t v_addr = v0 + st * L::kTile;
 #pragma unroll
-        for (int kk = 0; kk < kBlk / 32; ++kk)
-          mma_i8(tPV + D * b, desc_kmajor(p_addr, 128, kk * 32), desc_mnmajor(v_addr, D, kk * 32), kIdPV, kk > 0);
-        mma_commit(v_empty + st);
-        mma_commit(p_empty + b);
-        mma_commit(o_full + b);
+          for (int kk = 0; kk < kBlk / 32; ++kk)
+            mma_i8(tPV, desc_kmajor(p_addr, 128, kk * 32), desc_mnmajor(v_addr, D, kk * 32), kIdPV, kk > 0);
+          mma_commit(v_empty + st);
+          mma_commit(o_full);
+        }
+        __syncwarp();
       };
+      mbar_wait(q_full, 0);
+      issue_s(0);
       for (int j = 0; j < nj; ++j) {
-        issue_s(j);
-        if (j > 0) issue_pv(j - 1);
+        mbar_wait(p_full, j & 1);  // S_j consumed, P^_j written
+        if (j + 1 < nj) issue_s(j + 1);
+        if (j > 0) mbar_wait(o_empty, (j - 1) & 1);  // PV_{j-1} drained
+        issue_pv(j);
       }
-      issue_pv(nj - 1);
     }
   } else {
+    reg_alloc<184>();
     // ------------------------------------------------------------ softmax / correction (128 threads)
     const int r = threadIdx.x;  // query row within the block == TMEM lane
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
@@ -171,106 +184,132 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int c = 0; c < D; ++c) oacc[c] = 0.f;
     float m = -INFINITY, l = 0.f;
     float prev_alpha = 0.f, prev_spv = 0.f;
+    uint8_t* prow = smem + L::kP;
 
-    auto correct = [&](int j, float alpha, float spv) {
-      const int b = j & 1;
-      mbar_wait(o_full + b, (j >> 1) & 1);
-      tc_fence_after();
+    // O = alpha O + PV s_P s_V  (Alg. 1 line 10, reading A7); alpha == 1 skips the rescale
+    auto correct = [&](float alpha, float spv) {
+      const float2 f = make_float2(spv, spv);
+      const bool rescale = __any_sync(0xffffffffu, alpha != 1.f);
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t v[32];
-        tmem_ld32(tPV + D * b + c0 + lane_off, v);
+        tmem_ld32(tPV + c0 + lane_off, v);
         tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
-          oacc[c0 + e] = fmaf(alpha, oacc[c0 + e], __int2float_rn((int)v[e]) * spv);
+        for (int e = 0; e < 32; e += 2) {
+          float2 acc = make_float2(oacc[c0 + e], oacc[c0 + e + 1]);
+          if (rescale) acc = fmul2(acc, make_float2(alpha, alpha));
+          acc = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f, acc);
+          oacc[c0 + e] = acc.x;
+          oacc[c0 + e + 1] = acc.y;
+        }
       }
       tc_fence_before();
-      mbar_arrive(o_empty + b);
+      warp_arrive(o_empty);
     };
 
     for (int j = 0; j < nj; ++j) {
-      const int b = j & 1;
       const float c2 = sq * k_scale[(size_t)bh * T + j] * tau2;  // int32 -> log2-domain logit
+      const float sv = v_scale[(size_t)bh * T + j];
       const bool diag = CAUSAL && (j == i);
+      const float* bj = bias_s + (j & 1) * kBlk;
       if constexpr (QSMOOTH) {
-        // bias row (tau*log2e * mu_Qi . K_sm[n]) for this kv tile, shared by all rows
-        named_bar_sync(1, 128);
-        bias_s[b * kBlk + r] = bias[((size_t)bh * T + i) * N + (size_t)j * kBlk + r] * tau2;
+        // bias row (tau*log2e * mu_Qi . K_sm[n]) for this kv tile, shared by all rows; two slots
+        // so one barrier per tile suffices (slot j&1 was last read in tile j-2)
+        bias_s[(j & 1) * kBlk + r] = bias[((size_t)bh * T + i) * N + (size_t)j * kBlk + r] * tau2;
         named_bar_sync(1, 128);
       }
-      mbar_wait(s_full + b, (j >> 1) & 1);
+      mbar_wait(s_full, j & 1);
       tc_fence_after();
       // pass 1: row max (on int32 when there is no per-column bias)
       float rm;
       if constexpr (!QSMOOTH) {
         int mx = INT_MIN;
-#pragma unroll 1
+#pragma unroll
         for (int c0 = 0; c0 < kBlk; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(tS + 128 * b + c0 + lane_off, v);
+          tmem_ld32(tS + c0 + lane_off, v);
           tmem_wait_ld();
+          if (diag) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (!diag || c0 + e <= r) mx = max(mx, (int)v[e]);
+            for (int e = 0; e < 32; ++e)
+              if (c0 + e <= r) mx = max(mx, (int)v[e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) mx = max(mx, max((int)v[e], (int)v[e + 1]));
+          }
         }
         rm = __int2float_rn(mx) * c2;  // max commutes with the positive scale
       } else {
         rm = -INFINITY;
-#pragma unroll 1
+#pragma unroll
         for (int c0 = 0; c0 < kBlk; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(tS + 128 * b + c0 + lane_off, v);
+          tmem_ld32(tS + c0 + lane_off, v);
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 32; ++e)
-            if (!diag || c0 + e <= r) rm = fmaxf(rm, fmaf(__int2float_rn((int)v[e]), c2, bias_s[b * kBlk + c0 + e]));
+            if (!diag || c0 + e <= r) rm = fmaxf(rm, fmaf(__int2float_rn((int)v[e]), c2, bj[c0 + e]));
         }
       }
       const float m_new = fmaxf(m, rm);
       const float alpha = ex2(m - m_new);
       const float e_rm = ex2(rm - m_new);
-      // pass 2: e = 2^{S - rowmax}, P^ = RNE(127 e) -> swizzled K-major smem row r
-      mbar_wait(p_empty + b, ((j >> 1) & 1) ^ 1);
-      uint8_t* prow = smem + L::kP + b * kBlk * kBlk;
-      float rs = 0.f;
-#pragma unroll 1
+      const float sub = rm - kLog2_127;  // p' = 2^{s - rm + log2 127} = 127 e^{S - rowmax}
+      // pass 2: p' and P^ = RNE(p') -> swizzled K-major smem row r (the buffer is free once
+      // PV_{j-1} has completed)
+      if (j > 0) mbar_wait(o_full, (j - 1) & 1);
+      float2 rs2 = make_float2(0.f, 0.f);
+#pragma unroll
       for (int c0 = 0; c0 < kBlk; c0 += 32) {
         uint32_t v[32];
-        tmem_ld32(tS + 128 * b + c0 + lane_off, v);
+        tmem_ld32(tS + c0 + lane_off, v);
         tmem_wait_ld();
         uint32_t pk[8];
 #pragma unroll
         for (int e4 = 0; e4 < 8; ++e4) {
-          uint32_t w = 0;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int e = e4 * 4 + t;
-            float s2 = QSMOOTH ? fmaf(__int2float_rn((int)v[e]), c2, bias_s[b * kBlk + c0 + e]) - rm
-                               : fmaf(__int2float_rn((int)v[e]), c2, -rm);
-            float p = ex2(s2);
-            if (diag && c0 + e > r) p = 0.f;
-            rs += p;
-            w |= rne_small(127.f * p) << (8 * t);
+          const int e = e4 * 4;
+          float2 a = make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1]));
+          float2 b = make_float2(__int2float_rn((int)v[e + 2]), __int2float_rn((int)v[e + 3]));
+          if constexpr (QSMOOTH) {
+            const float4 b4 = *reinterpret_cast<const float4*>(bj + c0 + e);
+            a = ffma2(a, make_float2(c2, c2), make_float2(b4.x - sub, b4.y - sub));
+            b = ffma2(b, make_float2(c2, c2), make_float2(b4.z - sub, b4.w - sub));
+          } else {
+            a = ffma2(a, make_float2(c2, c2), make_float2(-sub, -sub));
+            b = ffma2(b, make_float2(c2, c2), make_float2(-sub, -sub));
           }
-          pk[e4] = w;
+          a = make_float2(ex2(a.x), ex2(a.y));
+          b = make_float2(ex2(b.x), ex2(b.y));
+          if (diag) {  // causal mask (reading A14): key n > query r -> P = 0
+            if (c0 + e > r) a.x = 0.f;
+            if (c0 + e + 1 > r) a.y = 0.f;
+            if (c0 + e + 2 > r) b.x = 0.f;
+            if (c0 + e + 3 > r) b.y = 0.f;
+          }
+          rs2 = fadd2(rs2, fadd2(a, b));
+          const float2 qa = fadd2(a, make_float2(kMagic, kMagic));
+          const float2 qb = fadd2(b, make_float2(kMagic, kMagic));
+          pk[e4] = pack4_magic(qa.x, qa.y, qb.x, qb.y);
         }
         const int chunk = c0 / 16;
         *reinterpret_cast<uint4*>(prow + sw_offset(r, chunk, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         *reinterpret_cast<uint4*>(prow + sw_offset(r, chunk + 1, 128)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
-      tc_fence_before();
-      mbar_arrive(s_empty + b);
       fence_proxy_async_smem();
-      mbar_arrive(p_full + b);
-      l = fmaf(alpha, l, e_rm * rs);
-      const float spv = e_rm * (1.f / 127.f) * v_scale[(size_t)bh * T + j];
+      tc_fence_before();
+      warp_arrive(p_full);
+      // l = alpha l + e^{rowmax - m_ij} sum(e^{S - rowmax})  (line 8, reading A7)
+      l = fmaf(alpha, l, e_rm * (1.f / 127.f) * (rs2.x + rs2.y));
+      const float spv = e_rm * (1.f / 127.f) * sv;
       m = m_new;
-      if (j > 0) correct(j - 1, prev_alpha, prev_spv);
+      if (j > 0) correct(prev_alpha, prev_spv);  // PV_{j-1} (its o_full was waited for above)
       prev_alpha = alpha;
       prev_spv = spv;
     }
-    correct(nj - 1, prev_alpha, prev_spv);
+    mbar_wait(o_full, (nj - 1) & 1);
+    tc_fence_after();
+    correct(prev_alpha, prev_spv);
     // epilogue: O = acc / l (Alg. 1 line 13), L = m + ln l (line 14, natural log)
     const float inv_l = l > 0.f ? 1.f / l : 0.f;
     __nv_bfloat16* orow = o + ((size_t)row0 + r) * D;
@@ -288,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 5) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, 256);
   }
 }
 
