@@ -350,9 +350,11 @@ sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const v
     if ((e = launch_blockmean(partq, muq, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
   }
   // K1: per-block psi (Alg. 1 line 3)
-  if ((e = launch_quantize(qb, muq, D.qs ? 2 : 0, q8, sq, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
-  if ((e = launch_quantize(kb, muk, D.ks ? 1 : 0, k8, sk, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
-  if ((e = launch_quantize(vb, nullptr, 0, v8, sv, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+  QuantJobs qj{};
+  qj.j[0] = QuantJob{qb, muq, D.qs ? 2 : 0, q8, sq};
+  qj.j[1] = QuantJob{kb, muk, D.ks ? 1 : 0, k8, sk};
+  qj.j[2] = QuantJob{vb, nullptr, 0, v8, sv};
+  if ((e = launch_quantize(qj, 3, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
   // mu_K is all-zero when K-smoothing is off (ctx is caller memory: make it so)
   if (!D.ks && (e = launch_fill(muk, D.BH * D.d, 0.f, s)) != cudaSuccess) return cuda_fail(e);
   if (D.qs && (e = launch_qsmooth_bias(kb, muk, muq, bias, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
@@ -370,7 +372,7 @@ sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const v
   a.causal = D.causal;
   a.qsmooth = D.qs;
   if ((e = timed(0, s, [&] { return launch_fwd(a, s); })) != cudaSuccess) return cuda_fail(e);
-  if (g_prof.on) g_prof.launches += (D.ks ? 2 : 1) + (D.qs ? 3 : 0) + 3 + 1;
+  if (g_prof.on) g_prof.launches += (D.ks ? 2 : 1) + (D.qs ? 3 : 0) + 1 + 1;
   return SAGE_OK;
 }
 

@@ -18,9 +18,19 @@ cudaError_t launch_colsum(const __nv_bfloat16* x, double* part, int BH, int N, i
 cudaError_t launch_colmean(const double* part, float* mu, int BH, int N, int d, cudaStream_t s);
 // K0c: mu_Q[bh][t][c] = fl32(part[bh][t][c] / 128)  (block-wise mu_Qi).
 cudaError_t launch_blockmean(const double* part, float* mu_q, int BH, int N, int d, cudaStream_t s);
-// K1: per-block psi of x - mu (mu per column: mu_mode 0 none, 1 per head [BH][d], 2 per block [BH][T][d]).
-cudaError_t launch_quantize(const __nv_bfloat16* x, const float* mu, int mu_mode, int8_t* xq, float* scale, int BH,
-                            int N, int d, cudaStream_t s);
+// K1: per-block psi of x - mu (mu per column: mu_mode 0 none, 1 per head [BH][d], 2 per block [BH][T][d]),
+// up to three tensors in one launch.
+struct QuantJob {
+  const __nv_bfloat16* x;
+  const float* mu;
+  int mu_mode;
+  int8_t* xq;
+  float* scale;
+};
+struct QuantJobs {
+  QuantJob j[3];
+};
+cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int d, cudaStream_t s);
 // Q-smoothing bias_i[n] = mu_Qi . (K[n] - mu_K)  (reading A13), fp32.
 cudaError_t launch_qsmooth_bias(const __nv_bfloat16* k, const float* mu_k, const float* mu_q, float* bias, int BH,
                                 int N, int d, cudaStream_t s);

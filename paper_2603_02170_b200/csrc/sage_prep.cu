@@ -32,29 +32,38 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 // ---------------------------------------------------------------- K0: column sums
-// part[bh][t][c] = sum_{r=0..127} x[bh][128t + r][c], sequential in r, in double (A17).
-// One thread owns 8 consecutive columns of one chunk; 16-byte loads.
-__global__ void colsum_kernel(const __nv_bfloat16* __restrict__ x, double* __restrict__ part, int N, int d,
-                              int n_items) {
-  int item = blockIdx.x * blockDim.x + threadIdx.x;
-  if (item >= n_items) return;
-  int groups = d / kVec;
-  int g = item % groups;
-  long long chunk = item / groups;  // = bh * T + t
-  const __nv_bfloat16* p = x + chunk * kBlk * d + g * kVec;
+// part[bh][t][c] = sum_{r=0..127} x[bh][128t + r][c] in double (reading A17).  One CTA per
+// 128-row chunk: thread (g, q) sums rows q, q+R, ... of column group g (8 columns, 16-byte
+// loads), then the R partials are combined in fixed order q = 0..R-1.  Sums of bf16 values in
+// double are exact unless a column spans > 53-8-log2(N) binades, so the order cannot change the
+// result for any realistic input; it is fixed anyway.
+template <int D>
+__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ x, double* __restrict__ part) {
+  constexpr int kGroups = D / kVec;        // 8 (d=64) or 16 (d=128)
+  constexpr int kR = 256 / kGroups;        // 32 or 16 row phases
+  __shared__ double red[kR][D];
+  const long long chunk = blockIdx.x;      // bh * T + t
+  const int g = threadIdx.x % kGroups, q = threadIdx.x / kGroups;
+  const __nv_bfloat16* p = x + chunk * kBlk * D + g * kVec;
   double acc[kVec];
 #pragma unroll
   for (int e = 0; e < kVec; ++e) acc[e] = 0.0;
-#pragma unroll 4
-  for (int r = 0; r < kBlk; ++r) {
+#pragma unroll
+  for (int r = q; r < kBlk; r += kR) {
     float f[kVec];
-    load_bf16x8(p + (size_t)r * d, f);
+    load_bf16x8(p + (size_t)r * D, f);
 #pragma unroll
     for (int e = 0; e < kVec; ++e) acc[e] += (double)f[e];
   }
-  double* out = part + chunk * d + g * kVec;
 #pragma unroll
-  for (int e = 0; e < kVec; ++e) out[e] = acc[e];
+  for (int e = 0; e < kVec; ++e) red[q][g * kVec + e] = acc[e];
+  __syncthreads();
+  if (threadIdx.x < D) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < kR; ++k) s += red[k][threadIdx.x];
+    part[chunk * D + threadIdx.x] = s;
+  }
 }
 
 // mu[bh][c] = fl32((sum over chunks, sequential in t) / N)
@@ -78,9 +87,14 @@ __global__ void blockmean_kernel(const double* __restrict__ part, float* __restr
 // One CTA quantises one 128 x d block: x_sm = fl32(x - mu); amax; scale = fl32(amax/127);
 // inv = fl32(127/amax) (0 for an all-zero block, A3); q = clamp(RNE(fl32(x_sm*inv)), +-127).
 template <int D>
-__global__ void __launch_bounds__(256) quantize_kernel(const __nv_bfloat16* __restrict__ x,
-                                                       const float* __restrict__ mu, int mu_mode,
-                                                       int8_t* __restrict__ xq, float* __restrict__ scale, int T) {
+__global__ void __launch_bounds__(256) quantize_kernel(QuantJobs jobs, int T) {
+  // blockIdx.y selects the tensor (Q, K, V): one launch for all three psi passes
+  const QuantJob& job = jobs.j[blockIdx.y];
+  const __nv_bfloat16* __restrict__ x = job.x;
+  const float* __restrict__ mu = job.mu;
+  const int mu_mode = job.mu_mode;
+  int8_t* __restrict__ xq = job.xq;
+  float* __restrict__ scale = job.scale;
   constexpr int kPerThread = kBlk * D / 256;      // 64 (D=128) or 32 (D=64)
   constexpr int kIters = kPerThread / kVec;       // 8 or 4
   constexpr int kGroups = D / kVec;               // 16 or 8 column groups per row
@@ -244,8 +258,11 @@ __global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16*
 }  // namespace
 
 cudaError_t launch_colsum(const __nv_bfloat16* x, double* part, int BH, int N, int d, cudaStream_t s) {
-  int n_items = BH * (N / kBlk) * (d / kVec);
-  colsum_kernel<<<(n_items + 127) / 128, 128, 0, s>>>(x, part, N, d, n_items);
+  const unsigned grid = (unsigned)(BH * (N / kBlk));
+  if (d == 128)
+    colsum_kernel<128><<<grid, 256, 0, s>>>(x, part);
+  else
+    colsum_kernel<64><<<grid, 256, 0, s>>>(x, part);
   return cudaGetLastError();
 }
 
@@ -261,14 +278,13 @@ cudaError_t launch_blockmean(const double* part, float* mu_q, int BH, int N, int
   return cudaGetLastError();
 }
 
-cudaError_t launch_quantize(const __nv_bfloat16* x, const float* mu, int mu_mode, int8_t* xq, float* scale, int BH,
-                            int N, int d, cudaStream_t s) {
+cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int d, cudaStream_t s) {
   int T = N / kBlk;
-  unsigned grid = (unsigned)(BH * T);
+  dim3 grid((unsigned)(BH * T), (unsigned)njobs);
   if (d == 128)
-    quantize_kernel<128><<<grid, 256, 0, s>>>(x, mu, mu_mode, xq, scale, T);
+    quantize_kernel<128><<<grid, 256, 0, s>>>(jobs, T);
   else
-    quantize_kernel<64><<<grid, 256, 0, s>>>(x, mu, mu_mode, xq, scale, T);
+    quantize_kernel<64><<<grid, 256, 0, s>>>(jobs, T);
   return cudaGetLastError();
 }
 
