@@ -147,34 +147,46 @@ __global__ void __launch_bounds__(256) quantize_kernel(QuantJobs jobs, int T) {
 }
 
 // ---------------------------------------------------------------- Q-smoothing bias
-// bias[bh][i][n] = sum_c mu_Q[bh][i][c] * fl32(K[n][c] - mu_K[c]), fp32 in fixed c order.
-// One CTA per (bh, 128-key block); K_sm staged in smem (padded rows).
+// bias[bh][i][n] = sum_c mu_Q[bh][i][c] * fl32(K[n][c] - mu_K[c]), fp32 FMAs in fixed c order
+// (reading A13).  CTA = (bh, 128-key block, group of kBiasI query blocks); thread = key n holds
+// its smoothed K row in registers, the group's mu_Q rows are broadcast from shared memory.
+constexpr int kBiasI = 16;
 template <int D>
 __global__ void __launch_bounds__(128) qsmooth_bias_kernel(const __nv_bfloat16* __restrict__ k,
                                                            const float* __restrict__ mu_k,
                                                            const float* __restrict__ mu_q, float* __restrict__ bias,
                                                            int N) {
-  extern __shared__ float sm[];
-  float* ks = sm;                      // [128][D+1]
-  float* mq = sm + kBlk * (D + 1);     // [D]
+  __shared__ float4 mq[kBiasI][D / 4];
   const int T = N / kBlk;
   const long long blk = blockIdx.x;    // bh * T + jn
   const int bh = (int)(blk / T), jn = (int)(blk % T);
-  const __nv_bfloat16* kb = k + blk * kBlk * D;
-  for (int e = threadIdx.x; e < kBlk * D; e += blockDim.x) {
-    int r = e / D, c = e % D;
-    ks[r * (D + 1) + c] = __fsub_rn(__bfloat162float(kb[e]), mu_k[(size_t)bh * D + c]);
+  const int i0 = blockIdx.y * kBiasI, ni = min(kBiasI, T - i0);
+  const int n = threadIdx.x;
+  for (int e = threadIdx.x; e < ni * (D / 4); e += blockDim.x)
+    mq[e / (D / 4)][e % (D / 4)] = reinterpret_cast<const float4*>(mu_q + ((size_t)bh * T + i0) * D)[e];
+  float ks[D];
+  const __nv_bfloat16* krow = k + (blk * kBlk + n) * D;
+  const float* mk = mu_k + (size_t)bh * D;
+#pragma unroll
+  for (int c = 0; c < D; c += kVec) {
+    float f[kVec];
+    load_bf16x8(krow + c, f);
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) ks[c + e] = __fsub_rn(f[e], mk[c + e]);
   }
   __syncthreads();
-  const int n = threadIdx.x;
-  for (int i = 0; i < T; ++i) {
-    for (int c = threadIdx.x; c < D; c += blockDim.x) mq[c] = mu_q[((size_t)bh * T + i) * D + c];
-    __syncthreads();
+  float* out = bias + ((size_t)bh * T + i0) * N + (size_t)jn * kBlk + n;
+  for (int ii = 0; ii < ni; ++ii) {
     float acc = 0.f;
-#pragma unroll 8
-    for (int c = 0; c < D; ++c) acc = fmaf(mq[c], ks[n * (D + 1) + c], acc);
-    bias[((size_t)bh * T + i) * N + (size_t)jn * kBlk + n] = acc;
-    __syncthreads();
+#pragma unroll
+    for (int c4 = 0; c4 < D / 4; ++c4) {
+      const float4 m4 = mq[ii][c4];
+      acc = fmaf(m4.x, ks[4 * c4], acc);
+      acc = fmaf(m4.y, ks[4 * c4 + 1], acc);
+      acc = fmaf(m4.z, ks[4 * c4 + 2], acc);
+      acc = fmaf(m4.w, ks[4 * c4 + 3], acc);
+    }
+    out[(size_t)ii * N] = acc;
   }
 }
 
@@ -290,15 +302,12 @@ cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int
 
 cudaError_t launch_qsmooth_bias(const __nv_bfloat16* k, const float* mu_k, const float* mu_q, float* bias, int BH,
                                 int N, int d, cudaStream_t s) {
-  unsigned grid = (unsigned)(BH * (N / kBlk));
-  size_t smem = (size_t)(kBlk * (d + 1) + d) * sizeof(float);
-  if (d == 128) {
-    cudaFuncSetAttribute(qsmooth_bias_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    qsmooth_bias_kernel<128><<<grid, 128, smem, s>>>(k, mu_k, mu_q, bias, N);
-  } else {
-    cudaFuncSetAttribute(qsmooth_bias_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    qsmooth_bias_kernel<64><<<grid, 128, smem, s>>>(k, mu_k, mu_q, bias, N);
-  }
+  const int T = N / kBlk;
+  dim3 grid((unsigned)(BH * T), (unsigned)((T + kBiasI - 1) / kBiasI));
+  if (d == 128)
+    qsmooth_bias_kernel<128><<<grid, 128, 0, s>>>(k, mu_k, mu_q, bias, N);
+  else
+    qsmooth_bias_kernel<64><<<grid, 128, 0, s>>>(k, mu_k, mu_q, bias, N);
   return cudaGetLastError();
 }
 
