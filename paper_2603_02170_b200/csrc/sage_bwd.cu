@@ -41,28 +41,35 @@ template <int D>
 struct BwdSmem {
   static constexpr int kStages = D == 64 ? 3 : 2;
   static constexpr int kTile = kBlk * D;           // int8 [128][D]
+  // d=128: bf16 dO_i gets its own single buffer (it is only read by the dP MMA, early in a
+  // tile), which frees the shared memory for the dQ reduce staging below
+  static constexpr bool kSplitDO = D == 128;
   static constexpr int kK = 0;                     // K^_j
   static constexpr int kV = kK + kTile;            // V_j bf16: D/64 panels of [128][64]
-  static constexpr int kStage = kV + 2 * kTile;    // per stage: Q^_i, dO_i (bf16 panels), dO^_i, L2, delta
-  static constexpr int kSQ = 0, kSDO = kTile, kSDOQ = 3 * kTile, kSL = 4 * kTile, kSDelta = 4 * kTile + 512;
-  static constexpr int kStageBytes = 4 * kTile + 1024;
-  static constexpr int kPt = kStage + kStages * kStageBytes;  // P^^T [128 kv][128 q]
+  static constexpr int kStage = kV + 2 * kTile;    // per stage: Q^_i, dO^_i, L2, delta (+ dO_i bf16 for d=64)
+  static constexpr int kSQ = 0, kSDOQ = kTile, kSL = 2 * kTile, kSDelta = 2 * kTile + 512, kSDO = 2 * kTile + 1024;
+  static constexpr int kStageBytes = 2 * kTile + 1024 + (kSplitDO ? 0 : 2 * kTile);
+  static constexpr int kDO = kStage + kStages * kStageBytes;    // d=128: dO_i bf16 panels
+  static constexpr int kPt = kDO + (kSplitDO ? 2 * kTile : 0);  // P^^T [128 kv][128 q]
   static constexpr int kDSt = kPt + kBlk * kBlk;              // dS^^T [128 kv][128 q]
   static constexpr int kRed = kDSt + kBlk * kBlk;             // [2][8] floats (cross-warp max)
   static constexpr int kScl = kRed + 64;                      // [4][2] floats {s_P, s_dS} per tile slot
   static constexpr int kRowSum = kScl + 32;                   // [2 slots][2 wg][128] int (Q-smoothing colsum of dS^)
   static constexpr int kScQ = kRowSum + 4 * kBlk * 4;          // s_Q[bh][0..T), s_dO[bh][0..T) (T <= kMaxT)
   static constexpr int kScDO = kScQ + kMaxT * 4;
-  // dQ tile staging for the TMA reduce-add (d=64: 2 buffers x [2 boxes][128][32] fp32, 128B-swizzled)
-  static constexpr bool kDqTma = D == 64;
+  // dQ staging for the TMA reduce-add: 2 buffers of [kDqBoxes][128 rows][32 cols] fp32, 128B-swizzled;
+  // d=64 stages a whole tile per round, d=128 a quarter tile per round (4 rounds per tile)
   static constexpr int kDqBox = kBlk * 32 * 4;
+  static constexpr int kDqBoxes = D == 64 ? 2 : 1;
+  static constexpr int kDqRounds = (D / 32) / kDqBoxes;
   static constexpr int kDq = (kScDO + kMaxT * 4 + 1023) / 1024 * 1024;
-  static constexpr int kBar = kDq + (kDqTma ? 2 * (D / 32) * kDqBox : 0);
-  static constexpr int kNumBars = 1 + 2 * kStages + 8;
+  static constexpr int kBar = kDq + 2 * kDqBoxes * kDqBox;
+  static constexpr int kNumBars = 1 + 2 * kStages + 10;
   static constexpr int kTmemSlot = kBar + kNumBars * 8;
   static constexpr int kBytes = kTmemSlot + 16;
   static constexpr int kAlloc = kBytes + 1024;
-  static constexpr uint32_t kStageTx = 4 * kTile + 1024;
+  static constexpr uint32_t kStageTx = kStageBytes;
+  static constexpr uint32_t kDOTx = 2 * kTile;
 };
 
 // Profiling hooks (timeline + ablation switches) exist only in the SAGE_TRACE=1 build
@@ -133,6 +140,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* ds_ready = b0 + 5;     // compute -> MMA (8 warps): dS^^T written, dP^T read
   uint64_t* dv_drained = b0 + 6;   // drain -> MMA (4 warps)
   uint64_t* dkq_drained = b0 + 7;
+  uint64_t* do_full = b0 + 8;      // d=128 dO buffer: TMA -> MMA
+  uint64_t* do_empty = b0 + 9;     // d=128 dO buffer: MMA (dP done) -> TMA
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
   float* red = reinterpret_cast<float*>(smem + L::kRed);
   float* scl = reinterpret_cast<float*>(smem + L::kScl);
@@ -160,6 +169,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = 0; b < 4; ++b) mbar_init(b0 + b, 1);
     for (int b = 4; b < 6; ++b) mbar_init(b0 + b, kComputeWarps);
     for (int b = 6; b < 8; ++b) mbar_init(b0 + b, kDrainWarps);
+    mbar_init(do_full, 1);
+    mbar_init(do_empty, 1);
     fence_mbar_init();
   }
   for (int t = threadIdx.x; t < T; t += kThreads) {
@@ -203,13 +214,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           TR(14, it);
           mbar_expect_tx(q_full + s, L::kStageTx);
           tma_load_2d(st + L::kSQ, &tm_q, q_full + s, 0, qrow);
+          if constexpr (!L::kSplitDO) {
 #pragma unroll
-          for (int p = 0; p < D / 64; ++p) tma_load_2d(st + L::kSDO + p * 16384, &tm_do, q_full + s, p * 64, qrow);
+            for (int p = 0; p < D / 64; ++p) tma_load_2d(st + L::kSDO + p * 16384, &tm_do, q_full + s, p * 64, qrow);
+          }
           tma_load_2d(st + L::kSDOQ, &tm_doq, q_full + s, 0, qrow);
           bulk_load(st + L::kSL, l2g + qrow, 512, q_full + s);
           bulk_load(st + L::kSDelta, deltag + qrow, 512, q_full + s);
         }
         __syncwarp();
+        if constexpr (L::kSplitDO) {
+          mbar_wait(do_empty, (it & 1) ^ 1);  // dP_{it-1} has read the dO buffer
+          if (elect_one()) {
+            mbar_expect_tx(do_full, L::kDOTx);
+#pragma unroll
+            for (int p = 0; p < D / 64; ++p) tma_load_2d(smem + L::kDO + p * 16384, &tm_do, do_full, p * 64, qrow);
+          }
+          __syncwarp();
+        }
       }
     } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer (whole warp, one elected lane issues)
@@ -239,14 +261,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       };
       auto issue_dp = [&](int it) {  // stage `it` was already waited for by issue_s(it)
+        if constexpr (L::kSplitDO) {
+          mbar_wait(do_full, it & 1);
+          tc_fence_after();
+        }
         if (elect_one()) {
-          const uint32_t do_addr = st0 + soff(it) + L::kSDO;
+          const uint32_t do_addr = L::kSplitDO ? smem_u32(smem + L::kDO) : st0 + soff(it) + L::kSDO;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk / 4) * 16384 + (kk % 4) * 32;
             mma_bf16(tDP, desc_kmajor(v_addr + off, 128, 0), desc_kmajor(do_addr + off, 128, 0), kIdDP, kk > 0);
           }
           mma_commit(dp_full);
+          if constexpr (L::kSplitDO) mma_commit(do_empty);
           TR(2, it);
         }
         __syncwarp();
@@ -583,49 +610,39 @@ if (cm) {
 
       // dQ_i += tile * s_dS * s_K * tau, fp32 reduction across key blocks (line 10)
       if (threadIdx.x == 384) TR(12, it);
-      if constexpr (L::kDqTma) {
-        // scaled tile -> swizzled smem staging (double-buffered) -> one TMA reduce-add per 32-col box
-        uint8_t* stage = smem + L::kDq + (it & 1) * (D / 32) * L::kDqBox;
-        if (threadIdx.x == 384 && it >= 2) bulk_wait_read<1>();  // reduce of tile it-2 has read `stage`
-        named_bar_sync(3, 128);
-        if (!(ablate & 1)) {
-          const float s_ds = scl[(it & 3) * 2 + 1];
-          const float2 f = make_float2(s_ds * sk * tau, s_ds * sk * tau);
-#pragma unroll
-          for (int c0 = 0; c0 < D; c0 += 32) {
-            uint32_t v[32];
-            tmem_ld32(tDQ + c0 + lane_off, v);
-            tmem_wait_ld();
-            uint8_t* box = stage + (c0 / 32) * L::kDqBox;
-#pragma unroll
-            for (int e = 0; e < 32; e += 4) {
-              float2 a = fmul2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f);
-              float2 b = fmul2(make_float2(__int2float_rn((int)v[e + 2]), __int2float_rn((int)v[e + 3])), f);
-              *reinterpret_cast<float4*>(box + sw_offset(r, e / 4, 128)) = make_float4(a.x, a.y, b.x, b.y);
-            }
-          }
-        }
-        fence_proxy_async_smem();
-        named_bar_sync(3, 128);
-        if (threadIdx.x == 384 && !(ablate & 4)) {
-#pragma unroll
-          for (int b = 0; b < D / 32; ++b) tma_reduce_add_2d(&tm_dq, stage + b * L::kDqBox, b * 32, bh * N + i * kBlk);
-          bulk_commit();
-        }
-      } else if (!(ablate & 1)) {
+      {
+        // scaled tile -> swizzled smem staging (2 buffers) -> TMA reduce-add, one box per 32 columns
         const float s_ds = scl[(it & 3) * 2 + 1];
         const float2 f = make_float2(s_ds * sk * tau, s_ds * sk * tau);
-        float* grow = dq_acc + ((size_t)bh * N + (size_t)i * kBlk + r) * D;
 #pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tDQ + c0 + lane_off, v);
-          tmem_wait_ld();
+        for (int qq = 0; qq < L::kDqRounds; ++qq) {
+          const int rnd = it * L::kDqRounds + qq;
+          uint8_t* stage = smem + L::kDq + (rnd & 1) * L::kDqBoxes * L::kDqBox;
+          if (threadIdx.x == 384 && rnd >= 2) bulk_wait_read<1>();  // round rnd-2 has read `stage`
+          named_bar_sync(3, 128);
+          if (!(ablate & 1)) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 4) {
-            float2 a = fmul2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f);
-            float2 b = fmul2(make_float2(__int2float_rn((int)v[e + 2]), __int2float_rn((int)v[e + 3])), f);
-            if (!(ablate & 4)) red_add_v4(grow + c0 + e, a.x, a.y, b.x, b.y);
+            for (int bx = 0; bx < L::kDqBoxes; ++bx) {
+              const int c0 = (qq * L::kDqBoxes + bx) * 32;
+              uint32_t v[32];
+              tmem_ld32(tDQ + c0 + lane_off, v);
+              tmem_wait_ld();
+              uint8_t* box = stage + bx * L::kDqBox;
+#pragma unroll
+              for (int e = 0; e < 32; e += 4) {
+                float2 a = fmul2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f);
+                float2 b = fmul2(make_float2(__int2float_rn((int)v[e + 2]), __int2float_rn((int)v[e + 3])), f);
+                *reinterpret_cast<float4*>(box + sw_offset(r, e / 4, 128)) = make_float4(a.x, a.y, b.x, b.y);
+              }
+            }
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(3, 128);
+          if (threadIdx.x == 384 && !(ablate & 4)) {
+#pragma unroll
+            for (int bx = 0; bx < L::kDqBoxes; ++bx)
+              tma_reduce_add_2d(&tm_dq, stage + bx * L::kDqBox, (qq * L::kDqBoxes + bx) * 32, bh * N + i * kBlk);
+            bulk_commit();
           }
         }
       }
@@ -633,9 +650,7 @@ if (cm) {
       warp_arrive(dkq_drained);
       if (threadIdx.x == 384) TR(13, it);
     }
-    if constexpr (L::kDqTma) {
-      if (threadIdx.x == 384) bulk_wait_all();  // staging smem must outlive the in-flight reduces
-    }
+    if (threadIdx.x == 384) bulk_wait_all();  // staging smem must outlive the in-flight reduces
     // epilogue: dK_j, dV_j rows -> bf16
     const size_t orow = ((size_t)krow + r) * D;
 #pragma unroll
