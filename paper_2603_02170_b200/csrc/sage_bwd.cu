@@ -47,8 +47,10 @@ struct BwdSmem {
   static constexpr int kK = 0;                     // K^_j
   static constexpr int kV = kK + kTile;            // V_j bf16: D/64 panels of [128][64]
   static constexpr int kStage = kV + 2 * kTile;    // per stage: Q^_i, dO^_i, L2, delta (+ dO_i bf16 for d=64)
-  static constexpr int kSQ = 0, kSDOQ = kTile, kSL = 2 * kTile, kSDelta = 2 * kTile + 512, kSDO = 2 * kTile + 1024;
-  static constexpr int kStageBytes = 2 * kTile + 1024 + (kSplitDO ? 0 : 2 * kTile);
+  // d=128 stages also carry mu_Qi (Q-smoothing dK bias branch) after delta
+  static constexpr int kSQ = 0, kSDOQ = kTile, kSL = 2 * kTile, kSDelta = 2 * kTile + 512, kSMu = 2 * kTile + 1024;
+  static constexpr int kSDO = 2 * kTile + 1024;  // d=64 only (1024-aligned for the 128B-swizzled panel)
+  static constexpr int kStageBytes = kSplitDO ? 2 * kTile + 2048 : 4 * kTile + 1024;
   static constexpr int kDO = kStage + kStages * kStageBytes;    // d=128: dO_i bf16 panels
   static constexpr int kPt = kDO + (kSplitDO ? 2 * kTile : 0);  // P^^T [128 kv][128 q]
   static constexpr int kDSt = kPt + kBlk * kBlk;              // dS^^T [128 kv][128 q]
@@ -64,11 +66,11 @@ struct BwdSmem {
   static constexpr int kDqRounds = (D / 32) / kDqBoxes;
   static constexpr int kDq = (kScDO + kMaxT * 4 + 1023) / 1024 * 1024;
   static constexpr int kBar = kDq + 2 * kDqBoxes * kDqBox;
-  static constexpr int kNumBars = 1 + 2 * kStages + 10;
+  static constexpr int kNumBars = 1 + 2 * kStages + 11;
   static constexpr int kTmemSlot = kBar + kNumBars * 8;
   static constexpr int kBytes = kTmemSlot + 16;
   static constexpr int kAlloc = kBytes + 1024;
-  static constexpr uint32_t kStageTx = kStageBytes;
+  static constexpr uint32_t kStageTx = kSplitDO ? 2 * kTile + 1024 : 4 * kTile + 1024;  // + D*4 with mu_Q
   static constexpr uint32_t kDOTx = 2 * kTile;
 };
 
@@ -142,6 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* dkq_drained = b0 + 7;
   uint64_t* do_full = b0 + 8;      // d=128 dO buffer: TMA -> MMA
   uint64_t* do_empty = b0 + 9;     // d=128 dO buffer: MMA (dP done) -> TMA
+  uint64_t* dq_drained = b0 + 10;  // drain -> MMA (4 warps): dQ tile read (dkq_drained: dK tile read)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
   float* red = reinterpret_cast<float*>(smem + L::kRed);
   float* scl = reinterpret_cast<float*>(smem + L::kScl);
@@ -162,15 +165,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
+    // a stage is released by the dK/dQ MMA commit, and (when it carries mu_Qi) by the drain
+    // warps once their dK drain has read mu_Qi
+    constexpr uint32_t kEmptyCount = (L::kSplitDO && QSMOOTH) ? 1 + kDrainWarps : 1;
     for (int s = 0; s < kStages; ++s) {
       mbar_init(q_full + s, 1);
-      mbar_init(q_empty + s, 1);
+      mbar_init(q_empty + s, kEmptyCount);
     }
     for (int b = 0; b < 4; ++b) mbar_init(b0 + b, 1);
     for (int b = 4; b < 6; ++b) mbar_init(b0 + b, kComputeWarps);
     for (int b = 6; b < 8; ++b) mbar_init(b0 + b, kDrainWarps);
     mbar_init(do_full, 1);
     mbar_init(do_empty, 1);
+    mbar_init(dq_drained, kDrainWarps);
     fence_mbar_init();
   }
   for (int t = threadIdx.x; t < T; t += kThreads) {
@@ -212,7 +219,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(q_empty + s, ((it / kStages) & 1) ^ 1);
         if (elect_one()) {
           TR(14, it);
-          mbar_expect_tx(q_full + s, L::kStageTx);
+          const bool mu_in_stage = L::kSplitDO && QSMOOTH;
+          mbar_expect_tx(q_full + s, L::kStageTx + (mu_in_stage ? D * 4 : 0));
+          if (mu_in_stage) bulk_load(st + L::kSMu, mu_q + ((size_t)bh * T + i) * D, D * 4, q_full + s);
           tma_load_2d(st + L::kSQ, &tm_q, q_full + s, 0, qrow);
           if constexpr (!L::kSplitDO) {
 #pragma unroll
@@ -323,7 +332,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             issue_dp(it + 1);
           }
           mbar_wait(ds_ready, ph);
-          if (it > 0) mbar_wait(dkq_drained, pph);
+          if (it > 0) {
+            mbar_wait(dkq_drained, pph);
+            mbar_wait(dq_drained, pph);
+          }
           if (lane == 0) TR(20, it);
           tc_fence_after();
           issue_dkdq(it);
@@ -339,11 +351,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             issue_s(it + 1);
           }
           mbar_wait(ds_ready, ph);
-          if (it > 0) mbar_wait(dkq_drained, pph);
+          if (it > 0) mbar_wait(dq_drained, pph);  // dQ slot; the dK slot (dP's) was freed at p_ready
           tc_fence_after();
           issue_dkdq(it);
           if (more) {
-            mbar_wait(dkq_drained, ph);
+            mbar_wait(dkq_drained, ph);  // dK_i read out of dP's columns
             tc_fence_after();
             issue_dp(it + 1);
           }
@@ -534,25 +546,33 @@ if (cm) {
         const float s_p = scl[(it & 3) * 2];
         const float2 f = make_float2(s_p * sdo, s_p * sdo);
         if constexpr (kAlias) {
-          // fp32 accumulator in TMEM: 16-column chunks keep the drain within its register budget
+          // fp32 accumulator in TMEM; 8-column chunks, loads double-buffered
+          uint32_t vb[2][8], ab[2][8];
+          tmem_ld8(tDV + lane_off, vb[0]);
+          tmem_ld8(tDVacc + lane_off, ab[0]);
+          tmem_wait_ld();
 #pragma unroll
-          for (int c0 = 0; c0 < D; c0 += 16) {
-            uint32_t v[16], a[16];
-            tmem_ld16(tDV + c0 + lane_off, v);
-            tmem_ld16(tDVacc + c0 + lane_off, a);
-            tmem_wait_ld();
+          for (int c = 0; c < D / 8; ++c) {
+            uint32_t(&v)[8] = vb[c & 1];
+            uint32_t(&a)[8] = ab[c & 1];
+            if (c + 1 < D / 8) {
+              if (c >= 1) tmem_wait_st();  // the other buffer's accumulator store has read its registers
+              tmem_ld8(tDV + (c + 1) * 8 + lane_off, vb[(c + 1) & 1]);
+              tmem_ld8(tDVacc + (c + 1) * 8 + lane_off, ab[(c + 1) & 1]);
+            }
             if (it == 0) {
 #pragma unroll
-              for (int e = 0; e < 16; ++e) a[e] = 0u;
+              for (int e = 0; e < 8; ++e) a[e] = 0u;
             }
 #pragma unroll
-            for (int e = 0; e < 16; e += 2) {
+            for (int e = 0; e < 8; e += 2) {
               float2 x = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f,
                                make_float2(__uint_as_float(a[e]), __uint_as_float(a[e + 1])));
               a[e] = __float_as_uint(x.x);
               a[e + 1] = __float_as_uint(x.y);
             }
-            tmem_st16(tDVacc + c0 + lane_off, a);
+            tmem_st8(tDVacc + c * 8 + lane_off, a);
+            if (c + 1 < D / 8) tmem_wait_ld();
           }
         } else {
 #pragma unroll
@@ -586,27 +606,34 @@ if (cm) {
         if constexpr (QSMOOTH) {
           const int* rs = rowsum_s + (it & 1) * kBlk * 2;
           fb = tau * s_ds * (float)(rs[r] + rs[kBlk + r]);
-          muq = mu_q + ((size_t)bh * T + i) * D;
+          muq = L::kSplitDO ? reinterpret_cast<const float*>(smem + L::kStage + (it % kStages) * L::kStageBytes + L::kSMu)
+                            : mu_q + ((size_t)bh * T + i) * D;
         }
+        uint32_t kb[2][16];
+        tmem_ld16(tDK + lane_off, kb[0]);
+        tmem_wait_ld();
 #pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tDK + c0 + lane_off, v);
-          tmem_wait_ld();
+        for (int c = 0; c < D / 16; ++c) {
+          uint32_t(&v)[16] = kb[c & 1];
+          if (c + 1 < D / 16) tmem_ld16(tDK + (c + 1) * 16 + lane_off, kb[(c + 1) & 1]);
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float2 acc = make_float2(dk_acc[c0 + e], dk_acc[c0 + e + 1]);
+          for (int e = 0; e < 16; e += 2) {
+            const int cc = c * 16 + e;
+            float2 acc = make_float2(dk_acc[cc], dk_acc[cc + 1]);
             if constexpr (QSMOOTH) {
-              const float2 m2 = *reinterpret_cast<const float2*>(muq + c0 + e);
+              const float2 m2 = *reinterpret_cast<const float2*>(muq + cc);
               acc = ffma2(make_float2(fb, fb), m2, acc);
             }
             float2 x = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f, acc);
-            dk_acc[c0 + e] = x.x;
-            dk_acc[c0 + e + 1] = x.y;
+            dk_acc[cc] = x.x;
+            dk_acc[cc + 1] = x.y;
           }
+          if (c + 1 < D / 16) tmem_wait_ld();
         }
       }
       tc_fence_before();
+      warp_arrive(dkq_drained);  // dK tile read (d=128: dP's columns may take dP_{i+1})
+      if constexpr (L::kSplitDO && QSMOOTH) warp_arrive(q_empty + it % kStages);  // mu_Qi read
 
       // dQ_i += tile * s_dS * s_K * tau, fp32 reduction across key blocks (line 10)
       if (threadIdx.x == 384) TR(12, it);
@@ -647,7 +674,7 @@ if (cm) {
         }
       }
       tc_fence_before();
-      warp_arrive(dkq_drained);
+      warp_arrive(dq_drained);
       if (threadIdx.x == 384) TR(13, it);
     }
     if (threadIdx.x == 384) bulk_wait_all();  // staging smem must outlive the in-flight reduces
