@@ -121,13 +121,14 @@ def dist_setup(args):
 
 
 def traffic_from_profile(cfg_name):
-    """dram bytes per K4 launch from the committed ncu --set full summary, if any."""
+    """(dram bytes, report name) per K4 launch from the committed ncu --set full summary
+    (profiles/ncu_summary.json, written by scripts/ncu_summary.py json), if any."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
-        d = json.load(open(path))
-        return d["kernels"]["sage_bwd"][cfg_name]["dram_bytes"]
+        d = json.load(open(path))["kernels"]["sage_bwd"][cfg_name]
+        return d["dram_bytes"], d["report"]
     except Exception:
-        return None
+        return None, None
 
 
 # ---------------------------------------------------------------------- CPU oracle (baseline / reference arm)
@@ -291,9 +292,11 @@ def main():
         bwd_ms = prof["bwd_ms"] / max(1, prof["n_bwd"])
         fwd_ms = prof["fwd_ms"] / max(1, prof["n_fwd"])
         achieved = bwd_kernel_ops(c) / (bwd_ms * 1e-3) / 1e12
+        traffic, traffic_src = traffic_from_profile(c.name)
         roof = {"bound": "tensor", "kernel": "sage_bwd_kernel (K4)", "achieved": achieved,
                 "peak": pk["bwd_mixed"], "unit": "TFLOP/s", "frac": achieved / pk["bwd_mixed"],
-                "traffic": traffic_from_profile(c.name),
+                "traffic": traffic, "traffic_note": f"ncu dram__bytes_read+write.sum per launch, profiles/{traffic_src}"
+                if traffic else None,
                 "peak_note": f"{pk['src']} bf16 {pk['bf16']} TF/s x 5/3 (8/10 of K4's work INT8 at 2x bf16, 2/10 bf16)",
                 "kernel_ms": bwd_ms, "share_of_step": bwd_ms / ms, "fwd_kernel_ms": fwd_ms,
                 "fwd_share_of_step": fwd_ms / ms}

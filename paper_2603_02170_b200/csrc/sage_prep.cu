@@ -25,6 +25,17 @@ __device__ __forceinline__ void load_bf16x8(const __nv_bfloat16* p, float (&f)[8
   }
 }
 
+// q = RNE(fl32(x * inv)) for four values, packed as int8x4.  fl32(y + 1.5*2^23) holds RNE(y) in
+// its low bits (|y| < 2^22), so the rounding is an FADD instead of an XU-pipe F2I; |y| <= 127(1+2^-23)
+// because inv = fl32(127/amax), hence |RNE(y)| <= 127 and no clamp is needed (readings A1, A2, A4).
+__device__ __forceinline__ uint32_t quant4(const float* x, float inv) {
+  constexpr float kMagic = 12582912.0f;
+  uint32_t b[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) b[e] = __float_as_uint(__fadd_rn(__fmul_rn(x[e], inv), kMagic));
+  return __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -135,13 +146,9 @@ __global__ void __launch_bounds__(256) quantize_kernel(QuantJobs jobs, int T) {
 #pragma unroll
   for (int it = 0; it < kIters; ++it) {
     int r = r0 + it * kRowsPerPass;
-    uint32_t w[2] = {0u, 0u};
+    uint32_t w[2];
 #pragma unroll
-    for (int e = 0; e < kVec; ++e) {
-      int qv = __float2int_rn(__fmul_rn(v[it][e], inv));
-      qv = max(-127, min(127, qv));
-      w[e / 4] |= (uint32_t)(qv & 0xFF) << (8 * (e % 4));
-    }
+    for (int h = 0; h < 2; ++h) w[h] = quant4(v[it] + 4 * h, inv);
     *reinterpret_cast<uint2*>(qb + (size_t)r * D + g * kVec) = make_uint2(w[0], w[1]);
   }
 }
@@ -241,13 +248,9 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
 #pragma unroll
   for (int it = 0; it < kIters; ++it) {
     const int r = r0 + it * kRowsPerPass;
-    uint32_t w[2] = {0u, 0u};
+    uint32_t w[2];
 #pragma unroll
-    for (int e = 0; e < kVec; ++e) {
-      int qv = __float2int_rn(__fmul_rn(v[it][e], inv));
-      qv = max(-127, min(127, qv));
-      w[e / 4] |= (uint32_t)(qv & 0xFF) << (8 * (e % 4));
-    }
+    for (int h = 0; h < 2; ++h) w[h] = quant4(v[it] + 4 * h, inv);
     *reinterpret_cast<uint2*>(do_q + base + (size_t)r * D + g * kVec) = make_uint2(w[0], w[1]);
   }
 }
