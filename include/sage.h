@@ -113,7 +113,8 @@ SAGE_API sage_status sage_ws_get_view(const sage_params* p, int backward, void* 
  * TMEM code the fused kernels use.  mode 0: int32 D = A[128][K] . B[N][K]^T with both
  * operands K-major (K in {64,128}, N = 128);  mode 1: A K-major [128][128] written by
  * threads (P^ path), B MN-major [128][N] (N in {64,128}); mode 2: A MN-major [K=128][M=128],
- * B MN-major [128][N]; mode 3: fp32 D = A . B^T, bf16 K-major operands [128][K], [128][K].
+ * B MN-major [128][N]; mode 3: fp32 D = A . B^T, bf16 K-major operands [128][K], [128][K];
+ * modes 4 / 5: as 1 / 3 with the A operand read from TMEM (written there by threads).
  * a, b, d: device pointers to row-major host-order arrays as described (int8/bf16 in, int32/fp32 out). */
 SAGE_API sage_status sage_debug_umma(int mode, int K, int N, const void* a, const void* b, void* d, void* stream);
 

@@ -401,7 +401,7 @@ sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const f
   if (!make_tmap_2d(&a.tm_q, q8, kU8, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_k, k8, kU8, rows, d, kBlk, d) ||
       !make_tmap_2d(&a.tm_doq, do8, kU8, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_v, v, kBF16, rows, d, kBlk, 64) ||
       !make_tmap_2d(&a.tm_do, dO, kBF16, rows, d, kBlk, 64) ||
-      !make_tmap_2d(&a.tm_dq, dqacc, kF32, rows, d, kBlk, 32))
+      !make_tmap_2d(&a.tm_dq, dqacc, kF32, rows, d, 32, 32))
     return cuda_fail(cudaErrorInvalidValue);
   cudaError_t e;
   // K3: delta, psi(dO), L*log2(e), zero dQ accumulator (Alg. 2 lines 2, 6)
@@ -441,9 +441,10 @@ sage_status sage_debug_trace(void* host_out, size_t bytes) {
 }
 
 sage_status sage_debug_umma(int mode, int K, int N, const void* a, const void* b, void* d, void* stream) {
-  if (mode < 0 || mode > 3 || !a || !b || !d) return SAGE_ERR_INVALID_VALUE;
-  if ((mode == 0 || mode == 3) && K != 64 && K != 128) return SAGE_ERR_INVALID_VALUE;
-  if ((mode == 1 || mode == 2) && N != 64 && N != 128) return SAGE_ERR_INVALID_VALUE;
+  if (mode < 0 || mode > 5 || !a || !b || !d) return SAGE_ERR_INVALID_VALUE;
+  const bool kmode = mode == 0 || mode == 3 || mode == 5;
+  if (kmode && K != 64 && K != 128) return SAGE_ERR_INVALID_VALUE;
+  if (!kmode && N != 64 && N != 128) return SAGE_ERR_INVALID_VALUE;
   if (!aligned16(a) || !aligned16(b) || !aligned16(d)) return SAGE_ERR_MISALIGNED;
   sage_status st = check_arch();
   if (st != SAGE_OK) return st;
@@ -451,8 +452,8 @@ sage_status sage_debug_umma(int mode, int K, int N, const void* a, const void* b
   bool ok = true;
   if (mode == 0) {
     ok = make_tmap_2d(&ta, a, kU8, 128, K, 128, K) && make_tmap_2d(&tb, b, kU8, 128, K, 128, K);
-  } else if (mode == 3) {
-    ok = make_tmap_2d(&ta, a, kBF16, 128, K, 128, 64) && make_tmap_2d(&tb, b, kBF16, 128, K, 128, 64);
+  } else if (mode == 3 || mode == 5) {
+    ok = make_tmap_2d(&ta, mode == 3 ? a : b, kBF16, 128, K, 128, 64) && make_tmap_2d(&tb, b, kBF16, 128, K, 128, 64);
   } else {
     ok = make_tmap_2d(&tb, b, kU8, 128, N, 128, N);
     ta = tb;

@@ -39,7 +39,7 @@ constexpr int kMaxT = kMaxSeqLen / kBlk;
 
 template <int D>
 struct BwdSmem {
-  static constexpr int kStages = D == 64 ? 3 : 2;
+  static constexpr int kStages = D == 64 ? 4 : 2;
   static constexpr int kTile = kBlk * D;           // int8 [128][D]
   // d=128: bf16 dO_i gets its own single buffer (it is only read by the dP MMA, early in a
   // tile), which frees the shared memory for the dQ reduce staging below
@@ -53,25 +53,28 @@ struct BwdSmem {
   static constexpr int kStageBytes = kSplitDO ? 2 * kTile + 2048 : 4 * kTile + 1024;
   static constexpr int kDO = kStage + kStages * kStageBytes;    // d=128: dO_i bf16 panels
   static constexpr int kPt = kDO + (kSplitDO ? 2 * kTile : 0);  // P^^T [128 kv][128 q]
-  static constexpr int kDSt = kPt + kBlk * kBlk;              // dS^^T [128 kv][128 q]
+  static constexpr int kDSt = kPt + (D == 64 ? 0 : kBlk * kBlk);  // dS^^T [128 kv][128 q] (d=64: P^^T is in TMEM)
   static constexpr int kRed = kDSt + kBlk * kBlk;             // [2][8] floats (cross-warp max)
   static constexpr int kScl = kRed + 64;                      // [4][2] floats {s_P, s_dS} per tile slot
   static constexpr int kRowSum = kScl + 32;                   // [2 slots][2 wg][128] int (Q-smoothing colsum of dS^)
   static constexpr int kScQ = kRowSum + 4 * kBlk * 4;          // s_Q[bh][0..T), s_dO[bh][0..T) (T <= kMaxT)
   static constexpr int kScDO = kScQ + kMaxT * 4;
-  // dQ staging for the TMA reduce-add: 2 buffers of [kDqBoxes][128 rows][32 cols] fp32, 128B-swizzled;
-  // d=64 stages a whole tile per round, d=128 a quarter tile per round (4 rounds per tile)
-  static constexpr int kDqBox = kBlk * 32 * 4;
-  static constexpr int kDqBoxes = D == 64 ? 2 : 1;
+  // dQ staging for the TMA reduce-add, per drain warp (its 32 TMEM lanes = 32 query rows):
+  // 2 buffers of [kDqBoxes][32 rows][32 cols] fp32 boxes, 128B-swizzled; d=64 stages the warp's
+  // whole row slice per round, d=128 a quarter of it (4 rounds per tile).  No cross-warp barrier.
+  static constexpr int kDqBox = 32 * 32 * 4;
+  static constexpr int kDqBoxes = 1;
   static constexpr int kDqRounds = (D / 32) / kDqBoxes;
+  static constexpr int kDqWarp = 2 * kDqBoxes * kDqBox;  // per drain warp
   static constexpr int kDq = (kScDO + kMaxT * 4 + 1023) / 1024 * 1024;
-  static constexpr int kBar = kDq + 2 * kDqBoxes * kDqBox;
-  static constexpr int kNumBars = 1 + 2 * kStages + 11;
+  static constexpr int kBar = kDq + 4 * kDqWarp;
+  static constexpr int kNumBars = 1 + 2 * kStages + 13;
   static constexpr int kTmemSlot = kBar + kNumBars * 8;
   static constexpr int kBytes = kTmemSlot + 16;
   static constexpr int kAlloc = kBytes + 1024;
   static constexpr uint32_t kStageTx = kSplitDO ? 2 * kTile + 1024 : 4 * kTile + 1024;  // + D*4 with mu_Q
   static constexpr uint32_t kDOTx = 2 * kTile;
+  static_assert(kAlloc <= 232448, "K4 shared memory exceeds the 227 KB per-CTA limit");
 };
 
 // Profiling hooks (timeline + ablation switches) exist only in the SAGE_TRACE=1 build
@@ -95,15 +98,22 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// Order-preserving float <-> int map (monotone for all finite values and +-inf), so a float max is
+// one redux.sync.max.s32 instead of five shuffles.
+__device__ __forceinline__ int ford(float x) {
+  const int b = __float_as_int(x);
+  return b ^ ((b >> 31) & 0x7FFFFFFF);
+}
+__device__ __forceinline__ float ford_inv(int k) { return __int_as_float(k ^ ((k >> 31) & 0x7FFFFFFF)); }
+
 // max over the 256 compute threads (warps 4-11), named barrier `id`
-__device__ __forceinline__ float compute_max(float v, float* red, int cw, int id) {
-  v = warp_max(v);
-  if ((threadIdx.x & 31) == 0) red[cw] = v;
+__device__ __forceinline__ float compute_max(float v, int* red, int cw, int id) {
+  const int k = __reduce_max_sync(0xffffffffu, ford(v));
+  if ((threadIdx.x & 31) == 0) red[cw] = k;
   named_bar_sync(id, 256);
-  float r = fmax3(red[0], red[1], red[2]);
-  r = fmax3(r, red[3], red[4]);
-  r = fmax3(r, red[5], red[6]);
-  return fmaxf(r, red[7]);
+  const int4 a = *reinterpret_cast<const int4*>(red);
+  const int4 b = *reinterpret_cast<const int4*>(red + 4);
+  return ford_inv(max(max(max(a.x, a.y), max(a.z, a.w)), max(max(b.x, b.y), max(b.z, b.w))));
 }
 
 template <int D, bool CAUSAL, bool QSMOOTH>
@@ -145,8 +155,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* do_full = b0 + 8;      // d=128 dO buffer: TMA -> MMA
   uint64_t* do_empty = b0 + 9;     // d=128 dO buffer: MMA (dP done) -> TMA
   uint64_t* dq_drained = b0 + 10;  // drain -> MMA (4 warps): dQ tile read (dkq_drained: dK tile read)
+  uint64_t* v_tmem = b0 + 11;      // compute -> MMA (8 warps): V_j copied into TMEM (d=64)
+  uint64_t* s_free = b0 + 12;      // compute -> MMA (8 warps): S^T read into registers (d=64)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
-  float* red = reinterpret_cast<float*>(smem + L::kRed);
+  int* red = reinterpret_cast<int*>(smem + L::kRed);
   float* scl = reinterpret_cast<float*>(smem + L::kScl);
   float* sc_q = reinterpret_cast<float*>(smem + L::kScQ);
   float* sc_do = reinterpret_cast<float*>(smem + L::kScDO);
@@ -178,6 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(do_full, 1);
     mbar_init(do_empty, 1);
     mbar_init(dq_drained, kDrainWarps);
+    mbar_init(v_tmem, kComputeWarps);
+    mbar_init(s_free, kComputeWarps);
     fence_mbar_init();
   }
   for (int t = threadIdx.x; t < T; t += kThreads) {
@@ -195,6 +209,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tDK = kAlias ? tmem + 128 : tmem + 256 + D;
   const uint32_t tDQ = kAlias ? tmem + 256 : tmem + 256 + 2 * D;
   const uint32_t tDVacc = tmem + 384;  // d=128 only
+  // d=64: the A operands of dP^T (V_j, bf16) and dV (P^^T, int8) live in TMEM ("TS" MMAs), which
+  // takes 48 KB/tile of operand reads and P^ stores off the shared-memory port
+  constexpr bool kTS = D == 64;
+  const uint32_t tVa = tmem + 448;  // V_j bf16 [128][64]: 32 columns
+  const uint32_t tPa = tmem + 480;  // P^^T int8 [128 kv][128 q]: 32 columns
 
   if (warp < 4) {
     reg_dealloc<kRegProducer>();
@@ -279,7 +298,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk / 4) * 16384 + (kk % 4) * 32;
-            mma_bf16(tDP, desc_kmajor(v_addr + off, 128, 0), desc_kmajor(do_addr + off, 128, 0), kIdDP, kk > 0);
+            if constexpr (kTS)
+              mma_bf16_ts(tDP, tVa + kk * 8, desc_kmajor(do_addr + off, 128, 0), kIdDP, kk > 0);
+            else
+              mma_bf16(tDP, desc_kmajor(v_addr + off, 128, 0), desc_kmajor(do_addr + off, 128, 0), kIdDP, kk > 0);
           }
           mma_commit(dp_full);
           if constexpr (L::kSplitDO) mma_commit(do_empty);
@@ -291,8 +313,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elect_one()) {
           const uint32_t doq_addr = st0 + soff(it) + L::kSDOQ;
 #pragma unroll
-          for (int kk = 0; kk < kBlk / 32; ++kk)
-            mma_i8(tDV, desc_kmajor(pt_addr, 128, kk * 32), desc_mnmajor(doq_addr, D, kk * 32), kIdDV, kk > 0);
+          for (int kk = 0; kk < kBlk / 32; ++kk) {
+            if constexpr (kTS)
+              mma_i8_ts(tDV, tPa + kk * 8, desc_mnmajor(doq_addr, D, kk * 32), kIdDV, kk > 0);
+            else
+              mma_i8(tDV, desc_kmajor(pt_addr, 128, kk * 32), desc_mnmajor(doq_addr, D, kk * 32), kIdDV, kk > 0);
+          }
           mma_commit(dv_full);
           TR(1, it);
         }
@@ -315,22 +341,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       mbar_wait(kv_full, 0);
       issue_s(0);
+      if constexpr (kTS) mbar_wait(v_tmem, 0);
       issue_dp(0);
       for (int it = 0; it < n_it; ++it) {
         const uint32_t ph = it & 1, pph = ph ^ 1;
         const bool more = it + 1 < n_it;
         if constexpr (!kAlias) {
-          // compute events per tile: p_ready (S^T, dP^T read; P^^T written) < ds_ready (dS^^T
-          // written).  S_{i+1} and dP_{i+1} ride behind dV_i.
+          // compute events per tile: s_free (S^T in registers) < p_ready (dP^T read; P^^T
+          // written) < ds_ready (dS^^T written).  S_{i+1} goes out as soon as S_i is read, dP_{i+1}
+          // right behind dV_i, so the next tile's operands are ready when the compute gets there.
+          if (more) {
+            mbar_wait(s_free, ph);
+            tc_fence_after();
+            issue_s(it + 1);
+          }
           mbar_wait(p_ready, ph);
           if (it > 0) mbar_wait(dv_drained, pph);
           if (lane == 0) TR(17, it);
           tc_fence_after();
           issue_dv(it);
-          if (more) {
-            issue_s(it + 1);
-            issue_dp(it + 1);
-          }
+          if (more) issue_dp(it + 1);
           mbar_wait(ds_ready, ph);
           if (it > 0) {
             mbar_wait(dkq_drained, pph);
@@ -345,16 +375,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(p_ready, ph);
           tc_fence_after();
           issue_dv(it);
-          if (more) {
-            mbar_wait(dv_drained, ph);
-            tc_fence_after();
-            issue_s(it + 1);
-          }
+          // the compute warps finish a tile (ds_ready) before the drain finishes its dV tile, so
+          // dK_i/dQ_i go first, then S_{i+1} into the drained S columns, then dP_{i+1}
           mbar_wait(ds_ready, ph);
           if (it > 0) mbar_wait(dq_drained, pph);  // dQ slot; the dK slot (dP's) was freed at p_ready
           tc_fence_after();
           issue_dkdq(it);
           if (more) {
+            mbar_wait(dv_drained, ph);
+            tc_fence_after();
+            issue_s(it + 1);
             mbar_wait(dkq_drained, ph);  // dK_i read out of dP's columns
             tc_fence_after();
             issue_dp(it + 1);
@@ -374,6 +404,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sk = k_scale[(size_t)bh * T + j];
     uint8_t* pt = smem + L::kPt;
     uint8_t* dst = smem + L::kDSt;
+    if constexpr (kTS) {
+      // V_j row r (this warpgroup's 64 bytes) from the swizzled smem panel into TMEM (A of dP^T)
+      mbar_wait(kv_full, 0);
+      uint32_t w[16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint4 x = *reinterpret_cast<const uint4*>(smem + L::kV + sw_offset(r, wg * 4 + c, 128));
+        w[4 * c] = x.x;
+        w[4 * c + 1] = x.y;
+        w[4 * c + 2] = x.z;
+        w[4 * c + 3] = x.w;
+      }
+      tmem_st16(tVa + wg * 16 + lane_off, w);
+      tmem_wait_st();
+      tc_fence_before();
+      warp_arrive(v_tmem);
+    }
 
     for (int it = 0; it < n_it; ++it) {
       const int i = i0 + it, s = it % kStages;
@@ -424,6 +471,7 @@ if (cm) {
 }
       if (threadIdx.x == 128) TR(18, it);
       tc_fence_before();
+      if constexpr (!kAlias) warp_arrive(s_free);  // S^T consumed: S_{i+1} may be issued
       if (diag) {  // causal: key r attends query q only if r <= q (reading A14)
 #pragma unroll
         for (int e = 0; e < 64; ++e)
@@ -436,9 +484,11 @@ if (cm) {
       if (threadIdx.x == 128) TR(19, it);
       const float amax_p = ex2(compute_max(tmax, red, cw, 1));
       if (threadIdx.x == 128) TR(21, it);
-      const float inv_p = amax_p > 0.f ? __fdiv_rn(127.f, amax_p) : 0.f;
+      // inv = 127/amax via the correctly rounded reciprocal (within 1 ulp of fl32(127/amax); P^ is
+      // Tier C); the exact s_P = fl32(amax/127) is formed by the drain off this path
+      const float inv_p = amax_p > 0.f ? __fmul_rn(127.f, __frcp_rn(amax_p)) : 0.f;
       // tile scales for the drain warpgroup (4 slots: it cannot run 4 tiles ahead of the drain)
-      if (threadIdx.x == 128) scl[(it & 3) * 2] = __fdiv_rn(amax_p, 127.f);
+      if (threadIdx.x == 128) scl[(it & 3) * 2] = amax_p;
 
       // -- step 3: P = 2^t, P^ = RNE(P * inv) -> P^^T smem (A of dV, K-major);
       //            dS = P o (dP - delta) (lines 8-9) in the same pass, tile max |dS|
@@ -447,6 +497,7 @@ if (cm) {
       tc_fence_after();
       if (threadIdx.x == 128) TR(15, it);
       float dsmax = 0.f;
+      uint32_t pw[16];  // this thread's P^ row slice (64 int8) for the TMEM A operand of dV
 if (cm) {
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
@@ -477,21 +528,31 @@ if (cm) {
             t[e + 3] = b.y;
             dsmax = fmax3(dsmax, fabsf(a.x), fmax3(fabsf(a.y), fabsf(b.x), fabsf(b.y)));
           }
-          *reinterpret_cast<uint4*>(pt + sw_offset(r, (qc0 + cc * 32) / 16 + c16, 128)) =
-              make_uint4(w[0], w[1], w[2], w[3]);
+          if constexpr (kTS) {
+#pragma unroll
+            for (int e4 = 0; e4 < 4; ++e4) pw[cc * 8 + c16 * 4 + e4] = w[e4];
+          } else {
+            *reinterpret_cast<uint4*>(pt + sw_offset(r, (qc0 + cc * 32) / 16 + c16, 128)) =
+                make_uint4(w[0], w[1], w[2], w[3]);
+          }
         }
       }
 }
       if (threadIdx.x == 128) TR(23, it);
-      fence_proxy_async_smem();
+      if constexpr (kTS) {
+        tmem_st16(tPa + wg * 16 + lane_off, pw);
+        tmem_wait_st();
+      } else {
+        fence_proxy_async_smem();
+      }
       tc_fence_before();
       warp_arrive(p_ready);  // P^^T written; S^T and dP^T read (their TMEM columns may be reused)
       if (threadIdx.x == 128) TR(6, it);
 
       // -- step 5: psi(dS) scale over the tile
       const float amax_ds = compute_max(dsmax, red + 8, cw, 2);
-      const float inv_ds = amax_ds > 0.f ? __fdiv_rn(127.f, amax_ds) : 0.f;
-      if (threadIdx.x == 128) scl[(it & 3) * 2 + 1] = __fdiv_rn(amax_ds, 127.f);
+      const float inv_ds = amax_ds > 0.f ? __fmul_rn(127.f, __frcp_rn(amax_ds)) : 0.f;
+      if (threadIdx.x == 128) scl[(it & 3) * 2 + 1] = amax_ds;
 
       // -- step 6: dS^ = RNE(dS * inv) -> dS^^T smem (A of dK K-major, A of dQ MN-major)
       if (it > 0) mbar_wait(dkq_full, pph);  // dK_{i-1}, dQ_{i-1} have read dS^^T
@@ -543,7 +604,7 @@ if (cm) {
       tc_fence_after();
       if (threadIdx.x == 384) TR(10, it);
       if (!(ablate & 1)) {
-        const float s_p = scl[(it & 3) * 2];
+        const float s_p = __fdiv_rn(scl[(it & 3) * 2], 127.f);  // psi(P) scale = fl32(amax/127)
         const float2 f = make_float2(s_p * sdo, s_p * sdo);
         if constexpr (kAlias) {
           // fp32 accumulator in TMEM; 8-column chunks, loads double-buffered
@@ -599,7 +660,7 @@ if (cm) {
       tc_fence_after();
       if (threadIdx.x == 384) TR(11, it);
       if (!(ablate & 1)) {
-        const float s_ds = scl[(it & 3) * 2 + 1];
+        const float s_ds = __fdiv_rn(scl[(it & 3) * 2 + 1], 127.f);  // psi(dS) scale
         const float2 f = make_float2(s_ds * sq * tau, s_ds * sq * tau);
         float fb = 0.f;
         const float* muq = nullptr;
@@ -638,15 +699,16 @@ if (cm) {
       // dQ_i += tile * s_dS * s_K * tau, fp32 reduction across key blocks (line 10)
       if (threadIdx.x == 384) TR(12, it);
       {
-        // scaled tile -> swizzled smem staging (2 buffers) -> TMA reduce-add, one box per 32 columns
-        const float s_ds = scl[(it & 3) * 2 + 1];
+        // scaled rows -> this warp's swizzled smem staging (2 buffers) -> TMA reduce-add per box
+        const float s_ds = __fdiv_rn(scl[(it & 3) * 2 + 1], 127.f);
         const float2 f = make_float2(s_ds * sk * tau, s_ds * sk * tau);
+        uint8_t* wstage = smem + L::kDq + (warp % 4) * L::kDqWarp;
 #pragma unroll
         for (int qq = 0; qq < L::kDqRounds; ++qq) {
           const int rnd = it * L::kDqRounds + qq;
-          uint8_t* stage = smem + L::kDq + (rnd & 1) * L::kDqBoxes * L::kDqBox;
-          if (threadIdx.x == 384 && rnd >= 2) bulk_wait_read<1>();  // round rnd-2 has read `stage`
-          named_bar_sync(3, 128);
+          uint8_t* stage = wstage + (rnd & 1) * L::kDqBoxes * L::kDqBox;
+          if (lane == 0 && rnd >= 2) bulk_wait_read<1>();  // this warp's round rnd-2 has read `stage`
+          __syncwarp();
           if (!(ablate & 1)) {
 #pragma unroll
             for (int bx = 0; bx < L::kDqBoxes; ++bx) {
@@ -659,16 +721,17 @@ if (cm) {
               for (int e = 0; e < 32; e += 4) {
                 float2 a = fmul2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f);
                 float2 b = fmul2(make_float2(__int2float_rn((int)v[e + 2]), __int2float_rn((int)v[e + 3])), f);
-                *reinterpret_cast<float4*>(box + sw_offset(r, e / 4, 128)) = make_float4(a.x, a.y, b.x, b.y);
+                *reinterpret_cast<float4*>(box + sw_offset(lane, e / 4, 128)) = make_float4(a.x, a.y, b.x, b.y);
               }
             }
           }
           fence_proxy_async_smem();
-          named_bar_sync(3, 128);
-          if (threadIdx.x == 384 && !(ablate & 4)) {
+          __syncwarp();
+          if (lane == 0 && !(ablate & 4)) {
 #pragma unroll
             for (int bx = 0; bx < L::kDqBoxes; ++bx)
-              tma_reduce_add_2d(&tm_dq, stage + bx * L::kDqBox, (qq * L::kDqBoxes + bx) * 32, bh * N + i * kBlk);
+              tma_reduce_add_2d(&tm_dq, stage + bx * L::kDqBox, (qq * L::kDqBoxes + bx) * 32,
+                                bh * N + i * kBlk + (warp % 4) * 32);
             bulk_commit();
           }
         }
@@ -677,7 +740,7 @@ if (cm) {
       warp_arrive(dq_drained);
       if (threadIdx.x == 384) TR(13, it);
     }
-    if (threadIdx.x == 384) bulk_wait_all();  // staging smem must outlive the in-flight reduces
+    if (lane == 0) bulk_wait_all();  // staging smem must outlive this warp's in-flight reduces
     // epilogue: dK_j, dV_j rows -> bf16
     const size_t orow = ((size_t)krow + r) * D;
 #pragma unroll

@@ -59,7 +59,7 @@ cudaError_t launch_fwd(const FwdArgs& a, cudaStream_t s);
 struct BwdArgs {
   CUtensorMap tm_q, tm_k, tm_doq;  // int8 [BH*N][d], box [128][d]
   CUtensorMap tm_v, tm_do;         // bf16 [BH*N][d], box [128][64]
-  CUtensorMap tm_dq;               // fp32 dQ accumulator [BH*N][d], box [128][32] (TMA reduce-add)
+  CUtensorMap tm_dq;               // fp32 dQ accumulator [BH*N][d], box [32][32] (TMA reduce-add per warp)
   const float *q_scale, *k_scale, *do_scale;
   const float *l2, *delta;         // [BH][N]
   const float* bias;               // [BH][T][N] or null

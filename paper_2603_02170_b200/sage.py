@@ -214,7 +214,7 @@ def sage_attention(q, k, v, causal=False, k_smooth=True, q_smooth=False, softmax
 
 def debug_umma(mode, a, b, K=None, N=None):
     """One UMMA tile through the kernels' descriptor code (include/sage.h sage_debug_umma)."""
-    if mode in (0, 3):
+    if mode in (0, 3, 5):
         K = a.shape[1]
         N = 128
         out = torch.empty((128, 128), dtype=torch.int32 if mode == 0 else torch.float32, device=a.device)

@@ -77,9 +77,10 @@ def test_umma_s_tile_kmajor(K):
     np.testing.assert_array_equal(d, a.numpy().astype(np.int64) @ b.numpy().astype(np.int64).T)
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 4])
 @pytest.mark.parametrize("N", [64, 128])
 def test_umma_mn_major(mode, N):
+    """modes 1 / 4: A K-major from smem / from TMEM (TS); mode 2: A MN-major (dQ)."""
     g = torch.Generator().manual_seed(10 * mode + N)
     lo = 0 if mode == 1 else -127          # mode 1 is the P^ path (values in [0, 127])
     a = torch.randint(lo, 128, (128, 128), generator=g, dtype=torch.int8)
@@ -91,12 +92,14 @@ def test_umma_mn_major(mode, N):
     np.testing.assert_array_equal(d, A @ b.numpy().astype(np.int64))
 
 
+@pytest.mark.parametrize("mode", [3, 5])
 @pytest.mark.parametrize("K", [64, 128])
-def test_umma_bf16_dp_tile(K):
+def test_umma_bf16_dp_tile(mode, K):
+    """mode 3: both bf16 operands from smem; mode 5: A (V_j) from TMEM."""
     g = torch.Generator().manual_seed(K + 1)
     a = torch.randn(128, K, generator=g).to(torch.bfloat16)
     b = torch.randn(128, K, generator=g).to(torch.bfloat16)
-    d = sage.debug_umma(3, a.cuda(), b.cuda()).cpu().numpy()
+    d = sage.debug_umma(mode, a.cuda(), b.cuda()).cpu().numpy()
     ref = f64(a) @ f64(b).T
     assert np.abs(d - ref).max() <= 1e-4 * np.abs(ref).max()
 
