@@ -118,9 +118,9 @@ SAGE_API sage_status sage_ws_get_view(const sage_params* p, int backward, void* 
  * a, b, d: device pointers to row-major host-order arrays as described (int8/bf16 in, int32/fp32 out). */
 SAGE_API sage_status sage_debug_umma(int mode, int K, int N, const void* a, const void* b, void* d, void* stream);
 
-/* Profiling only (libsage_trace.so): copy the K4 pipeline timeline (clock64 stamps, uint64
- * [4 CTAs][64 tiles][24 events], recorded when the environment variable SAGE_ABLATE has bit 8 set)
- * to host memory. */
+/* Profiling only (libsage_trace.so): copy the K4 and K2 pipeline timelines (clock64 stamps, uint64
+ * [4 CTAs][64 tiles][24 events] each, recorded when the environment variable SAGE_ABLATE has bit 8
+ * set) to host memory: K4 in the first half of `bytes`, K2 in the second. */
 SAGE_API sage_status sage_debug_trace(void* host_out, size_t bytes);
 
 /* Optional instrumentation (calling thread only).  While enabled, sage_fwd / sage_bwd record

@@ -13,6 +13,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # -gencode arch=compute_100a,code=sm_100a: plain -arch=sm_100a embeds compute_100 PTX
 # that rejects tcgen05.  No --use_fast_math (bit-exact quantiser, reading A4).
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+         "-DSAGE_WAIT_HINT=" + os.environ.get("SAGE_WAIT_HINT", "0"),
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-shared",
          "-I" + os.path.join(HERE, "..", "include")]
 

@@ -371,6 +371,7 @@ sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const v
   a.tau = D.tau;
   a.causal = D.causal;
   a.qsmooth = D.qs;
+  a.ablate = ablate_flags();
   if ((e = timed(0, s, [&] { return launch_fwd(a, s); })) != cudaSuccess) return cuda_fail(e);
   if (g_prof.on) g_prof.launches += (D.ks ? 2 : 1) + (D.qs ? 3 : 0) + 1 + 1;
   return SAGE_OK;
@@ -436,7 +437,9 @@ sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const f
 
 sage_status sage_debug_trace(void* host_out, size_t bytes) {
   if (!host_out) return SAGE_ERR_INVALID_VALUE;
-  cudaError_t e = read_bwd_trace(host_out, bytes);
+  // first half: K4 timeline, second half: K2 timeline
+  cudaError_t e = read_bwd_trace(host_out, bytes / 2);
+  if (e == cudaSuccess) e = read_fwd_trace(static_cast<uint8_t*>(host_out) + bytes / 2, bytes / 2);
   return e == cudaSuccess ? SAGE_OK : cuda_fail(e);
 }
 

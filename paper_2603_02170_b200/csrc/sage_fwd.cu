@@ -26,6 +26,19 @@ constexpr int kThreads = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLog2_127 = 6.988684686772166f;
 
+#ifndef SAGE_TRACE
+#define SAGE_TRACE 0
+#endif
+// Profiling-only timeline (libsage_trace.so, SAGE_ABLATE bit 8), read back by sage_debug_trace
+// after the K4 timeline: [4 CTAs][64 tiles][24 events] clock64 stamps.
+constexpr int kTrCtas = 4, kTrTiles = 64, kTrEvents = 24;
+__device__ unsigned long long g_trace_fwd[kTrCtas * kTrTiles * kTrEvents];
+#define TRF(ev, jj)                                                                 \
+  do {                                                                              \
+    if (SAGE_TRACE && (ablate & 8) && blockIdx.x < kTrCtas && (jj) < kTrTiles)      \
+      g_trace_fwd[(blockIdx.x * kTrTiles + (jj)) * kTrEvents + (ev)] = clock64();   \
+  } while (0)
+
 template <int D>
 struct FwdSmem {
   static constexpr int kStages = D == 64 ? 3 : 2;
@@ -48,7 +61,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ q_scale,
                     const float* __restrict__ k_scale, const float* __restrict__ v_scale,
                     const float* __restrict__ bias, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, int N,
-                    int BH, float tau) {
+                    int BH, float tau, int ablate_arg) {
+  const int ablate = SAGE_TRACE ? ablate_arg : 0;
   using L = FwdSmem<D>;
   constexpr int kStages = L::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -146,6 +160,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             mma_i8(tS, desc_kmajor(q_addr, D, kk * 32), desc_kmajor(k_addr, D, kk * 32), kIdS, kk > 0);
           mma_commit(k_empty + st);
           mma_commit(s_full);
+          TRF(0, j);
         }
         __syncwarp();
       };
@@ -160,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             mma_i8(tPV, desc_kmajor(p_addr, 128, kk * 32), desc_mnmajor(v_addr, D, kk * 32), kIdPV, kk > 0);
           mma_commit(v_empty + st);
           mma_commit(o_full);
+          TRF(1, j);
         }
         __syncwarp();
       };
@@ -167,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       issue_s(0);
       for (int j = 0; j < nj; ++j) {
         mbar_wait(p_full, j & 1);  // S_j consumed, P^_j written
+        TRF(6, j);
         if (j + 1 < nj) issue_s(j + 1);
         if (j > 0) mbar_wait(o_empty, (j - 1) & 1);  // PV_{j-1} drained
         issue_pv(j);
@@ -221,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       mbar_wait(s_full, j & 1);
       tc_fence_after();
+      if (r == 0) TRF(2, j);
       // pass 1: row max (on int32 when there is no per-column bias)
       float rm;
       if constexpr (!QSMOOTH) {
@@ -240,6 +258,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
         }
         rm = __int2float_rn(mx) * c2;  // max commutes with the positive scale
+        if (r == 0) TRF(3, j);
       } else {
         rm = -INFINITY;
 #pragma unroll
@@ -299,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       fence_proxy_async_smem();
       tc_fence_before();
       warp_arrive(p_full);
+      if (r == 0) TRF(4, j);
       // l = alpha l + e^{rowmax - m_ij} sum(e^{S - rowmax})  (line 8, reading A7)
       l = fmaf(alpha, l, e_rm * (1.f / 127.f) * (rs2.x + rs2.y));
       const float spv = e_rm * (1.f / 127.f) * sv;
@@ -338,11 +358,16 @@ cudaError_t launch_t(const FwdArgs& a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   const int T = a.N / kBlk;
   kern<<<a.BH * T, kThreads, FwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_v, a.q_scale, a.k_scale, a.v_scale,
-                                                       a.bias, a.o, a.lse, a.N, a.BH, a.tau);
+                                                       a.bias, a.o, a.lse, a.N, a.BH, a.tau, a.ablate);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+cudaError_t read_fwd_trace(void* host, size_t bytes) {
+  if (bytes > sizeof(g_trace_fwd)) bytes = sizeof(g_trace_fwd);
+  return cudaMemcpyFromSymbol(host, g_trace_fwd, bytes);
+}
 
 cudaError_t launch_fwd(const FwdArgs& a, cudaStream_t s) {
   if (a.d == 128) {

@@ -53,8 +53,10 @@ struct FwdArgs {
   int BH, N, d;
   float tau;
   bool causal, qsmooth;
+  int ablate;  // profiling only (SAGE_ABLATE bit 8: timeline)
 };
 cudaError_t launch_fwd(const FwdArgs& a, cudaStream_t s);
+cudaError_t read_fwd_trace(void* host, size_t bytes);  // profiling: K2 event timeline
 
 struct BwdArgs {
   CUtensorMap tm_q, tm_k, tm_doq;  // int8 [BH*N][d], box [128][d]

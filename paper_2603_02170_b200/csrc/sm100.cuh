@@ -32,9 +32,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 // try_wait with a suspend-time hint: the waiting thread sleeps in hardware until the
 // phase completes (or the hint expires) instead of spinning on issue slots the
-// compute warps need.
+// compute warps need.  SAGE_WAIT_HINT=0 selects the hint-less form (the hardware's own
+// short suspend, then re-poll), which wakes up sooner.
+#ifndef SAGE_WAIT_HINT
+#define SAGE_WAIT_HINT 1
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
+#if SAGE_WAIT_HINT
   asm volatile(
       "{\n .reg .pred p;\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
@@ -42,6 +47,15 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
       : "memory");
+#else
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+#endif
   return ok != 0;
 }
 // Non-blocking probe: has the phase with `parity` completed?
@@ -181,6 +195,40 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// wait::ld that also pins the destination registers, so the compiler cannot hoist their first
+// use above the wait (needed when another load is in flight, i.e. double-buffered streaming).
+__device__ __forceinline__ void tmem_wait_ld_regs(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld_regs(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+                 "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+                 "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, uint32_t (&r)[16]) { tmem_ld16(taddr, r); }
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, uint32_t (&r)[32]) { tmem_ld32(taddr, r); }
+// Stream NCH chunks of CH 32-bit columns (this warp's 32 lanes) from TMEM through f(regs, chunk),
+// double-buffered: chunk c+1 is in flight while f runs on chunk c.
+template <int CH, int NCH, typename F>
+__device__ __forceinline__ void tmem_stream(uint32_t taddr, F&& f) {
+  uint32_t buf[2][CH];
+  tmem_ld_n(taddr, buf[0]);
+  tmem_wait_ld_regs(buf[0]);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    if (c + 1 < NCH) tmem_ld_n(taddr + (c + 1) * CH, buf[(c + 1) & 1]);
+    f(buf[c & 1], c);
+    if (c + 1 < NCH) tmem_wait_ld_regs(buf[(c + 1) & 1]);
+  }
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ----------------------------------------------------------------- UMMA

@@ -21,12 +21,15 @@ for _ in range(3):
     o, lse, ctx = sage.forward(q, k, v, **kw)
     sage.backward(ctx, v, o, lse, do)
 torch.cuda.synchronize()
-buf = np.zeros(4 * 64 * 24, dtype=np.uint64)
+buf = np.zeros(2 * 4 * 64 * 24, dtype=np.uint64)
 sage.lib().sage_debug_trace(buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes)
-tr = buf.reshape(4, 64, 24)[cta].astype(np.int64)
+which = 1 if os.environ.get('TRACE_FWD') else 0
+tr = buf.reshape(2, 4, 64, 24)[which][cta].astype(np.int64)
 names = ["S_iss", "dV_iss", "dP_iss", "dKQ_iss", "-", "c_sfull", "c_pready", "c_dpfull", "c_dsready", "c_dstfree",
          "d_dvfull", "d_dkfull", "d_dqfull", "d_dqdone", "tma_st", "c_ptfree",
          "c_ld0", "m_pready", "c_ldall", "c_tmax", "m_dsrdy", "c_bar1", "m_qfull", "c_st3"]
+if which:
+    names = ["S_iss", "PV_iss", "c_sfull", "c_pass1", "c_pfull", "-", "m_pfull"] + ["-"] * 17
 base = tr[tr > 0].min()
 rows = [t for t in range(64) if tr[t].any()]
 print("tile " + " ".join(f"{n:>8s}" for n in names))
