@@ -106,6 +106,22 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def rank_head_offset(c, rank):
+    """First global head index of this rank's batch: ranks own disjoint (batch x head) ranges
+    (weak scaling, no data-path collective) and, with per-head seeds, a head's
+    data does not depend on the world size."""
+    return rank * c.batch * c.heads
+
+
+def max_over_ranks(x, dist, device=None):
+    """Max of a per-rank float over all ranks (the timing reduction; identity without dist)."""
+    if dist is None:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -220,7 +236,7 @@ def main():
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
     # this rank's batch: distinct heads per rank (weak scaling), seeded on the CPU
-    q, k, v, do = config_inputs(c, head_offset=rank * c.batch * c.heads)
+    q, k, v, do = config_inputs(c, head_offset=rank_head_offset(c, rank))
     host = [t.pin_memory() for t in (q, k, v, do)]
     qd, kd, vd, dod = (t.to(dev) for t in host)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
@@ -254,11 +270,7 @@ def main():
             dist.barrier()
     prof = sage.profile_read()
     sage.profile_enable(False)
-    total_ms = sum(a.elapsed_time(b) for a, b in ev)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev), dist, dev)
     ms = total_ms / args.steps
     value = ops_of(c) * world / (ms * 1e-3) / 1e12
 
@@ -278,13 +290,11 @@ def main():
         torch.cuda.synchronize()
         if s > 0:
             e2e_ms.append(a.elapsed_time(b))
-    te = torch.tensor([sum(e2e_ms) / max(1, len(e2e_ms))], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    te_ms = max_over_ranks(sum(e2e_ms) / max(1, len(e2e_ms)), dist, dev)
     nbytes = sum(h.numel() * h.element_size() for h in host)
     e2e = None
     if e2e_ms:
-        e2e = {"value": ops_of(c) * world / (float(te.item()) * 1e-3) / 1e12, "unit": "TOPS",
+        e2e = {"value": ops_of(c) * world / (te_ms * 1e-3) / 1e12, "unit": "TOPS",
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
 
     if rank == 0:
