@@ -1,6 +1,9 @@
 // sage_fwd.cu -- K2: SageBwd forward, Alg. 1, one CTA per
 // (head, 128-query block i), two CTAs resident per SM (TMEM 256 columns, <= 113 KB smem,
-// setmaxnreg) so one CTA's softmax overlaps the other's MMAs and TMEM round trips.
+// setmaxnreg) so one CTA's softmax overlaps the other's MMAs and TMEM round trips.  Within a CTA
+// S is double-buffered in TMEM (PV_j reuses S_j's buffer once S_j is consumed), and the O update
+// for tile j-1 runs before tile j's exponential pass, so S_{j+1} is on the tensor cores while
+// tile j is being exponentiated.
 // tcgen05 kind::i8 MMAs with TMEM accumulators, TMA into 128B/64B-swizzled shared
 // memory, warp-specialised roles:
 //   warps 0-3  softmax + correction + epilogue (thread t owns query row t = TMEM lane t)
@@ -49,7 +52,7 @@ struct FwdSmem {
   static constexpr int kP = kV + kStages * kTile;  // [128][128] int8 P^, K-major 128B-swizzled
   static constexpr int kBias = kP + kBlk * kBlk;   // 2 x 128 floats (Q-smoothing)
   static constexpr int kBar = kBias + 2 * kBlk * 4;
-  static constexpr int kNumBars = 1 + 4 * kStages + 4;
+  static constexpr int kNumBars = 1 + 4 * kStages + 5;
   static constexpr int kTmemSlot = kBar + kNumBars * 8;
   static constexpr int kBytes = kTmemSlot + 16;
   static constexpr int kAlloc = kBytes + 1024;  // slack for 1024-byte alignment
@@ -75,10 +78,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* k_empty = k_full + kStages;
   uint64_t* v_full = k_empty + kStages;
   uint64_t* v_empty = v_full + kStages;
-  uint64_t* s_full = v_empty + kStages;  // MMA -> softmax: S_j in TMEM
-  uint64_t* p_full = s_full + 1;         // softmax -> MMA (4 warps): S_j read, P^_j in smem
-  uint64_t* o_full = s_full + 2;         // MMA -> softmax: PV_j in TMEM (P^_j read)
-  uint64_t* o_empty = s_full + 3;        // softmax -> MMA (4 warps): PV_j drained
+  uint64_t* s_full = v_empty + kStages;  // [2] MMA -> softmax: S_j in buffer j&1 (two in flight)
+  uint64_t* p_full = s_full + 2;         // softmax -> MMA (4 warps): S_j read, P^_j written
+  uint64_t* o_full = s_full + 3;         // MMA -> softmax: PV_j in TMEM (P^_j read)
+  uint64_t* o_empty = s_full + 4;        // softmax -> MMA (4 warps): PV_j drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
   float* bias_s = reinterpret_cast<float*>(smem + L::kBias);
 
@@ -100,6 +103,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(v_empty + s, 1);
     }
     mbar_init(s_full, 1);
+    mbar_init(s_full + 1, 1);
     mbar_init(p_full, 4);
     mbar_init(o_full, 1);
     mbar_init(o_empty, 4);
@@ -110,8 +114,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem;         // S_j   columns [0, 128)
-  const uint32_t tPV = tmem + 128;  // PV_j  columns [128, 128 + D)
+  // Two 128-column buffers; tile j uses buffer j&1: S_j, then (S_j consumed) PV_j in its first D
+  // columns and, for d=64, P^_j (the A operand of PV_j, 32 columns) right after PV_j.
+  // S_{j+1} is computed while tile j's softmax runs.
+  auto tbuf = [&](int j) { return tmem + (uint32_t)(j & 1) * 128; };
+  constexpr bool kPTmem = D == 64;
 
   if (warp >= 4) {
     reg_dealloc<72>();
@@ -157,9 +164,9 @@ __global__ void __launch_bounds__(kThreads, 2)
           const uint32_t k_addr = k0 + st * L::kTile;
 #pragma unroll
           for (int kk = 0; kk < D / 32; ++kk)
-            mma_i8(tS, desc_kmajor(q_addr, D, kk * 32), desc_kmajor(k_addr, D, kk * 32), kIdS, kk > 0);
+            mma_i8(tbuf(j), desc_kmajor(q_addr, D, kk * 32), desc_kmajor(k_addr, D, kk * 32), kIdS, kk > 0);
           mma_commit(k_empty + st);
-          mma_commit(s_full);
+          mma_commit(s_full + (j & 1));
           TRF(0, j);
         }
         __syncwarp();
@@ -171,8 +178,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (elect_one()) {
           const uint32_t v_addr = v0 + st * L::kTile;
 #pragma unroll
-          for (int kk = 0; kk < kBlk / 32; ++kk)
-            mma_i8(tPV, desc_kmajor(p_addr, 128, kk * 32), desc_mnmajor(v_addr, D, kk * 32), kIdPV, kk > 0);
+          for (int kk = 0; kk < kBlk / 32; ++kk) {
+            if constexpr (kPTmem)
+              mma_i8_ts(tbuf(j), tbuf(j) + D + kk * 8, desc_mnmajor(v_addr, D, kk * 32), kIdPV, kk > 0);
+            else
+              mma_i8(tbuf(j), desc_kmajor(p_addr, 128, kk * 32), desc_mnmajor(v_addr, D, kk * 32), kIdPV, kk > 0);
+          }
           mma_commit(v_empty + st);
           mma_commit(o_full);
           TRF(1, j);
@@ -181,12 +192,15 @@ __global__ void __launch_bounds__(kThreads, 2)
       };
       mbar_wait(q_full, 0);
       issue_s(0);
+      if (nj > 1) issue_s(1);
       for (int j = 0; j < nj; ++j) {
-        mbar_wait(p_full, j & 1);  // S_j consumed, P^_j written
+        mbar_wait(p_full, j & 1);  // S_j consumed, P^_j written (and PV_{j-1} drained)
         TRF(6, j);
-        if (j + 1 < nj) issue_s(j + 1);
-        if (j > 0) mbar_wait(o_empty, (j - 1) & 1);  // PV_{j-1} drained
-        issue_pv(j);
+        issue_pv(j);               // into S_j's buffer
+        if (j + 2 < nj) {
+          mbar_wait(o_empty, j & 1);  // PV_j drained (done early in tile j+1)
+          issue_s(j + 2);            // into the same buffer
+        }
       }
     }
   } else {
@@ -204,7 +218,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint8_t* prow = smem + L::kP;
 
     // O = alpha O + PV s_P s_V  (Alg. 1 line 10, reading A7); alpha == 1 skips the rescale
-    auto correct = [&](float alpha, float spv) {
+    auto correct = [&](int jj, float alpha, float spv) {
+      const uint32_t tPV = tbuf(jj);
       const float2 f = make_float2(spv, spv);
       const bool rescale = __any_sync(0xffffffffu, alpha != 1.f);
 #pragma unroll
@@ -236,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         bias_s[(j & 1) * kBlk + r] = bias[((size_t)bh * T + i) * N + (size_t)j * kBlk + r] * tau2;
         named_bar_sync(1, 128);
       }
-      mbar_wait(s_full, j & 1);
+      mbar_wait(s_full + (j & 1), (j >> 1) & 1);
       tc_fence_after();
       if (r == 0) TRF(2, j);
       // pass 1: row max (on int32 when there is no per-column bias)
@@ -246,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int c0 = 0; c0 < kBlk; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(tS + c0 + lane_off, v);
+          tmem_ld32(tbuf(j) + c0 + lane_off, v);
           tmem_wait_ld();
           if (diag) {
 #pragma unroll
@@ -264,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int c0 = 0; c0 < kBlk; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(tS + c0 + lane_off, v);
+          tmem_ld32(tbuf(j) + c0 + lane_off, v);
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 32; ++e)
@@ -275,14 +290,21 @@ __global__ void __launch_bounds__(kThreads, 2)
       const float alpha = ex2(m - m_new);
       const float e_rm = ex2(rm - m_new);
       const float sub = rm - kLog2_127;  // p' = 2^{s - rm + log2 127} = 127 e^{S - rowmax}
-      // pass 2: p' and P^ = RNE(p') -> swizzled K-major smem row r (the buffer is free once
-      // PV_{j-1} has completed)
-      if (j > 0) mbar_wait(o_full, (j - 1) & 1);
+      // O update for tile j-1 first: PV_{j-1} is ready by now, and draining it frees its buffer
+      // for S_{j+1}, which then runs on the tensor cores during this tile's pass 2
+      if (j > 0) {
+        mbar_wait(o_full, (j - 1) & 1);
+        tc_fence_after();
+        correct(j - 1, prev_alpha, prev_spv);
+      }
+      // pass 2: p' and P^ = RNE(p') -> the A operand of PV_j (d=64: TMEM after PV_j's columns;
+      // d=128: swizzled K-major smem, free since PV_{j-1} completed)
       float2 rs2 = make_float2(0.f, 0.f);
+      uint32_t pw[kPTmem ? 32 : 1];
 #pragma unroll
       for (int c0 = 0; c0 < kBlk; c0 += 32) {
         uint32_t v[32];
-        tmem_ld32(tS + c0 + lane_off, v);
+        tmem_ld32(tbuf(j) + c0 + lane_off, v);
         tmem_wait_ld();
         uint32_t pk[8];
 #pragma unroll
@@ -311,11 +333,21 @@ __global__ void __launch_bounds__(kThreads, 2)
           const float2 qb = fadd2(b, make_float2(kMagic, kMagic));
           pk[e4] = pack4_magic(qa.x, qa.y, qb.x, qb.y);
         }
-        const int chunk = c0 / 16;
-        *reinterpret_cast<uint4*>(prow + sw_offset(r, chunk, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4*>(prow + sw_offset(r, chunk + 1, 128)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        if constexpr (kPTmem) {
+#pragma unroll
+          for (int w = 0; w < 8; ++w) pw[c0 / 4 + w] = pk[w];
+        } else {
+          const int chunk = c0 / 16;
+          *reinterpret_cast<uint4*>(prow + sw_offset(r, chunk, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(prow + sw_offset(r, chunk + 1, 128)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
       }
-      fence_proxy_async_smem();
+      if constexpr (kPTmem) {
+        tmem_st32(tbuf(j) + D + lane_off, pw);  // S_j's columns [D, D+32) have all been read
+        tmem_wait_st();
+      } else {
+        fence_proxy_async_smem();
+      }
       tc_fence_before();
       warp_arrive(p_full);
       if (r == 0) TRF(4, j);
@@ -323,13 +355,12 @@ __global__ void __launch_bounds__(kThreads, 2)
       l = fmaf(alpha, l, e_rm * (1.f / 127.f) * (rs2.x + rs2.y));
       const float spv = e_rm * (1.f / 127.f) * sv;
       m = m_new;
-      if (j > 0) correct(prev_alpha, prev_spv);  // PV_{j-1} (its o_full was waited for above)
       prev_alpha = alpha;
       prev_spv = spv;
     }
     mbar_wait(o_full, (nj - 1) & 1);
     tc_fence_after();
-    correct(prev_alpha, prev_spv);
+    correct(nj - 1, prev_alpha, prev_spv);
     // epilogue: O = acc / l (Alg. 1 line 13), L = m + ln l (line 14, natural log)
     const float inv_l = l > 0.f ? 1.f / l : 0.f;
     __nv_bfloat16* orow = o + ((size_t)row0 + r) * D;
