@@ -31,8 +31,8 @@ def _stale():
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def _link(lib, defines, verbose):
-    tag = "trace" if defines else "prod"
+def _link(lib, defines, verbose, tag=None):
+    tag = tag or ("trace" if defines else "prod")
     objs = []
     for src in sources():
         obj = os.path.join(CSRC, "build", tag, os.path.basename(src) + ".o")
@@ -55,6 +55,13 @@ def build(force=False, verbose=False, trace=False):
     if trace:
         _link(TRACE_LIB, ["-DSAGE_TRACE=1"], verbose)
     return LIB
+
+
+def build_variant(name, defines, verbose=False):
+    """Profiling only: libsage_<name>.so built with extra -D flags (selected with SAGE_LIB=...)."""
+    lib = os.path.join(HERE, f"libsage_{name}.so")
+    _link(lib, list(defines), verbose, tag=name)
+    return lib
 
 
 if __name__ == "__main__":

@@ -37,4 +37,5 @@ for t in rows:
     print(f"{t:4d} " + " ".join(f"{(x - base) if x else -1:8d}" for x in tr[t]))
 if len(rows) > 4:
     a, b = rows[2], rows[-2]
-    print("per-tile period (S_iss):", (tr[b][0] - tr[a][0]) / (b - a))
+    col = names.index("S_iss")
+    print("per-tile period (S_iss):", (tr[b][col] - tr[a][col]) / (b - a))
