@@ -492,7 +492,8 @@ if (cm) {
 
       // -- step 3: P = 2^t, P^ = RNE(P * inv) -> P^^T smem (A of dV, K-major);
       //            dS = P o (dP - delta) (lines 8-9) in the same pass, tile max |dS|
-      if (it > 0) mbar_wait(dv_full, pph);  // dV_{i-1} has read P^^T (its commit = dv_full)
+      // P^^T may be overwritten once dV_{i-1} has read it: dP_i is issued after dV_{i-1} and a
+      // tcgen05.commit tracks every earlier MMA of the issuing thread, so dp_full(i) implies it
       mbar_wait(dp_full, ph);
       tc_fence_after();
       if (threadIdx.x == 128) TR(15, it);
