@@ -186,7 +186,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 4; ++b) mbar_init(b0 + b, 1);
     for (int b = 4; b < 6; ++b) mbar_init(b0 + b, kComputeWarps);
-    for (int b = 6; b < 8; ++b) mbar_init(b0 + b, kDrainWarps);
+    // d=128: the compute warps drain the dV tile (it aliases S, so draining it gates S_{i+1})
+    mbar_init(dv_drained, kAlias ? kComputeWarps : kDrainWarps);
+    mbar_init(dkq_drained, kDrainWarps);
     mbar_init(do_full, 1);
     mbar_init(do_empty, 1);
     mbar_init(dq_drained, kDrainWarps);
@@ -579,6 +581,38 @@ if (cm) {
       tc_fence_before();
       warp_arrive(ds_ready);
       if (threadIdx.x == 128) TR(8, it);
+      if constexpr (kAlias) {
+        // d=128: dV_j += tile * s_P * s_dO_i (Alg. 2 line 7) into the fp32 TMEM accumulator, this
+        // warpgroup's 64 columns.  The dV tile sits on S's columns, so S_{i+1} waits for this
+        // drain; the compute warps are otherwise idle here, and two warpgroups halve it.
+        mbar_wait(dv_full, ph);
+        tc_fence_after();
+        const float s_p = __fdiv_rn(amax_p, 127.f);  // psi(P) scale = fl32(amax/127)
+        const float sp_do = s_p * sc_do[i];
+        const float2 f = make_float2(sp_do, sp_do);
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t v[32], a[32];
+          tmem_ld32(tDV + qc0 + c0 + lane_off, v);
+          tmem_ld32(tDVacc + qc0 + c0 + lane_off, a);
+          tmem_wait_ld();
+          if (it == 0) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) a[e] = 0u;
+          }
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float2 x = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f,
+                                   make_float2(__uint_as_float(a[e]), __uint_as_float(a[e + 1])));
+            a[e] = __float_as_uint(x.x);
+            a[e + 1] = __float_as_uint(x.y);
+          }
+          tmem_st32(tDVacc + qc0 + c0 + lane_off, a);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        warp_arrive(dv_drained);
+      }
     }
   } else {
     reg_alloc<kRegDrain>();
@@ -600,43 +634,14 @@ if (cm) {
       const float sq = sc_q[i];
       const float sdo = sc_do[i];
 
-      // dV_j += tile * s_P * s_dO_i  (Alg. 2 line 7)
-      mbar_wait(dv_full, ph);
-      tc_fence_after();
-      if (threadIdx.x == 384) TR(10, it);
-      if (!(ablate & 1)) {
-        const float s_p = __fdiv_rn(scl[(it & 3) * 2], 127.f);  // psi(P) scale = fl32(amax/127)
-        const float2 f = make_float2(s_p * sdo, s_p * sdo);
-        if constexpr (kAlias) {
-          // fp32 accumulator in TMEM; 8-column chunks, loads double-buffered
-          uint32_t vb[2][8], ab[2][8];
-          tmem_ld8(tDV + lane_off, vb[0]);
-          tmem_ld8(tDVacc + lane_off, ab[0]);
-          tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < D / 8; ++c) {
-            uint32_t(&v)[8] = vb[c & 1];
-            uint32_t(&a)[8] = ab[c & 1];
-            if (c + 1 < D / 8) {
-              if (c >= 1) tmem_wait_st();  // the other buffer's accumulator store has read its registers
-              tmem_ld8(tDV + (c + 1) * 8 + lane_off, vb[(c + 1) & 1]);
-              tmem_ld8(tDVacc + (c + 1) * 8 + lane_off, ab[(c + 1) & 1]);
-            }
-            if (it == 0) {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) a[e] = 0u;
-            }
-#pragma unroll
-            for (int e = 0; e < 8; e += 2) {
-              float2 x = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f,
-                               make_float2(__uint_as_float(a[e]), __uint_as_float(a[e + 1])));
-              a[e] = __float_as_uint(x.x);
-              a[e + 1] = __float_as_uint(x.y);
-            }
-            tmem_st8(tDVacc + c * 8 + lane_off, a);
-            if (c + 1 < D / 8) tmem_wait_ld();
-          }
-        } else {
+      // dV_j += tile * s_P * s_dO_i  (Alg. 2 line 7); d=128: drained by the compute warps
+      if constexpr (!kAlias) {
+        mbar_wait(dv_full, ph);
+        tc_fence_after();
+        if (threadIdx.x == 384) TR(10, it);
+        if (!(ablate & 1)) {
+          const float s_p = __fdiv_rn(scl[(it & 3) * 2], 127.f);  // psi(P) scale = fl32(amax/127)
+          const float2 f = make_float2(s_p * sdo, s_p * sdo);
 #pragma unroll
           for (int c0 = 0; c0 < D; c0 += 32) {
             uint32_t v[32];
@@ -651,10 +656,9 @@ if (cm) {
             }
           }
         }
-        if constexpr (kAlias) tmem_wait_st();
+        tc_fence_before();
+        warp_arrive(dv_drained);
       }
-      tc_fence_before();
-      warp_arrive(dv_drained);
 
       // dK_j += tile * s_dS * s_Q * tau (+ Q-smoothing bias branch)  (line 11)
       mbar_wait(dkq_full, ph);
@@ -742,6 +746,10 @@ if (cm) {
       if (threadIdx.x == 384) TR(13, it);
     }
     if (lane == 0) bulk_wait_all();  // staging smem must outlive this warp's in-flight reduces
+    if constexpr (kAlias) {  // the compute warps' last dV accumulation
+      mbar_wait(dv_drained, (n_it - 1) & 1);
+      tc_fence_after();
+    }
     // epilogue: dK_j, dV_j rows -> bf16
     const size_t orow = ((size_t)krow + r) * D;
 #pragma unroll
