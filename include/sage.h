@@ -123,6 +123,17 @@ SAGE_API sage_status sage_debug_umma(int mode, int K, int N, const void* a, cons
  * set) to host memory: K4 in the first half of `bytes`, K2 in the second. */
 SAGE_API sage_status sage_debug_trace(void* host_out, size_t bytes);
 
+/* Test only (libsage_trace.so; the production libsage.so returns SAGE_ERR_UNSUPPORTED): make every
+ * later sage_bwd dump, for heads bh < `heads` (bh = b*H + h), K4's own backward intermediates
+ * (Alg. 2 lines 6 and 9, P:689 / P:695) into caller-owned device memory:
+ *   p_hat_t  int8 [heads][N kv][N q]  P^ of tile (i, j) transposed (key-major), psi(P) per tile (A11)
+ *   ds_hat_t int8 [heads][N kv][N q]  dS^, same layout
+ *   ds_t     fp32 [heads][N kv][N q]  dS = P o (dP - delta) before psi
+ *   s_p, s_ds fp32 [heads][T i][T j]  the tile scales fl32(amax / 127)
+ * Tiles a causal run skips are not written.  heads = 0 turns the dump off.  The buffers must stay
+ * valid until the dumping sage_bwd has completed.  Not thread-safe (process-wide state). */
+SAGE_API sage_status sage_debug_dump(void* p_hat_t, float* s_p, void* ds_hat_t, float* s_ds, float* ds_t, int heads);
+
 /* Optional instrumentation (calling thread only).  While enabled, sage_fwd / sage_bwd record
  * a CUDA event pair around their fused kernel (K2 / K4) and count every kernel they launch.
  * sage_profile_read synchronises on the recorded events, returns the summed K2 and K4 device

@@ -35,7 +35,7 @@ def _load():
         P = ctypes.c_void_p
         I, D = ctypes.c_int, ctypes.c_double
         _lib.oracle_fwd.argtypes = [I, I, I, I, I, D] + [P] * 14
-        _lib.oracle_bwd.argtypes = [I, I, I, I, I, D] + [P] * 12
+        _lib.oracle_bwd.argtypes = [I, I, I, I, I, D] + [P] * 17
         _lib.oracle_fpa.argtypes = [I, I, I, I, D] + [P] * 13
         _lib.oracle_psi_block.argtypes = [P, I, I, P, P]
         _lib.oracle_psi_token_row.argtypes = [P, I, D, P]
@@ -106,8 +106,12 @@ def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk
 
 
 def bwd(q, k, v, o_stored, do, lse, *, causal=False, k_smooth=True, q_smooth=False, quant=True,
-        blk=128, tau=None):
-    """Alg. 2 per head.  o_stored is the O the forward stored (A15)."""
+        blk=128, tau=None, tiles=False):
+    """Alg. 2 per head.  o_stored is the O the forward stored (A15).
+
+    tiles=True also returns the per-tile quantised P^ / dS^ ([BH, N q, N kv] int8, tile (i, j) at
+    rows i*blk.., columns j*blk..), their psi scales s_P / s_dS ([BH, T i, T j] fp32) and the
+    pre-psi dS ([BH, N, N] double); tiles a causal run skips stay zero."""
     q, k, v, o_stored, do, lse = map(_f64, (q, k, v, o_stored, do, lse))
     BH, N, d = q.shape
     T = N // blk
@@ -116,9 +120,15 @@ def bwd(q, k, v, o_stored, do, lse, *, causal=False, k_smooth=True, q_smooth=Fal
     out = dict(dq=np.zeros((BH, N, d)), dk=np.zeros((BH, N, d)), dv=np.zeros((BH, N, d)),
                delta=np.zeros((BH, N)), do8=np.zeros((BH, N, d), np.int8),
                sdo=np.zeros((BH, T), np.float32))
+    if tiles:
+        out.update(p8=np.zeros((BH, N, N), np.int8), sp=np.zeros((BH, T, T), np.float32),
+                   ds8=np.zeros((BH, N, N), np.int8), sds=np.zeros((BH, T, T), np.float32),
+                   ds=np.zeros((BH, N, N)))
     rc = _load().oracle_bwd(BH, N, d, blk, flags, _default_tau(d, tau), _p(q), _p(k), _p(v),
                             _p(o_stored), _p(do), _p(lse), _p(out["dq"]), _p(out["dk"]),
-                            _p(out["dv"]), _p(out["delta"]), _p(out["do8"]), _p(out["sdo"]))
+                            _p(out["dv"]), _p(out["delta"]), _p(out["do8"]), _p(out["sdo"]),
+                            _p(out.get("p8")), _p(out.get("sp")), _p(out.get("ds8")), _p(out.get("sds")),
+                            _p(out.get("ds")))
     if rc:
         raise ValueError("oracle_bwd: bad shape")
     return out

@@ -336,7 +336,8 @@ int oracle_fwd(int BH, int N, int d, int blk, int flags, double tau,
  * dP = dO_i V_j^T (A8) is exact in double from the I/O values (A9).          */
 static void bwd_head(const double *q, const double *k, const double *v, const double *o_stored,
                      const double *dO, const double *lse, int N, int d, int blk, int flags, double tau,
-                     double *dq, double *dk, double *dv, double *delta_out, int8_t *do8_out, float *sdo_out) {
+                     double *dq, double *dk, double *dv, double *delta_out, int8_t *do8_out, float *sdo_out,
+                     int8_t *p8_out, float *sp_out, int8_t *ds8_out, float *sds_out, double *ds_out) {
   head_prep h;
   prep_head(&h, q, k, N, d, blk, flags);
   int T = h.T, qo = (flags & ORC_QUANT_OFF) != 0, causal = (flags & ORC_CAUSAL) != 0;
@@ -401,6 +402,16 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
         }
       double sds;
       psi_block(dS, (int)bb, 0, qo, dS8, &sds, dSx);
+      /* optional tile dumps (test infrastructure: Tier-C and fidelity reports), [N q][N kv] */
+      for (int r = 0; r < blk; ++r)
+        for (int n = 0; n < blk; ++n) {
+          size_t g = (size_t)(i * blk + r) * N + (size_t)j * blk + n, t = (size_t)r * blk + n;
+          if (p8_out) p8_out[g] = P8[t];
+          if (ds8_out) ds8_out[g] = dS8[t];
+          if (ds_out) ds_out[g] = dS[t];
+        }
+      if (sp_out) sp_out[(size_t)i * T + j] = (float)sp;
+      if (sds_out) sds_out[(size_t)i * T + j] = (float)sds;
       /* line 10: dQ_i += MM(dS^_ij, K^_j) x s_dS x s_K  (x tau, A6). */
       for (int r = 0; r < blk; ++r)
         for (int c = 0; c < d; ++c) {
@@ -452,7 +463,8 @@ int oracle_bwd(int BH, int N, int d, int blk, int flags, double tau,
                const double *q, const double *k, const double *v, const double *o_stored,
                const double *dO, const double *lse,
                double *dq, double *dk, double *dv,
-               double *delta, int8_t *do8, float *sdo) {
+               double *delta, int8_t *do8, float *sdo,
+               int8_t *p8, float *sp, int8_t *ds8, float *sds, double *ds) {
   if (BH <= 0 || N <= 0 || d <= 0 || blk <= 0 || N % blk) return -1;
   int T = N / blk;
   size_t nd = (size_t)N * d;
@@ -461,7 +473,10 @@ int oracle_bwd(int BH, int N, int d, int blk, int flags, double tau,
     bwd_head(q + b * nd, k + b * nd, v + b * nd, o_stored + b * nd, dO + b * nd, lse + (size_t)b * N,
              N, d, blk, flags, tau, dq + b * nd, dk + b * nd, dv + b * nd,
              delta ? delta + (size_t)b * N : NULL, do8 ? do8 + b * nd : NULL,
-             sdo ? sdo + (size_t)b * T : NULL);
+             sdo ? sdo + (size_t)b * T : NULL,
+             p8 ? p8 + (size_t)b * N * N : NULL, sp ? sp + (size_t)b * T * T : NULL,
+             ds8 ? ds8 + (size_t)b * N * N : NULL, sds ? sds + (size_t)b * T * T : NULL,
+             ds ? ds + (size_t)b * N * N : NULL);
   }
   return 0;
 }

@@ -179,6 +179,9 @@ int ablate_flags() {
   return v;
 }
 
+// sage_debug_dump state (libsage_trace.so only): K4 tile dump on while heads > 0
+int g_dump_heads = 0;
+
 template <typename T>
 T* at(void* base, size_t off) {
   return reinterpret_cast<T*>(static_cast<uint8_t*>(base) + off);
@@ -426,7 +429,7 @@ sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const f
   a.tau = D.tau;
   a.causal = D.causal;
   a.qsmooth = D.qs;
-  a.ablate = ablate_flags();
+  a.ablate = ablate_flags() | (g_dump_heads > 0 ? 16 : 0);
   if ((e = timed(1, s, [&] { return launch_bwd(a, s); })) != cudaSuccess) return cuda_fail(e);
   if (g_prof.on) g_prof.launches += 3;
   // K5
@@ -441,6 +444,20 @@ sage_status sage_debug_trace(void* host_out, size_t bytes) {
   cudaError_t e = read_bwd_trace(host_out, bytes / 2);
   if (e == cudaSuccess) e = read_fwd_trace(static_cast<uint8_t*>(host_out) + bytes / 2, bytes / 2);
   return e == cudaSuccess ? SAGE_OK : cuda_fail(e);
+}
+
+sage_status sage_debug_dump(void* p_hat_t, float* s_p, void* ds_hat_t, float* s_ds, float* ds_t, int heads) {
+#if SAGE_TRACE
+  if (heads < 0 || (heads > 0 && (!p_hat_t || !s_p || !ds_hat_t || !s_ds || !ds_t))) return SAGE_ERR_INVALID_VALUE;
+  BwdDump d{static_cast<int8_t*>(p_hat_t), static_cast<int8_t*>(ds_hat_t), s_p, s_ds, ds_t, heads};
+  cudaError_t e = set_bwd_dump(d);
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_dump_heads = heads;
+  return SAGE_OK;
+#else
+  (void)p_hat_t; (void)s_p; (void)ds_hat_t; (void)s_ds; (void)ds_t; (void)heads;
+  return SAGE_ERR_UNSUPPORTED;
+#endif
 }
 
 sage_status sage_debug_umma(int mode, int K, int N, const void* a, const void* b, void* d, void* stream) {

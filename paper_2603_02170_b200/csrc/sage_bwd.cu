@@ -92,11 +92,11 @@ __device__ unsigned long long g_trace[kTrCtas * kTrTiles * kTrEvents];
       g_trace[(blockIdx.x * kTrTiles + (it)) * kTrEvents + (ev)] = clock64();       \
   } while (0)
 
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
+// Test-only tile dump (SAGE_ABLATE bit 16, libsage_trace.so; sage_debug_dump): the compute
+// warps write P^^T, dS^^T (int8) and the pre-psi dS^T (fp32) as [head][N kv][N q], and the tile
+// scales s_P, s_dS as [head][T i][T j], for heads bh < g_dump.heads (Tier C, fidelity reports).
+__device__ BwdDump g_dump;
+#define DUMPING (SAGE_TRACE && (ablate & 16) && bh < g_dump.heads)
 
 // Order-preserving float <-> int map (monotone for all finite values and +-inf), so a float max is
 // one redux.sync.max.s32 instead of five shuffles.
@@ -531,6 +531,9 @@ if (cm) {
             t[e + 3] = b.y;
             dsmax = fmax3(dsmax, fabsf(a.x), fmax3(fabsf(a.y), fabsf(b.x), fabsf(b.y)));
           }
+          if (DUMPING)
+            *reinterpret_cast<uint4*>(g_dump.pt + ((size_t)bh * N + j * kBlk + r) * N + i * kBlk + qc0 + cc * 32 +
+                                      c16 * 16) = make_uint4(w[0], w[1], w[2], w[3]);
           if constexpr (kTS) {
 #pragma unroll
             for (int e4 = 0; e4 < 4; ++e4) pw[cc * 8 + c16 * 4 + e4] = w[e4];
@@ -556,6 +559,15 @@ if (cm) {
       const float amax_ds = compute_max(dsmax, red + 8, cw, 2);
       const float inv_ds = amax_ds > 0.f ? __fmul_rn(127.f, __frcp_rn(amax_ds)) : 0.f;
       if (threadIdx.x == 128) scl[(it & 3) * 2 + 1] = amax_ds;
+      if (DUMPING) {
+        float* dsrow = g_dump.ds + ((size_t)bh * N + j * kBlk + r) * N + i * kBlk + qc0;
+#pragma unroll
+        for (int e = 0; e < 64; e += 4) *reinterpret_cast<float4*>(dsrow + e) = make_float4(t[e], t[e + 1], t[e + 2], t[e + 3]);
+        if (threadIdx.x == 128) {
+          g_dump.sp[((size_t)bh * T + i) * T + j] = __fdiv_rn(amax_p, 127.f);
+          g_dump.sds[((size_t)bh * T + i) * T + j] = __fdiv_rn(amax_ds, 127.f);
+        }
+      }
 
       // -- step 6: dS^ = RNE(dS * inv) -> dS^^T smem (A of dK K-major, A of dQ MN-major)
       if (it > 0) mbar_wait(dkq_full, pph);  // dK_{i-1}, dQ_{i-1} have read dS^^T
@@ -574,6 +586,9 @@ if (cm) {
           if constexpr (QSMOOTH) rsum = __dp4a((int)w[e4], 0x01010101, rsum);
         }
         *reinterpret_cast<uint4*>(dst + sw_offset(r, qc0 / 16 + c16, 128)) = make_uint4(w[0], w[1], w[2], w[3]);
+        if (DUMPING)
+          *reinterpret_cast<uint4*>(g_dump.dst + ((size_t)bh * N + j * kBlk + r) * N + i * kBlk + qc0 + c16 * 16) =
+              make_uint4(w[0], w[1], w[2], w[3]);
       }
 }
       if constexpr (QSMOOTH) rowsum_s[(it & 1) * kBlk * 2 + wg * kBlk + r] = rsum;
@@ -804,6 +819,8 @@ cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+cudaError_t set_bwd_dump(const BwdDump& d) { return cudaMemcpyToSymbol(g_dump, &d, sizeof(d)); }
 
 cudaError_t read_bwd_trace(void* host, size_t bytes) {
   if (bytes > sizeof(g_trace)) bytes = sizeof(g_trace);

@@ -75,6 +75,14 @@ struct BwdArgs {
 };
 cudaError_t launch_bwd(const BwdArgs& a, cudaStream_t s);
 cudaError_t read_bwd_trace(void* host, size_t bytes);  // profiling: K4 event timeline
+// test-only K4 tile dump (libsage_trace.so, SAGE_ABLATE bit 16): device pointers, [head][N kv][N q]
+// for the tiles, [head][T i][T j] for the scales; heads = 0 disables
+struct BwdDump {
+  int8_t *pt, *dst;
+  float *sp, *sds, *ds;
+  int heads;
+};
+cudaError_t set_bwd_dump(const BwdDump& d);
 
 // UMMA tile test (sage_debug_umma)
 cudaError_t launch_debug_umma(int mode, int K, int N, const CUtensorMap* tma, const CUtensorMap* tmb,

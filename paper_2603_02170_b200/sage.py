@@ -20,7 +20,7 @@ _STATUS = {0: "SAGE_OK", 1: "SAGE_ERR_INVALID_VALUE", 2: "SAGE_ERR_UNSUPPORTED",
 
 # exported symbols of include/sage.h
 SYMBOLS = ("sage_ctx_bytes", "sage_workspace_bytes", "sage_fwd", "sage_bwd", "sage_ctx_get_view",
-           "sage_ws_get_view", "sage_debug_umma", "sage_debug_trace", "sage_profile_enable", "sage_profile_read",
+           "sage_ws_get_view", "sage_debug_umma", "sage_debug_trace", "sage_debug_dump", "sage_profile_enable", "sage_profile_read",
            "sage_status_string", "sage_last_cuda_error", "sage_version")
 
 
@@ -63,11 +63,22 @@ def lib():
         L.sage_ws_get_view.argtypes = [pp, ctypes.c_int, P, ctypes.POINTER(SageWsView)]
         L.sage_debug_umma.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P]
         L.sage_debug_trace.argtypes = [P, S]
+        L.sage_debug_dump.argtypes = [P, P, P, P, P, ctypes.c_int]
         L.sage_profile_enable.argtypes = [ctypes.c_int]
         L.sage_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double)] * 2 + [ctypes.POINTER(ctypes.c_int64)] * 3
         L.sage_status_string.restype = ctypes.c_char_p
         _lib = L
     return _lib
+
+
+def use_library(path):
+    """Switch this binding to another build of the same C ABI (tests: libsage_trace.so for
+    sage_debug_dump); returns the previous path.  Workspaces are build-independent."""
+    global _lib, LIB_PATH
+    old = LIB_PATH
+    LIB_PATH, _lib = path, None
+    lib()
+    return old
 
 
 def _check(status, what):
@@ -224,6 +235,23 @@ def debug_umma(mode, a, b, K=None, N=None):
         out = torch.empty((128, N), dtype=torch.int32, device=a.device)
     _check(lib().sage_debug_umma(mode, K, N, _ptr(a), _ptr(b), _ptr(out), _stream(None)), "sage_debug_umma")
     return out
+
+
+def debug_dump(heads, N, device):
+    """Arm sage_debug_dump (libsage_trace.so only) for heads [0, heads) of sequence length N:
+    returns the device buffers every later sage_bwd fills (include/sage.h); heads=0 disarms."""
+    if heads == 0:
+        _check(lib().sage_debug_dump(None, None, None, None, None, 0), "sage_debug_dump")
+        return None
+    T = N // 128
+    bufs = dict(p_hat_t=torch.zeros((heads, N, N), dtype=torch.int8, device=device),
+                s_p=torch.zeros((heads, T, T), dtype=torch.float32, device=device),
+                ds_hat_t=torch.zeros((heads, N, N), dtype=torch.int8, device=device),
+                s_ds=torch.zeros((heads, T, T), dtype=torch.float32, device=device),
+                ds_t=torch.zeros((heads, N, N), dtype=torch.float32, device=device))
+    _check(lib().sage_debug_dump(_ptr(bufs["p_hat_t"]), _ptr(bufs["s_p"]), _ptr(bufs["ds_hat_t"]),
+                                 _ptr(bufs["s_ds"]), _ptr(bufs["ds_t"]), heads), "sage_debug_dump")
+    return bufs
 
 
 def profile_enable(on=True):

@@ -66,6 +66,22 @@ def test_error_paths_do_not_launch(L):
     assert L.sage_bwd(ctypes.byref(p), A, A, A, A, A, S(nctx), A, A, mis, A, S(nwb), z) == 3
     assert L.sage_debug_umma(7, 64, 128, A, A, A, z) == 1
     assert L.sage_debug_umma(1, 128, 96, A, A, A, z) == 1
+    # the tile dump exists only in the test build (libsage_trace.so)
+    assert L.sage_debug_dump(A, A, A, A, A, 1) == 2
+
+
+def test_trace_build_exports_the_same_abi():
+    """libsage_trace.so (timelines, tile dumps) exports the same C ABI and validates dump args."""
+    from paper_2603_02170_b200 import build, sage
+    if not os.path.exists(build.TRACE_LIB):
+        build.build(trace=True)
+    T = ctypes.CDLL(build.TRACE_LIB)
+    for name in sage.SYMBOLS:
+        assert hasattr(T, name), name
+    A, z = ctypes.c_void_p(0x10000), ctypes.c_void_p(0)
+    T.sage_debug_dump.argtypes = [ctypes.c_void_p] * 5 + [ctypes.c_int]
+    assert T.sage_debug_dump(A, A, z, A, A, 1) == 1
+    assert T.sage_debug_dump(A, A, A, A, A, -1) == 1
 
 
 @pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU behaviour")

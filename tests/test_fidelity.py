@@ -1,0 +1,211 @@
+"""Tier-C parity of K4's quantised backward intermediates, and the fidelity report.
+
+Both use libsage_trace.so's sage_debug_dump (include/sage.h): K4 writes its own P^, dS^ tiles,
+their scales and the pre-psi dS for the first heads, with the production kernel code.
+
+- Tier C: P^ = psi(P) and dS^ = psi(dS) pass through ex2.approx and fp32, so they are
+  compared statistically against the oracle (Alg. 2 lines 6 and 9, P:689 / P:695): almost every
+  element identical, none more than 1 LSB apart, tile scales within a few fp32 ulp.
+- Fidelity (BASELINE.json north_star: "Fidelity against an FP32 full-precision-attention oracle is
+  also reported, with dS error called out separately"): the CUDA path against FPA (oracle.fpa, fp64)
+  for O, dQ, dK, dV and the Table 2 components delta, P, dS (pre- and post-psi), on the Table 1
+  sigma sweep and the QK-norm on/off ablation.  The GPU's error against
+  FPA must match the quantised oracle's own error against FPA (the method's error, not the
+  kernel's), and follow Table 1's trend.  The numbers are written to gpurun_out/fidelity.json.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2603_02170_b200 import build, sage
+from paper_2603_02170_b200.inputs import make_inputs
+from tests.metrics import cos_sim, f64, rel_l2, round_bf16
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REPORT = os.path.join(ROOT, "gpurun_out", "fidelity.json")
+
+
+@pytest.fixture(scope="module")
+def dump_lib():
+    assert torch.cuda.is_available() and torch.cuda.get_device_capability() == (10, 0)
+    if not os.path.exists(build.TRACE_LIB):
+        build.build(trace=True)
+    oracle.build()
+    old = sage.use_library(build.TRACE_LIB)
+    yield
+    sage.debug_dump(0, 0, None)
+    sage.use_library(old)
+
+
+def _gpu_with_dump(q, k, v, do, causal, k_smooth, q_smooth):
+    B, H, N, d = q.shape
+    dev = torch.device("cuda")
+    qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
+    bufs = sage.debug_dump(B * H, N, dev)
+    o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth)
+    dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
+    torch.cuda.synchronize()
+    sage.debug_dump(0, 0, None)
+    # back to the oracle's [head][N q][N kv] layout
+    tiles = dict(p8=bufs["p_hat_t"].transpose(1, 2).cpu().numpy(), sp=bufs["s_p"].cpu().numpy(),
+                 ds8=bufs["ds_hat_t"].transpose(1, 2).cpu().numpy(), sds=bufs["s_ds"].cpu().numpy(),
+                 ds=bufs["ds_t"].transpose(1, 2).cpu().numpy().astype(np.float64))
+    wsb = sage._ws.get(ctx.params, True, dev)
+    wb = sage.ws_view(ctx.params, True, wsb)
+    off = wb.delta - wsb.data_ptr()
+    delta = wsb[off:off + B * H * N * 4].view(torch.float32).cpu().numpy().astype(np.float64).reshape(B * H, N)
+    flat = lambda t: f64(t).reshape(B * H, N, d)
+    return dict(o=flat(o), dq=flat(dq), dk=flat(dk), dv=flat(dv), delta=delta, **tiles)
+
+
+def _oracle_run(q, k, v, do, causal, k_smooth, q_smooth):
+    B, H, N, d = q.shape
+    qn, kn, vn, don = (f64(t).reshape(B * H, N, d) for t in (q, k, v, do))
+    kw = dict(causal=causal, k_smooth=k_smooth, q_smooth=q_smooth)
+    oracle.set_threads(min(8, os.cpu_count() or 1))
+    f = oracle.fwd(qn, kn, vn, **kw)
+    b = oracle.bwd(qn, kn, vn, round_bf16(f["o"]), don, f["lse"], tiles=True, **kw)
+    return f, b
+
+
+def _processed_tiles(T, causal):
+    return [(i, j) for i in range(T) for j in range(T) if not causal or j <= i]
+
+
+def _tier_c(g, b, N, causal):
+    """P^, dS^ element agreement over the processed tiles, and scale agreement (in fp32 ulps)."""
+    T = N // 128
+    tiles = _processed_tiles(T, causal)
+    mask = np.zeros((N, N), bool)
+    for i, j in tiles:
+        mask[i * 128:(i + 1) * 128, j * 128:(j + 1) * 128] = True
+    out = {}
+    for name in ("p8", "ds8"):
+        a = g[name][:, mask].astype(int)
+        r = b[name][:, mask].astype(int)
+        out[name] = dict(identical=float((a == r).mean()), max_abs_diff=int(np.abs(a - r).max()))
+    for name in ("sp", "sds"):
+        ii, jj = zip(*tiles)
+        a = g[name][:, ii, jj].astype(np.float64)
+        r = b[name][:, ii, jj].astype(np.float64)
+        ulp = np.spacing(np.abs(r).astype(np.float32)).astype(np.float64)
+        out[name] = dict(max_ulp=float((np.abs(a - r) / np.where(ulp > 0, ulp, 1)).max()))
+    out["ds_pre_psi_rel_l2"] = rel_l2(b["ds"][:, mask], g["ds"][:, mask])
+    return out
+
+
+TIER_C = [
+    # (B, H, N, d, causal, k_smooth, q_smooth, recipe)
+    (1, 2, 384, 64, True, True, False, "qknorm"),
+    (1, 2, 256, 64, False, True, False, "gauss"),
+    (1, 2, 384, 128, True, True, True, "outlier_kq"),
+    (1, 2, 256, 128, False, True, False, "qknorm"),
+]
+
+
+@pytest.mark.parametrize("B,H,N,d,causal,ks,qs,recipe", TIER_C)
+def test_tier_c_backward_tiles(dump_lib, B, H, N, d, causal, ks, qs, recipe):
+    """Tier C (SURVEY.md 8(c) parity contract): >= 99.9% of P^ and dS^ elements identical to the
+    oracle's, all within 1 LSB; s_P, s_dS within 64 fp32 ulp; pre-psi dS within 1e-3 rel-L2."""
+    q, k, v, do = make_inputs(B, H, N, d, recipe, seed=300 + N + d)
+    g = _gpu_with_dump(q, k, v, do, causal, ks, qs)
+    f, b = _oracle_run(q, k, v, do, causal, ks, qs)
+    res = _tier_c(g, b, N, causal)
+    _write_report(f"tier_c/B{B}H{H}N{N}d{d}{'c' if causal else 'n'}{'ks' if ks else ''}{'qs' if qs else ''}_{recipe}", res)
+    for name in ("p8", "ds8"):
+        assert res[name]["identical"] >= 0.999 and res[name]["max_abs_diff"] <= 1, (name, res)
+    assert res["sp"]["max_ulp"] <= 64 and res["sds"]["max_ulp"] <= 64, res
+    assert res["ds_pre_psi_rel_l2"] <= 1e-3, res
+    # skipped (causal) tiles are never written
+    if causal:
+        assert not g["ds8"][:, :128, 128:].any()
+
+
+def _fidelity_row(g, b, f, ref, N, causal):
+    """Errors vs FPA (fp64) of the GPU path and of the quantised oracle (QO), Table 1/2 style."""
+    T = N // 128
+    deq = lambda x8, s: x8.astype(np.float64) * np.kron(s.astype(np.float64), np.ones((1, 128, 128)))
+    row = {}
+    for name, fpa_key in (("o", "o"), ("dq", "dq"), ("dk", "dk"), ("dv", "dv")):
+        qo = f["o"] if name == "o" else b[name]
+        row[name] = dict(gpu_rel_l2=rel_l2(ref[fpa_key], g[name]), gpu_cos=cos_sim(ref[fpa_key], g[name]),
+                         oracle_rel_l2=rel_l2(ref[fpa_key], qo))
+    row["delta"] = dict(gpu_rel_l2=rel_l2(ref["delta"], g["delta"]), oracle_rel_l2=rel_l2(ref["delta"], b["delta"]))
+    row["P"] = dict(gpu_rel_l2=rel_l2(ref["P"], deq(g["p8"], g["sp"])),
+                    oracle_rel_l2=rel_l2(ref["P"], deq(b["p8"], b["sp"])))
+    row["dS_pre_psi"] = dict(gpu_rel_l2=rel_l2(ref["dS"], g["ds"]), oracle_rel_l2=rel_l2(ref["dS"], b["ds"]))
+    row["dS"] = dict(gpu_rel_l2=rel_l2(ref["dS"], deq(g["ds8"], g["sds"])),
+                     oracle_rel_l2=rel_l2(ref["dS"], deq(b["ds8"], b["sds"])))
+    return row
+
+
+def _fpa(q, k, v, do, causal):
+    B, H, N, d = q.shape
+    qn, kn, vn, don = (f64(t).reshape(B * H, N, d) for t in (q, k, v, do))
+    return oracle.fpa(qn, kn, vn, don, causal=causal, intermediates=True)
+
+
+def _write_report(key, rows):
+    os.makedirs(os.path.dirname(REPORT), exist_ok=True)
+    rep = json.load(open(REPORT)) if os.path.exists(REPORT) else {}
+    rep[key] = rows
+    json.dump(rep, open(REPORT, "w"), indent=1, sort_keys=True)
+
+
+def _assert_gpu_tracks_oracle(row, what):
+    """The GPU's error vs FPA is the method's error: within 5% (+1e-4) of the oracle's own."""
+    for name in ("o", "dq", "dk", "dv", "P", "dS"):
+        gr, orr = row[name]["gpu_rel_l2"], row[name]["oracle_rel_l2"]
+        assert abs(gr - orr) <= 0.05 * orr + 1e-4, (what, name, gr, orr)
+
+
+TABLE1 = {1.0: (0.0160, 0.0184, 0.0220, 0.0159), 3.0: (0.0389, 0.0758, 0.0777, 0.0387),
+          5.0: (0.0603, 0.2014, 0.2007, 0.0605), 8.0: (0.0972, 0.4666, 0.4699, 0.0973),
+          10.0: (0.1161, 0.6648, 0.6684, 0.1157)}  # P:375-379 (O, dQ, dK, dV rel-L2)
+
+
+def test_fidelity_table1_sigma_sweep(dump_lib):
+    """Table 1 on the GPU: Gaussian Q, K with sigma in {1, 3, 5, 8, 10}, N = 1024,
+    d = 64, non-causal, K-smoothing on (the oracle's Table 1 pin setting)."""
+    B, H, N, d = 1, 2, 1024, 64
+    rows = {}
+    for sigma in sorted(TABLE1):
+        q, k, v, do = make_inputs(B, H, N, d, "gauss", seed=11, sigma=sigma)
+        g = _gpu_with_dump(q, k, v, do, False, True, False)
+        f, b = _oracle_run(q, k, v, do, False, True, False)
+        row = _fidelity_row(g, b, f, _fpa(q, k, v, do, False), N, False)
+        row["paper"] = dict(zip(("o", "dq", "dk", "dv"), TABLE1[sigma]))
+        _assert_gpu_tracks_oracle(row, sigma)
+        rows[str(sigma)] = row
+    _write_report("table1_sigma_sweep", dict(setting=f"B={B} H={H} N={N} d={d} non-causal K-smooth, gauss(sigma)",
+                                             rows=rows))
+    for name in ("o", "dq", "dk"):
+        rels = [rows[str(s)][name]["gpu_rel_l2"] for s in sorted(TABLE1)]
+        assert all(a < c for a, c in zip(rels, rels[1:])), (name, rels)
+    # dS is the largest error source of the backward: above dV's and O's
+    for s in sorted(TABLE1):
+        r = rows[str(s)]
+        assert r["dS"]["gpu_rel_l2"] > max(r["dv"]["gpu_rel_l2"], r["o"]["gpu_rel_l2"]), (s, r)
+
+
+def test_fidelity_qknorm_ablation(dump_lib):
+    """C5's QK-norm on vs off ablation at a reduced size: with QK-norm the logits stay
+    small and every tensor is closer to FPA than without (P:486-506's mechanism)."""
+    B, H, N, d = 1, 2, 1024, 128
+    rows = {}
+    for recipe in ("qknorm", "noqknorm"):
+        q, k, v, do = make_inputs(B, H, N, d, recipe, seed=5000)
+        g = _gpu_with_dump(q, k, v, do, True, True, False)
+        f, b = _oracle_run(q, k, v, do, True, True, False)
+        row = _fidelity_row(g, b, f, _fpa(q, k, v, do, True), N, True)
+        _assert_gpu_tracks_oracle(row, recipe)
+        rows[recipe] = row
+    _write_report("qknorm_ablation", dict(setting=f"B={B} H={H} N={N} d={d} causal K-smooth", rows=rows))
+    for name in ("dq", "dk", "dS"):
+        assert rows["qknorm"][name]["gpu_rel_l2"] < rows["noqknorm"][name]["gpu_rel_l2"], (name, rows)

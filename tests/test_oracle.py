@@ -287,3 +287,34 @@ def test_q_smoothing_bias_pathways(orc):
     res = _fidelity(orc, q, k, v, do, causal=True, k_smooth=True, q_smooth=True)
     assert res["o"][1] < 0.06
     assert res["dk"][1] < 0.15 and res["dq"][1] < 0.15
+
+
+def test_bwd_tile_dumps(orc):
+    """The tile dumps (Tier-C and fidelity reports) are Alg. 2's own intermediates:
+    - quant-off dS equals FPA's dS = P o (dP - delta) element-wise, so its
+      rows sum to 0 (sum_n P (dP - delta) = delta - delta, S:203);
+    - quantised mode: each dumped dS^ tile is psi of the dumped pre-psi dS tile (line 9, A4, A11):
+      max|dS^| = 127 for a nonzero tile and |dS - dS^ s_dS| <= s_dS/2;
+    - psi(P) per tile (line 6): P^ in [0, 127], 127 attained, s_P = max P / 127 with P = exp(S - L)
+      <= 1, and tiles a causal run skips (above the diagonal) stay empty."""
+    q, k, v, do = (f64(t).reshape(1, 384, 64) for t in make_inputs(1, 1, 384, 64, "gauss", seed=21, sigma=2.0))
+    exact = orc.fwd(q, k, v, causal=True, quant=False)
+    be = orc.bwd(q, k, v, exact["o"], do, exact["lse"], causal=True, quant=False, tiles=True)
+    ref = orc.fpa(q, k, v, do, causal=True, intermediates=True)
+    np.testing.assert_allclose(be["ds"], ref["dS"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(be["ds"].sum(2), 0.0, rtol=0, atol=1e-12)
+
+    f = orc.fwd(q, k, v, causal=True)
+    b = orc.bwd(q, k, v, f["o"], do, f["lse"], causal=True, tiles=True)
+    for i in range(3):
+        for j in range(3):
+            blk = np.s_[0, i * 128:(i + 1) * 128, j * 128:(j + 1) * 128]
+            ds, ds8, sds = b["ds"][blk], b["ds8"][blk].astype(np.float64), float(b["sds"][0, i, j])
+            p8, sp = b["p8"][blk].astype(int), float(b["sp"][0, i, j])
+            if j > i:
+                assert sds == 0.0 and sp == 0.0 and not ds8.any() and not p8.any()
+                continue
+            assert np.abs(ds8).max() == 127
+            assert sds == pytest.approx(np.abs(ds).max() / 127.0, rel=2 ** -23)
+            assert np.abs(ds - ds8 * sds).max() <= sds * (0.5 + 2 ** -15)
+            assert p8.min() >= 0 and p8.max() == 127 and 0.0 < sp <= 1.0 / 127.0 * (1 + 2 ** -23)
