@@ -9,7 +9,7 @@ import subprocess
 
 import numpy as np
 
-CAUSAL, K_SMOOTH, Q_SMOOTH, QUANT_OFF = 1, 2, 4, 8
+CAUSAL, K_SMOOTH, Q_SMOOTH, QUANT_OFF, P_U8 = 1, 2, 4, 8, 16
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sage_oracle.c")
@@ -38,7 +38,7 @@ def _load():
         _lib.oracle_bwd.argtypes = [I, I, I, I, I, D] + [P] * 17
         _lib.oracle_fpa.argtypes = [I, I, I, I, D] + [P] * 13
         _lib.oracle_psi_block.argtypes = [P, I, I, P, P]
-        _lib.oracle_psi_token_row.argtypes = [P, I, D, P]
+        _lib.oracle_psi_token_row.argtypes = [P, I, D, I, P]
         _lib.oracle_psi_token_row.restype = D
         _lib.oracle_set_threads.argtypes = [I]
         _lib.oracle_max_threads.restype = I
@@ -70,11 +70,12 @@ def psi_block(x, fp32_product=True):
     return q, float(s[0])
 
 
-def psi_token_row(pt, rm_minus_m):
-    """Per-token P quantisation of one row (Alg. 1 line 9).  Returns (uint8 values, s_P)."""
+def psi_token_row(pt, rm_minus_m, pmax=127):
+    """Per-token P quantisation of one row (Alg. 1 line 9; pmax 255: the u8 variant).
+    Returns (integer values, s_P)."""
     pt = _f64(pt)
-    q = np.zeros(pt.shape, dtype=np.int8)
-    sp = _load().oracle_psi_token_row(_p(pt), pt.size, float(rm_minus_m), _p(q))
+    q = np.zeros(pt.shape, dtype=np.int16)
+    sp = _load().oracle_psi_token_row(_p(pt), pt.size, float(rm_minus_m), int(pmax), _p(q))
     return q, sp
 
 
@@ -82,13 +83,17 @@ def _default_tau(d, tau):
     return 1.0 / np.sqrt(d) if tau is None else float(tau)
 
 
-def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk=128, tau=None):
+def _flags(causal, k_smooth, q_smooth, quant, p_u8):
+    return (CAUSAL if causal else 0) | (K_SMOOTH if k_smooth else 0) | (Q_SMOOTH if q_smooth else 0) | \
+        (0 if quant else QUANT_OFF) | (P_U8 if p_u8 else 0)
+
+
+def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk=128, tau=None, p_u8=False):
     """Alg. 1 per head.  Returns dict with o, lse and the Tier-A intermediates."""
     q, k, v = _f64(q), _f64(k), _f64(v)
     BH, N, d = q.shape
     T = N // blk
-    flags = (CAUSAL if causal else 0) | (K_SMOOTH if k_smooth else 0) | \
-            (Q_SMOOTH if q_smooth else 0) | (0 if quant else QUANT_OFF)
+    flags = _flags(causal, k_smooth, q_smooth, quant, p_u8)
     out = dict(o=np.zeros((BH, N, d)), lse=np.zeros((BH, N)),
                mu_k=np.zeros((BH, d), np.float32), mu_q=np.zeros((BH, T, d), np.float32),
                bias=np.zeros((BH, T, N)),
@@ -106,22 +111,21 @@ def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk
 
 
 def bwd(q, k, v, o_stored, do, lse, *, causal=False, k_smooth=True, q_smooth=False, quant=True,
-        blk=128, tau=None, tiles=False):
+        blk=128, tau=None, tiles=False, p_u8=False):
     """Alg. 2 per head.  o_stored is the O the forward stored (A15).
 
-    tiles=True also returns the per-tile quantised P^ / dS^ ([BH, N q, N kv] int8, tile (i, j) at
+    tiles=True also returns the per-tile quantised P^ / dS^ ([BH, N q, N kv] uint8 / int8, tile (i, j) at
     rows i*blk.., columns j*blk..), their psi scales s_P / s_dS ([BH, T i, T j] fp32) and the
     pre-psi dS ([BH, N, N] double); tiles a causal run skips stay zero."""
     q, k, v, o_stored, do, lse = map(_f64, (q, k, v, o_stored, do, lse))
     BH, N, d = q.shape
     T = N // blk
-    flags = (CAUSAL if causal else 0) | (K_SMOOTH if k_smooth else 0) | \
-            (Q_SMOOTH if q_smooth else 0) | (0 if quant else QUANT_OFF)
+    flags = _flags(causal, k_smooth, q_smooth, quant, p_u8)
     out = dict(dq=np.zeros((BH, N, d)), dk=np.zeros((BH, N, d)), dv=np.zeros((BH, N, d)),
                delta=np.zeros((BH, N)), do8=np.zeros((BH, N, d), np.int8),
                sdo=np.zeros((BH, T), np.float32))
     if tiles:
-        out.update(p8=np.zeros((BH, N, N), np.int8), sp=np.zeros((BH, T, T), np.float32),
+        out.update(p8=np.zeros((BH, N, N), np.uint8), sp=np.zeros((BH, T, T), np.float32),
                    ds8=np.zeros((BH, N, N), np.int8), sds=np.zeros((BH, T, T), np.float32),
                    ds=np.zeros((BH, N, N)))
     rc = _load().oracle_bwd(BH, N, d, blk, flags, _default_tau(d, tau), _p(q), _p(k), _p(v),

@@ -36,6 +36,8 @@
 #define ORC_K_SMOOTH  2   /* K <- K - mean_row(K) */
 #define ORC_Q_SMOOTH  4   /* Q_i <- Q_i - mean_row(Q_i), bias added back */
 #define ORC_QUANT_OFF 8   /* psi = identity, no FP32 emulation: tiled full-precision attention */
+#define ORC_P_U8     16   /* unsigned 8-bit P^ (0..255, scale max/255) instead of 0..127: the
+                             u8 x s8 variant; psi(dS), psi(Q/K/V/dO) unchanged */
 
 void oracle_set_threads(int n) {
 #ifdef _OPENMP
@@ -60,7 +62,7 @@ int oracle_max_threads(void) {
  *   q     = clamp(RNE(x * inv), -127, 127)                          (A1, A2)
  * fp32_product != 0: x*inv is an FP32 multiply (inputs Q,K,V,dO are FP32
  * values); otherwise the product is taken in double (P and dS, A4).          */
-static void psi_block(const double *x, int n, int fp32_product, int quant_off,
+static void psi_block(const double *x, int n, int fp32_product, int quant_off, double qmax,
                       int8_t *q, double *scale_out, double *xq_out) {
   double amax = 0.0;
   for (int e = 0; e < n; ++e) {
@@ -73,8 +75,9 @@ static void psi_block(const double *x, int n, int fp32_product, int quant_off,
     return;
   }
   float famax = (float)amax;    /* exact: x are FP32 values or amax rounds once */
-  float scale = famax / 127.0f;
-  float inv = famax > 0.0f ? 127.0f / famax : 0.0f;
+  float fq = (float)qmax;       /* 127, or 255 for the unsigned P^ variant */
+  float scale = famax / fq;
+  float inv = famax > 0.0f ? fq / famax : 0.0f;
   for (int e = 0; e < n; ++e) {
     double y;
     if (fp32_product) {
@@ -84,9 +87,9 @@ static void psi_block(const double *x, int n, int fp32_product, int quant_off,
       y = x[e] * (double)inv;
     }
     double r = nearbyint(y);       /* round half to even (default mode) */
-    if (r > 127.0) r = 127.0;
-    if (r < -127.0) r = -127.0;
-    q[e] = (int8_t)r;
+    if (r > qmax) r = qmax;
+    if (r < -qmax) r = -qmax;
+    if (q) q[e] = (int8_t)r;
     if (xq_out) xq_out[e] = r;
   }
   *scale_out = (double)scale;
@@ -94,25 +97,25 @@ static void psi_block(const double *x, int n, int fp32_product, int quant_off,
 
 /* Exported for the worked-example pins. */
 void oracle_psi_block(const double *x, int n, int fp32_product, int8_t *q, double *scale) {
-  psi_block(x, n, fp32_product, 0, q, scale, NULL);
+  psi_block(x, n, fp32_product, 0, 127.0, q, scale, NULL);
 }
 
 /* Per-token P quantisation, Alg. 1 line 9:
  *   s_P = exp(rowmax(S_ij) - m_ij) / 127,  P^_ij = P~_ij / s_P  (rounded, A1/A2)
  * pt: one row of P~ = exp(S - m_ij); rm_minus_m = rowmax(S_ij) - m_ij.       */
-static double psi_token_row(const double *pt, int n, double rm_minus_m, int8_t *q) {
-  double sp = exp(rm_minus_m) / 127.0;
+static double psi_token_row(const double *pt, int n, double rm_minus_m, double pmax, int16_t *q) {
+  double sp = exp(rm_minus_m) / pmax;   /* pmax = 127, or 255 with ORC_P_U8 */
   for (int e = 0; e < n; ++e) {
     double r = nearbyint(pt[e] / sp);
-    if (r > 127.0) r = 127.0;
+    if (r > pmax) r = pmax;
     if (r < 0.0) r = 0.0;
-    q[e] = (int8_t)r;
+    q[e] = (int16_t)r;
   }
   return sp;
 }
 
-double oracle_psi_token_row(const double *pt, int n, double rm_minus_m, int8_t *q) {
-  return psi_token_row(pt, n, rm_minus_m, q);
+double oracle_psi_token_row(const double *pt, int n, double rm_minus_m, int pmax, int16_t *q) {
+  return psi_token_row(pt, n, rm_minus_m, (double)pmax, q);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -193,8 +196,8 @@ static void prep_head(head_prep *h, const double *q, const double *k, int N, int
   /* Alg. 1 line 3: per-block psi of Q_i, K_j. */
   for (int t = 0; t < T; ++t) {
     size_t off = (size_t)t * blk * d;
-    psi_block(h->qs + off, blk * d, 1, qo, h->q8 + off, &h->sq[t], h->qx + off);
-    psi_block(h->ks + off, blk * d, 1, qo, h->k8 + off, &h->sk[t], h->kx + off);
+    psi_block(h->qs + off, blk * d, 1, qo, 127.0, h->q8 + off, &h->sq[t], h->qx + off);
+    psi_block(h->ks + off, blk * d, 1, qo, 127.0, h->k8 + off, &h->sk[t], h->kx + off);
   }
 }
 
@@ -245,11 +248,12 @@ static void fwd_head(const double *q, const double *k, const double *v, int N, i
   double *sv = malloc(T * sizeof(double));
   for (int t = 0; t < T; ++t) {
     size_t off = (size_t)t * blk * d;
-    psi_block(v + off, blk * d, 1, qo, v8 + off, &sv[t], vx + off);
+    psi_block(v + off, blk * d, 1, qo, 127.0, v8 + off, &sv[t], vx + off);
   }
   double *S = malloc((size_t)blk * blk * sizeof(double));
   double *Pt = malloc((size_t)blk * blk * sizeof(double));
-  int8_t *Ph = malloc((size_t)blk * blk);
+  int16_t *Ph = malloc((size_t)blk * blk * sizeof(int16_t));
+  double pmax = (flags & ORC_P_U8) ? 255.0 : 127.0;
   double *acc = malloc((size_t)blk * d * sizeof(double));
   double *m = malloc(blk * sizeof(double)), *l = malloc(blk * sizeof(double));
 
@@ -278,8 +282,8 @@ static void fwd_head(const double *q, const double *k, const double *v, int N, i
             ar[c] = alpha * ar[c] + pv;
           }
         } else {
-          int8_t *Phr = Ph + (size_t)r * blk;
-          double sp = psi_token_row(Pr, blk, rm - mnew, Phr);   /* line 9 */
+          int16_t *Phr = Ph + (size_t)r * blk;
+          double sp = psi_token_row(Pr, blk, rm - mnew, pmax, Phr);   /* line 9 */
           for (int c = 0; c < d; ++c) {                            /* line 10 */
             int32_t pv = 0;
             for (int n = 0; n < blk; ++n)
@@ -337,7 +341,7 @@ int oracle_fwd(int BH, int N, int d, int blk, int flags, double tau,
 static void bwd_head(const double *q, const double *k, const double *v, const double *o_stored,
                      const double *dO, const double *lse, int N, int d, int blk, int flags, double tau,
                      double *dq, double *dk, double *dv, double *delta_out, int8_t *do8_out, float *sdo_out,
-                     int8_t *p8_out, float *sp_out, int8_t *ds8_out, float *sds_out, double *ds_out) {
+                     uint8_t *p8_out, float *sp_out, int8_t *ds8_out, float *sds_out, double *ds_out) {
   head_prep h;
   prep_head(&h, q, k, N, d, blk, flags);
   int T = h.T, qo = (flags & ORC_QUANT_OFF) != 0, causal = (flags & ORC_CAUSAL) != 0;
@@ -355,11 +359,12 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
   double *sdo = malloc(T * sizeof(double));
   for (int t = 0; t < T; ++t) {
     size_t off = (size_t)t * blk * d;
-    psi_block(dO + off, blk * d, 1, qo, do8 + off, &sdo[t], dox + off);
+    psi_block(dO + off, blk * d, 1, qo, 127.0, do8 + off, &sdo[t], dox + off);
   }
   double *S = malloc(bb * sizeof(double)), *P = malloc(bb * sizeof(double));
   double *dS = malloc(bb * sizeof(double)), *Px = malloc(bb * sizeof(double)), *dSx = malloc(bb * sizeof(double));
-  int8_t *P8 = malloc(bb), *dS8 = malloc(bb);
+  int8_t *dS8 = malloc(bb);
+  double pmax = (flags & ORC_P_U8) ? 255.0 : 127.0;
   memset(dq, 0, nd * sizeof(double));
   memset(dk, 0, nd * sizeof(double));
   memset(dv, 0, nd * sizeof(double));
@@ -375,7 +380,7 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
         }
       /* line 6: psi(P_ij) over the whole B_q x B_kv tile (A11). */
       double sp;
-      psi_block(P, (int)bb, 0, qo, P8, &sp, Px);
+      psi_block(P, (int)bb, 0, qo, pmax, NULL, &sp, Px);  /* Px: the integer P^ (0..pmax) */
       /* line 7: dV_j += MM(P^_ij^T, dO^_i) x s_P x s_dO. */
       for (int n = 0; n < blk; ++n)
         for (int c = 0; c < d; ++c) {
@@ -387,7 +392,7 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
           } else {
             int32_t a = 0;
             for (int r = 0; r < blk; ++r)
-              a += (int32_t)P8[(size_t)r * blk + n] * (int32_t)do8[(size_t)(i * blk + r) * d + c];
+              a += (int32_t)Px[(size_t)r * blk + n] * (int32_t)do8[(size_t)(i * blk + r) * d + c];
             val = (double)a * sp * sdo[i];
           }
           dv[(size_t)(j * blk + n) * d + c] += val;
@@ -401,12 +406,12 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
           dS[(size_t)r * blk + n] = P[(size_t)r * blk + n] * (a - delta[i * blk + r]);
         }
       double sds;
-      psi_block(dS, (int)bb, 0, qo, dS8, &sds, dSx);
+      psi_block(dS, (int)bb, 0, qo, 127.0, dS8, &sds, dSx);
       /* optional tile dumps (test infrastructure: Tier-C and fidelity reports), [N q][N kv] */
       for (int r = 0; r < blk; ++r)
         for (int n = 0; n < blk; ++n) {
           size_t g = (size_t)(i * blk + r) * N + (size_t)j * blk + n, t = (size_t)r * blk + n;
-          if (p8_out) p8_out[g] = P8[t];
+          if (p8_out) p8_out[g] = (uint8_t)Px[t];
           if (ds8_out) ds8_out[g] = dS8[t];
           if (ds_out) ds_out[g] = dS[t];
         }
@@ -455,7 +460,7 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
   if (do8_out) memcpy(do8_out, do8, nd);
   if (sdo_out) for (int t = 0; t < T; ++t) sdo_out[t] = (float)sdo[t];
   free(delta); free(dox); free(do8); free(sdo); free(S); free(P); free(dS); free(Px); free(dSx);
-  free(P8); free(dS8);
+  free(dS8);
   prep_free(&h);
 }
 
@@ -464,7 +469,7 @@ int oracle_bwd(int BH, int N, int d, int blk, int flags, double tau,
                const double *dO, const double *lse,
                double *dq, double *dk, double *dv,
                double *delta, int8_t *do8, float *sdo,
-               int8_t *p8, float *sp, int8_t *ds8, float *sds, double *ds) {
+               uint8_t *p8, float *sp, int8_t *ds8, float *sds, double *ds) {
   if (BH <= 0 || N <= 0 || d <= 0 || blk <= 0 || N % blk) return -1;
   int T = N / blk;
   size_t nd = (size_t)N * d;

@@ -318,3 +318,33 @@ def test_bwd_tile_dumps(orc):
             assert sds == pytest.approx(np.abs(ds).max() / 127.0, rel=2 ** -23)
             assert np.abs(ds - ds8 * sds).max() <= sds * (0.5 + 2 ** -15)
             assert p8.min() >= 0 and p8.max() == 127 and 0.0 < sp <= 1.0 / 127.0 * (1 + 2 ** -23)
+
+
+def test_p_u8_variant(orc):
+    """Unsigned P^ (readings A2/A10 with 255 levels): P~ >= 0, so the
+    per-token scale s_P = rowmax(P~)/255 (Alg. 1 line 9 with 255 for 127) and psi(P) over the
+    backward tile (line 6) use 0..255.  Pins: the S:150 example at 255 levels; every tile's P^
+    attains 255 with s_P = max P / 255; halving the rounding step lowers O's and dV's error
+    against FPA (both carry P^'s rounding noise) while dQ/dK (dominated by dS) barely move."""
+    q, sp = orc.psi_token_row(np.array([1.0, 0.5]), 0.0, pmax=255)
+    assert list(q) == [255, 128] and sp == pytest.approx(1.0 / 255.0, rel=1e-15)
+    errs = {}
+    for u8 in (False, True):
+        acc = {"o": [], "dv": [], "dq": []}
+        for seed, recipe in ((31, "gauss"), (32, "qknorm")):
+            q, k, v, do = (f64(t).reshape(2, 512, 64) for t in make_inputs(1, 2, 512, 64, recipe, seed=seed))
+            ref = orc.fpa(q, k, v, do, causal=True)
+            f = orc.fwd(q, k, v, causal=True, p_u8=u8)
+            b = orc.bwd(q, k, v, f["o"], do, f["lse"], causal=True, p_u8=u8, tiles=True)
+            acc["o"].append(rel_l2(ref["o"], f["o"]))
+            acc["dv"].append(rel_l2(ref["dv"], b["dv"]))
+            acc["dq"].append(rel_l2(ref["dq"], b["dq"]))
+            if u8:
+                for i in range(4):
+                    p8 = b["p8"][0, i * 128:(i + 1) * 128, i * 128:(i + 1) * 128]
+                    assert p8.max() == 255
+                    assert float(b["sp"][0, i, i]) <= 1.0 / 255.0 * (1 + 2 ** -23)
+        errs[u8] = {k_: float(np.mean(v_)) for k_, v_ in acc.items()}
+    assert errs[True]["o"] < 0.95 * errs[False]["o"], errs
+    assert errs[True]["dv"] < 0.7 * errs[False]["dv"], errs
+    assert abs(errs[True]["dq"] - errs[False]["dq"]) < 0.25 * errs[False]["dq"], errs
