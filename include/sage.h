@@ -60,7 +60,11 @@ typedef enum {
 enum {
   SAGE_CAUSAL = 1u << 0,   /* mask key n > query r (reading A14) */
   SAGE_K_SMOOTH = 1u << 1, /* K-smoothing, P:136-147 (the paper's default) */
-  SAGE_Q_SMOOTH = 1u << 2  /* block-wise Q-smoothing + bias */
+  SAGE_Q_SMOOTH = 1u << 2, /* block-wise Q-smoothing + bias */
+  SAGE_P_U8 = 1u << 3      /* variant: P^ unsigned in 0..255 with scale max/255,
+                              for the per-token P^ of Alg. 1 line 9 and psi(P) of Alg. 2 line 6 (the
+                              paper's reading: 0..127, A2); the PV / dV MMAs run u8 x s8.  Halves P^'s
+                              rounding step at no cost: lower O and dV error vs full precision. */
 };
 
 typedef struct {
@@ -114,7 +118,8 @@ SAGE_API sage_status sage_ws_get_view(const sage_params* p, int backward, void* 
  * operands K-major (K in {64,128}, N = 128);  mode 1: A K-major [128][128] written by
  * threads (P^ path), B MN-major [128][N] (N in {64,128}); mode 2: A MN-major [K=128][M=128],
  * B MN-major [128][N]; mode 3: fp32 D = A . B^T, bf16 K-major operands [128][K], [128][K];
- * modes 4 / 5: as 1 / 3 with the A operand read from TMEM (written there by threads).
+ * modes 4 / 5: as 1 / 3 with the A operand read from TMEM (written there by threads);
+ * modes 6 / 7: as 1 / 4 with an unsigned u8 A operand (values 0..255, the SAGE_P_U8 P^ paths).
  * a, b, d: device pointers to row-major host-order arrays as described (int8/bf16 in, int32/fp32 out). */
 SAGE_API sage_status sage_debug_umma(int mode, int K, int N, const void* a, const void* b, void* d, void* stream);
 

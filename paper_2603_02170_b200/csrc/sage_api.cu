@@ -66,7 +66,7 @@ size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Dims {
   size_t BH, N, d, T;
-  bool causal, ks, qs;
+  bool causal, ks, qs, pu8;
   float tau;
 };
 
@@ -75,7 +75,7 @@ bool dims_of(const sage_params* p, Dims* o) {
   if (p->batch <= 0 || p->heads <= 0 || p->seqlen <= 0) return false;
   if (p->head_dim != 64 && p->head_dim != 128) return false;
   if (p->seqlen % kBlk || p->seqlen > kMaxSeqLen) return false;
-  if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH)) return false;
+  if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH | SAGE_P_U8)) return false;
   if (!(p->softmax_scale >= 0.f) || std::isinf(p->softmax_scale)) return false;
   const size_t BH = (size_t)p->batch * p->heads;
   if (BH * p->seqlen > (size_t)INT32_MAX / 2) return false;  // TMA row coordinates are int32
@@ -86,6 +86,7 @@ bool dims_of(const sage_params* p, Dims* o) {
   o->causal = p->flags & SAGE_CAUSAL;
   o->ks = p->flags & SAGE_K_SMOOTH;
   o->qs = p->flags & SAGE_Q_SMOOTH;
+  o->pu8 = p->flags & SAGE_P_U8;
   o->tau = p->softmax_scale > 0.f ? p->softmax_scale : 1.f / std::sqrt((float)p->head_dim);
   return true;
 }
@@ -374,6 +375,7 @@ sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const v
   a.tau = D.tau;
   a.causal = D.causal;
   a.qsmooth = D.qs;
+  a.pu8 = D.pu8;
   a.ablate = ablate_flags();
   if ((e = timed(0, s, [&] { return launch_fwd(a, s); })) != cudaSuccess) return cuda_fail(e);
   if (g_prof.on) g_prof.launches += (D.ks ? 2 : 1) + (D.qs ? 3 : 0) + 1 + 1;
@@ -429,6 +431,7 @@ sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const f
   a.tau = D.tau;
   a.causal = D.causal;
   a.qsmooth = D.qs;
+  a.pu8 = D.pu8;
   a.ablate = ablate_flags() | (g_dump_heads > 0 ? 16 : 0);
   if ((e = timed(1, s, [&] { return launch_bwd(a, s); })) != cudaSuccess) return cuda_fail(e);
   if (g_prof.on) g_prof.launches += 3;
@@ -461,7 +464,7 @@ sage_status sage_debug_dump(void* p_hat_t, float* s_p, void* ds_hat_t, float* s_
 }
 
 sage_status sage_debug_umma(int mode, int K, int N, const void* a, const void* b, void* d, void* stream) {
-  if (mode < 0 || mode > 5 || !a || !b || !d) return SAGE_ERR_INVALID_VALUE;
+  if (mode < 0 || mode > 7 || !a || !b || !d) return SAGE_ERR_INVALID_VALUE;
   const bool kmode = mode == 0 || mode == 3 || mode == 5;
   if (kmode && K != 64 && K != 128) return SAGE_ERR_INVALID_VALUE;
   if (!kmode && N != 64 && N != 128) return SAGE_ERR_INVALID_VALUE;

@@ -125,8 +125,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* __restrict__ k_scale, const float* __restrict__ do_scale,
                     const float* __restrict__ l2g, const float* __restrict__ deltag, const float* __restrict__ bias,
                     const float* __restrict__ mu_q, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dk,
-                    __nv_bfloat16* __restrict__ dv, int N, int BH, float tau, int ablate_arg) {
+                    __nv_bfloat16* __restrict__ dv, int N, int BH, float tau, int pu8, int ablate_arg) {
   const int ablate = SAGE_TRACE ? ablate_arg : 0;
+  // psi(P) levels (Alg. 2 line 6): 127, or 255 for the unsigned P^ variant (SAGE_P_U8)
+  const float pmax = pu8 ? 255.f : 127.f;
   using L = BwdSmem<D>;
   constexpr int kStages = L::kStages;
   constexpr bool kAlias = D == 128;
@@ -267,7 +269,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------------------------------------------------- MMA issuer (whole warp, one elected lane issues)
       constexpr uint32_t kIdS = idesc_i8(128, 128, false, false);     // S^T
       constexpr uint32_t kIdDP = idesc_bf16(128, 128, false, false);  // dP^T
-      constexpr uint32_t kIdDV = idesc_i8(128, D, false, true);       // dV, dK (B MN-major)
+      constexpr uint32_t kIdDV = idesc_i8(128, D, false, true);       // dK (B MN-major)
+      const uint32_t kIdDVp = pu8 ? idesc_i8(128, D, false, true, true) : kIdDV;  // dV: A = P^^T, s8 or u8
       constexpr uint32_t kIdDQ = idesc_i8(128, D, true, true);        // dQ (A, B MN-major)
       // smem operand addresses; descriptors are formed at issue time (cheap uniform-datapath ALU)
       const uint32_t st0 = smem_u32(smem + L::kStage);
@@ -317,9 +320,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kBlk / 32; ++kk) {
             if constexpr (kTS)
-              mma_i8_ts(tDV, tPa + kk * 8, desc_mnmajor(doq_addr, D, kk * 32), kIdDV, kk > 0);
+              mma_i8_ts(tDV, tPa + kk * 8, desc_mnmajor(doq_addr, D, kk * 32), kIdDVp, kk > 0);
             else
-              mma_i8(tDV, desc_kmajor(pt_addr, 128, kk * 32), desc_mnmajor(doq_addr, D, kk * 32), kIdDV, kk > 0);
+              mma_i8(tDV, desc_kmajor(pt_addr, 128, kk * 32), desc_mnmajor(doq_addr, D, kk * 32), kIdDVp, kk > 0);
           }
           mma_commit(dv_full);
           TR(1, it);
@@ -488,7 +491,7 @@ if (cm) {
       if (threadIdx.x == 128) TR(21, it);
       // inv = 127/amax via the correctly rounded reciprocal (within 1 ulp of fl32(127/amax); P^ is
       // Tier C); the exact s_P = fl32(amax/127) is formed by the drain off this path
-      const float inv_p = amax_p > 0.f ? __fmul_rn(127.f, __frcp_rn(amax_p)) : 0.f;
+      const float inv_p = amax_p > 0.f ? __fmul_rn(pmax, __frcp_rn(amax_p)) : 0.f;
       // tile scales for the drain warpgroup (4 slots: it cannot run 4 tiles ahead of the drain)
       if (threadIdx.x == 128) scl[(it & 3) * 2] = amax_p;
 
@@ -564,7 +567,7 @@ if (cm) {
 #pragma unroll
         for (int e = 0; e < 64; e += 4) *reinterpret_cast<float4*>(dsrow + e) = make_float4(t[e], t[e + 1], t[e + 2], t[e + 3]);
         if (threadIdx.x == 128) {
-          g_dump.sp[((size_t)bh * T + i) * T + j] = __fdiv_rn(amax_p, 127.f);
+          g_dump.sp[((size_t)bh * T + i) * T + j] = __fdiv_rn(amax_p, pmax);
           g_dump.sds[((size_t)bh * T + i) * T + j] = __fdiv_rn(amax_ds, 127.f);
         }
       }
@@ -602,7 +605,7 @@ if (cm) {
         // drain; the compute warps are otherwise idle here, and two warpgroups halve it.
         mbar_wait(dv_full, ph);
         tc_fence_after();
-        const float s_p = __fdiv_rn(amax_p, 127.f);  // psi(P) scale = fl32(amax/127)
+        const float s_p = __fdiv_rn(amax_p, pmax);  // psi(P) scale = fl32(amax/127)
         const float sp_do = s_p * sc_do[i];
         const float2 f = make_float2(sp_do, sp_do);
 #pragma unroll
@@ -655,7 +658,7 @@ if (cm) {
         tc_fence_after();
         if (threadIdx.x == 384) TR(10, it);
         if (!(ablate & 1)) {
-          const float s_p = __fdiv_rn(scl[(it & 3) * 2], 127.f);  // psi(P) scale = fl32(amax/127)
+          const float s_p = __fdiv_rn(scl[(it & 3) * 2], pmax);  // psi(P) scale = fl32(amax/127)
           const float2 f = make_float2(s_p * sdo, s_p * sdo);
 #pragma unroll
           for (int c0 = 0; c0 < D; c0 += 32) {
@@ -814,7 +817,8 @@ cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
   const int T = a.N / kBlk;
   kern<<<a.BH * T, kThreads, BwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_doq, a.tm_v, a.tm_do, a.tm_dq, a.q_scale,
                                                        a.k_scale, a.do_scale, a.l2, a.delta, a.bias, a.mu_q,
-                                                       a.dq_acc, a.dk, a.dv, a.N, a.BH, a.tau, a.ablate);
+                                                       a.dq_acc, a.dk, a.dv, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
+                                                       a.ablate);
   return cudaGetLastError();
 }
 

@@ -13,10 +13,13 @@ namespace {
 // mode 3: fp32 D[128][128] = A[128][K] B[128][K]^T, bf16 K-major panels via TMA (dP^T)
 // mode 4: as mode 1 with A read from TMEM (tcgen05.st by threads, "TS" MMA): the P^ / dS^^T in TMEM paths
 // mode 5: as mode 3 with A read from TMEM (bf16, 2 per 32-bit column): the V_j-in-TMEM dP^T path
-template <int MODE, int K, int N>
+// modes 6 / 7: as 1 / 4 with an unsigned u8 A operand (the SAGE_P_U8 P^ paths)
+template <int MODE_, int K, int N>
 __global__ void __launch_bounds__(128, 1)
     debug_umma_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                       const int8_t* __restrict__ a_host_layout, void* __restrict__ out) {
+  constexpr int MODE = MODE_ == 6 ? 1 : MODE_ == 7 ? 4 : MODE_;
+  constexpr bool kU8 = MODE_ >= 6;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int kABytes = (MODE == 3 || MODE == 5) ? 128 * K * 2 : (MODE == 0 ? 128 * K : 128 * 128);
@@ -82,7 +85,8 @@ __global__ void __launch_bounds__(128, 1)
         mma_i8(tmem, desc_kmajor(a, K, kk * 32), desc_kmajor(b, K, kk * 32), idesc_i8(128, 128, false, false), kk > 0);
     } else if (MODE == 1) {
       for (int kk = 0; kk < 4; ++kk)
-        mma_i8(tmem, desc_kmajor(a, 128, kk * 32), desc_mnmajor(b, N, kk * 32), idesc_i8(128, N, false, true), kk > 0);
+        mma_i8(tmem, desc_kmajor(a, 128, kk * 32), desc_mnmajor(b, N, kk * 32), idesc_i8(128, N, false, true, kU8),
+               kk > 0);
     } else if (MODE == 2) {
       for (int kk = 0; kk < 4; ++kk)
         mma_i8(tmem, desc_mnmajor(a, 128, kk * 32), desc_mnmajor(b, N, kk * 32), idesc_i8(128, N, true, true), kk > 0);
@@ -94,7 +98,7 @@ __global__ void __launch_bounds__(128, 1)
       }
     } else if (MODE == 4) {
       for (int kk = 0; kk < 4; ++kk)
-        mma_i8_ts(tmem, tmem + 128 + kk * 8, desc_mnmajor(b, N, kk * 32), idesc_i8(128, N, false, true), kk > 0);
+        mma_i8_ts(tmem, tmem + 128 + kk * 8, desc_mnmajor(b, N, kk * 32), idesc_i8(128, N, false, true, kU8), kk > 0);
     } else {
       for (int kk = 0; kk < K / 16; ++kk) {
         const uint32_t po = (kk / 4) * 16384, ko = (kk % 4) * 32;
@@ -144,7 +148,9 @@ cudaError_t launch_debug_umma(int mode, int K, int N, const CUtensorMap* tma, co
     case 2: return N == 128 ? run<2, 128, 128>(tma, tmb, a, d, s) : run<2, 128, 64>(tma, tmb, a, d, s);
     case 3: return K == 128 ? run<3, 128, 128>(tma, tmb, a, d, s) : run<3, 64, 128>(tma, tmb, a, d, s);
     case 4: return N == 128 ? run<4, 128, 128>(tma, tmb, a, d, s) : run<4, 128, 64>(tma, tmb, a, d, s);
-    default: return K == 128 ? run<5, 128, 128>(tma, tmb, a, d, s) : run<5, 64, 128>(tma, tmb, a, d, s);
+    case 5: return K == 128 ? run<5, 128, 128>(tma, tmb, a, d, s) : run<5, 64, 128>(tma, tmb, a, d, s);
+    case 6: return N == 128 ? run<6, 128, 128>(tma, tmb, a, d, s) : run<6, 128, 64>(tma, tmb, a, d, s);
+    default: return N == 128 ? run<7, 128, 128>(tma, tmb, a, d, s) : run<7, 128, 64>(tma, tmb, a, d, s);
   }
 }
 

@@ -28,6 +28,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLog2_127 = 6.988684686772166f;
+constexpr float kLog2_255 = 7.994353436858858f;
 
 #ifndef SAGE_TRACE
 #define SAGE_TRACE 0
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ q_scale,
                     const float* __restrict__ k_scale, const float* __restrict__ v_scale,
                     const float* __restrict__ bias, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, int N,
-                    int BH, float tau, int ablate_arg) {
+                    int BH, float tau, int pu8, int ablate_arg) {
   const int ablate = SAGE_TRACE ? ablate_arg : 0;
   using L = FwdSmem<D>;
   constexpr int kStages = L::kStages;
@@ -152,7 +153,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     } else if (warp == 5) {
       // ---------------------------------------------------------- MMA issuer
       constexpr uint32_t kIdS = idesc_i8(128, 128, false, false);
-      constexpr uint32_t kIdPV = idesc_i8(128, D, false, true);
+      // P^ is s8 in 0..127, or u8 in 0..255 with SAGE_P_U8 (u8 x s8 MMA)
+      const uint32_t kIdPV = pu8 ? idesc_i8(128, D, false, true, true) : idesc_i8(128, D, false, true);
       const uint32_t q_addr = smem_u32(smem + L::kQ);
       const uint32_t k0 = smem_u32(smem + L::kK), v0 = smem_u32(smem + L::kV);
       const uint32_t p_addr = smem_u32(smem + L::kP);
@@ -210,6 +212,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     const float sq = q_scale[(size_t)bh * T + i];
     const float tau2 = tau * kLog2e;
+    // P^ levels: 127, or 255 for the unsigned variant (SAGE_P_U8)
+    const float log2_pmax = pu8 ? kLog2_255 : kLog2_127;
+    const float inv_pmax = pu8 ? 1.f / 255.f : 1.f / 127.f;
     float oacc[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) oacc[c] = 0.f;
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const float m_new = fmaxf(m, rm);
       const float alpha = ex2(m - m_new);
       const float e_rm = ex2(rm - m_new);
-      const float sub = rm - kLog2_127;  // p' = 2^{s - rm + log2 127} = 127 e^{S - rowmax}
+      const float sub = rm - log2_pmax;  // p' = 2^{s - rm + log2 127} = 127 e^{S - rowmax}
       // O update for tile j-1 first: PV_{j-1} is ready by now, and draining it frees its buffer
       // for S_{j+1}, which then runs on the tensor cores during this tile's pass 2
       if (j > 0) {
@@ -352,8 +357,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       warp_arrive(p_full);
       if (r == 0) TRF(4, j);
       // l = alpha l + e^{rowmax - m_ij} sum(e^{S - rowmax})  (line 8, reading A7)
-      l = fmaf(alpha, l, e_rm * (1.f / 127.f) * (rs2.x + rs2.y));
-      const float spv = e_rm * (1.f / 127.f) * sv;
+      l = fmaf(alpha, l, e_rm * inv_pmax * (rs2.x + rs2.y));
+      const float spv = e_rm * inv_pmax * sv;
       m = m_new;
       prev_alpha = alpha;
       prev_spv = spv;
@@ -389,7 +394,8 @@ cudaError_t launch_t(const FwdArgs& a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   const int T = a.N / kBlk;
   kern<<<a.BH * T, kThreads, FwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_v, a.q_scale, a.k_scale, a.v_scale,
-                                                       a.bias, a.o, a.lse, a.N, a.BH, a.tau, a.ablate);
+                                                       a.bias, a.o, a.lse, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
+                                                       a.ablate);
   return cudaGetLastError();
 }
 

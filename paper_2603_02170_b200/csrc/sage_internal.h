@@ -53,6 +53,7 @@ struct FwdArgs {
   int BH, N, d;
   float tau;
   bool causal, qsmooth;
+  bool pu8;    // SAGE_P_U8: P^ in 0..255 (u8 x s8 PV)
   int ablate;  // profiling only (SAGE_ABLATE bit 8: timeline)
 };
 cudaError_t launch_fwd(const FwdArgs& a, cudaStream_t s);
@@ -71,6 +72,7 @@ struct BwdArgs {
   int BH, N, d;
   float tau;
   bool causal, qsmooth;
+  bool pu8;    // SAGE_P_U8: psi(P) in 0..255 (u8 x s8 dV)
   int ablate;  // profiling only (SAGE_ABLATE): 1 drain math off, 2 compute math off, 4 dQ reduction off
 };
 cudaError_t launch_bwd(const BwdArgs& a, cudaStream_t s);

@@ -264,8 +264,9 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t tile_addr, uint32_t ro
 // Instruction descriptor (PTX ISA tcgen05 "Instruction descriptor" for .kind::i8 / .kind::f16):
 //   [4,6) D format (1 F32, 2 S32)  [7,10) A fmt  [10,13) B fmt  [15] A MN-major  [16] B MN-major
 //   [17,23) N>>3  [24,29) M>>4
-__host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N, bool a_mn, bool b_mn) {
-  return (2u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+// kind::i8 A/B formats: 0 = u8, 1 = s8 (bits 7-9 / 10-12); a_u8 for the unsigned P^ (SAGE_P_U8)
+__host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N, bool a_mn, bool b_mn, bool a_u8 = false) {
+  return (2u << 4) | ((a_u8 ? 0u : 1u) << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
          ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, bool a_mn, bool b_mn) {

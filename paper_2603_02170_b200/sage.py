@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # SAGE_LIB selects the profiling build (libsage_trace.so) for scripts/trace_bwd.py only.
 LIB_PATH = os.environ.get("SAGE_LIB") or os.path.join(_HERE, "libsage.so")
 
-SAGE_CAUSAL, SAGE_K_SMOOTH, SAGE_Q_SMOOTH = 1, 2, 4
+SAGE_CAUSAL, SAGE_K_SMOOTH, SAGE_Q_SMOOTH, SAGE_P_U8 = 1, 2, 4, 8
 _STATUS = {0: "SAGE_OK", 1: "SAGE_ERR_INVALID_VALUE", 2: "SAGE_ERR_UNSUPPORTED", 3: "SAGE_ERR_MISALIGNED",
            4: "SAGE_ERR_WORKSPACE", 5: "SAGE_ERR_CUDA", 6: "SAGE_ERR_ARCH"}
 
@@ -87,8 +87,10 @@ def _check(status, what):
         raise SageError(f"{what}: {_STATUS.get(status, status)}{extra}")
 
 
-def make_params(batch, heads, seqlen, head_dim, causal=False, k_smooth=True, q_smooth=False, softmax_scale=None):
-    flags = (SAGE_CAUSAL if causal else 0) | (SAGE_K_SMOOTH if k_smooth else 0) | (SAGE_Q_SMOOTH if q_smooth else 0)
+def make_params(batch, heads, seqlen, head_dim, causal=False, k_smooth=True, q_smooth=False, softmax_scale=None,
+                p_u8=False):
+    flags = (SAGE_CAUSAL if causal else 0) | (SAGE_K_SMOOTH if k_smooth else 0) | (SAGE_Q_SMOOTH if q_smooth else 0) | \
+        (SAGE_P_U8 if p_u8 else 0)
     return SageParams(batch, heads, seqlen, head_dim, flags, 0.0 if softmax_scale is None else softmax_scale)
 
 
@@ -171,11 +173,12 @@ def ws_view(params, backward, ws):
 
 
 def forward(q, k, v, causal=False, k_smooth=True, q_smooth=False, softmax_scale=None, out=None, lse=None,
-            ctx=None, workspace=None, stream=None):
-    """sage_fwd (Alg. 1): returns (o, lse, SageCtx).  q, k, v: CUDA bf16 [B, H, N, d]."""
+            ctx=None, workspace=None, stream=None, p_u8=False):
+    """sage_fwd (Alg. 1): returns (o, lse, SageCtx).  q, k, v: CUDA bf16 [B, H, N, d].
+    p_u8: the unsigned-P^ variant (SAGE_P_U8); the backward inherits it through the ctx."""
     _check_io(q, k, v)
     B, H, N, d = q.shape
-    p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale)
+    p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8)
     nctx = lib().sage_ctx_bytes(ctypes.byref(p))
     if nctx == 0:
         raise SageError(f"unsupported shape/flags {tuple(q.shape)} (N % 128 == 0, d in {{64, 128}})")

@@ -64,7 +64,7 @@ def test_error_paths_do_not_launch(L):
     nwb = L.sage_workspace_bytes(ctypes.byref(p), 1)
     assert L.sage_bwd(ctypes.byref(p), A, A, A, A, A, S(nctx), A, A, A, A, S(nwb - 1), z) == 4
     assert L.sage_bwd(ctypes.byref(p), A, A, A, A, A, S(nctx), A, A, mis, A, S(nwb), z) == 3
-    assert L.sage_debug_umma(7, 64, 128, A, A, A, z) == 1
+    assert L.sage_debug_umma(8, 64, 128, A, A, A, z) == 1
     assert L.sage_debug_umma(1, 128, 96, A, A, A, z) == 1
     # the tile dump exists only in the test build (libsage_trace.so)
     assert L.sage_debug_dump(A, A, A, A, A, 1) == 2

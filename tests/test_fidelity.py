@@ -43,17 +43,17 @@ def dump_lib():
     sage.use_library(old)
 
 
-def _gpu_with_dump(q, k, v, do, causal, k_smooth, q_smooth):
+def _gpu_with_dump(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False):
     B, H, N, d = q.shape
     dev = torch.device("cuda")
     qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
     bufs = sage.debug_dump(B * H, N, dev)
-    o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth)
+    o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8)
     dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
     torch.cuda.synchronize()
     sage.debug_dump(0, 0, None)
     # back to the oracle's [head][N q][N kv] layout
-    tiles = dict(p8=bufs["p_hat_t"].transpose(1, 2).cpu().numpy(), sp=bufs["s_p"].cpu().numpy(),
+    tiles = dict(p8=bufs["p_hat_t"].transpose(1, 2).cpu().numpy().view(np.uint8), sp=bufs["s_p"].cpu().numpy(),
                  ds8=bufs["ds_hat_t"].transpose(1, 2).cpu().numpy(), sds=bufs["s_ds"].cpu().numpy(),
                  ds=bufs["ds_t"].transpose(1, 2).cpu().numpy().astype(np.float64))
     wsb = sage._ws.get(ctx.params, True, dev)
@@ -64,10 +64,10 @@ def _gpu_with_dump(q, k, v, do, causal, k_smooth, q_smooth):
     return dict(o=flat(o), dq=flat(dq), dk=flat(dk), dv=flat(dv), delta=delta, **tiles)
 
 
-def _oracle_run(q, k, v, do, causal, k_smooth, q_smooth):
+def _oracle_run(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False):
     B, H, N, d = q.shape
     qn, kn, vn, don = (f64(t).reshape(B * H, N, d) for t in (q, k, v, do))
-    kw = dict(causal=causal, k_smooth=k_smooth, q_smooth=q_smooth)
+    kw = dict(causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8)
     oracle.set_threads(min(8, os.cpu_count() or 1))
     f = oracle.fwd(qn, kn, vn, **kw)
     b = oracle.bwd(qn, kn, vn, round_bf16(f["o"]), don, f["lse"], tiles=True, **kw)
@@ -101,23 +101,26 @@ def _tier_c(g, b, N, causal):
 
 
 TIER_C = [
-    # (B, H, N, d, causal, k_smooth, q_smooth, recipe)
-    (1, 2, 384, 64, True, True, False, "qknorm"),
-    (1, 2, 256, 64, False, True, False, "gauss"),
-    (1, 2, 384, 128, True, True, True, "outlier_kq"),
-    (1, 2, 256, 128, False, True, False, "qknorm"),
+    # (B, H, N, d, causal, k_smooth, q_smooth, recipe, p_u8)
+    (1, 2, 384, 64, True, True, False, "qknorm", False),
+    (1, 2, 256, 64, False, True, False, "gauss", False),
+    (1, 2, 384, 128, True, True, True, "outlier_kq", False),
+    (1, 2, 256, 128, False, True, False, "qknorm", False),
+    (1, 2, 384, 64, True, True, False, "qknorm", True),
+    (1, 2, 256, 128, False, True, True, "outlier_kq", True),
 ]
 
 
-@pytest.mark.parametrize("B,H,N,d,causal,ks,qs,recipe", TIER_C)
-def test_tier_c_backward_tiles(dump_lib, B, H, N, d, causal, ks, qs, recipe):
+@pytest.mark.parametrize("B,H,N,d,causal,ks,qs,recipe,u8", TIER_C)
+def test_tier_c_backward_tiles(dump_lib, B, H, N, d, causal, ks, qs, recipe, u8):
     """Tier C (SURVEY.md 8(c) parity contract): >= 99.9% of P^ and dS^ elements identical to the
     oracle's, all within 1 LSB; s_P, s_dS within 64 fp32 ulp; pre-psi dS within 1e-3 rel-L2."""
     q, k, v, do = make_inputs(B, H, N, d, recipe, seed=300 + N + d)
-    g = _gpu_with_dump(q, k, v, do, causal, ks, qs)
-    f, b = _oracle_run(q, k, v, do, causal, ks, qs)
+    g = _gpu_with_dump(q, k, v, do, causal, ks, qs, u8)
+    f, b = _oracle_run(q, k, v, do, causal, ks, qs, u8)
     res = _tier_c(g, b, N, causal)
-    _write_report(f"tier_c/B{B}H{H}N{N}d{d}{'c' if causal else 'n'}{'ks' if ks else ''}{'qs' if qs else ''}_{recipe}", res)
+    tag = f"B{B}H{H}N{N}d{d}{'c' if causal else 'n'}{'ks' if ks else ''}{'qs' if qs else ''}{'u8' if u8 else ''}"
+    _write_report(f"tier_c/{tag}_{recipe}", res)
     for name in ("p8", "ds8"):
         assert res[name]["identical"] >= 0.999 and res[name]["max_abs_diff"] <= 1, (name, res)
     assert res["sp"]["max_ulp"] <= 64 and res["sds"]["max_ulp"] <= 64, res
@@ -209,3 +212,21 @@ def test_fidelity_qknorm_ablation(dump_lib):
     _write_report("qknorm_ablation", dict(setting=f"B={B} H={H} N={N} d={d} causal K-smooth", rows=rows))
     for name in ("dq", "dk", "dS"):
         assert rows["qknorm"][name]["gpu_rel_l2"] < rows["noqknorm"][name]["gpu_rel_l2"], (name, rows)
+
+
+def test_fidelity_p_u8(dump_lib):
+    """SAGE_P_U8 on the GPU: unsigned P^ halves P^'s rounding step, so O and dV get closer to FPA
+    (the quantised oracle predicts it: tests/test_oracle.py::test_p_u8_variant) at no kernel cost."""
+    B, H, N, d = 1, 2, 1024, 128
+    rows = {}
+    q, k, v, do = make_inputs(B, H, N, d, "qknorm", seed=5001)
+    ref = _fpa(q, k, v, do, True)
+    for u8 in (False, True):
+        g = _gpu_with_dump(q, k, v, do, True, True, False, u8)
+        f, b = _oracle_run(q, k, v, do, True, True, False, u8)
+        row = _fidelity_row(g, b, f, ref, N, True)
+        _assert_gpu_tracks_oracle(row, ("u8", u8))
+        rows["u8" if u8 else "s8"] = row
+    _write_report("p_u8_vs_s8", dict(setting=f"B={B} H={H} N={N} d={d} causal K-smooth qknorm", rows=rows))
+    assert rows["u8"]["o"]["gpu_rel_l2"] < rows["s8"]["o"]["gpu_rel_l2"]
+    assert rows["u8"]["dv"]["gpu_rel_l2"] < 0.8 * rows["s8"]["dv"]["gpu_rel_l2"]

@@ -27,21 +27,21 @@ def _gpu():
     oracle.build()
 
 
-def _run(q, k, v, do, causal, k_smooth, q_smooth):
+def _run(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False):
     dev = "cuda"
     qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
-    o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth)
+    o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8)
     dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
     torch.cuda.synchronize()
     return dict(o=o, lse=lse, dq=dq, dk=dk, dv=dv, ctx=ctx)
 
 
-def _oracle(q, k, v, do, heads, causal, k_smooth, q_smooth):
+def _oracle(q, k, v, do, heads, causal, k_smooth, q_smooth, p_u8=False):
     """Oracle on the selected flattened heads; O is stored as bf16 before the backward (A15)."""
     B, H, N, d = q.shape
     sel = lambda t: f64(t).reshape(B * H, N, d)[heads]
     qn, kn, vn, don = map(sel, (q, k, v, do))
-    kw = dict(causal=causal, k_smooth=k_smooth, q_smooth=q_smooth)
+    kw = dict(causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8)
     f = oracle.fwd(qn, kn, vn, **kw)
     o_st = round_bf16(f["o"])
     b = oracle.bwd(qn, kn, vn, o_st, don, f["lse"], **kw)
@@ -77,13 +77,17 @@ def test_umma_s_tile_kmajor(K):
     np.testing.assert_array_equal(d, a.numpy().astype(np.int64) @ b.numpy().astype(np.int64).T)
 
 
-@pytest.mark.parametrize("mode", [1, 2, 4])
+@pytest.mark.parametrize("mode", [1, 2, 4, 6, 7])
 @pytest.mark.parametrize("N", [64, 128])
 def test_umma_mn_major(mode, N):
-    """modes 1 / 4: A K-major from smem / from TMEM (TS); mode 2: A MN-major (dQ)."""
+    """modes 1 / 4: A K-major from smem / from TMEM (TS); mode 2: A MN-major (dQ);
+    modes 6 / 7: as 1 / 4 with an unsigned u8 A (SAGE_P_U8: P^ in [0, 255])."""
     g = torch.Generator().manual_seed(10 * mode + N)
-    lo = 0 if mode == 1 else -127          # mode 1 is the P^ path (values in [0, 127])
-    a = torch.randint(lo, 128, (128, 128), generator=g, dtype=torch.int8)
+    if mode >= 6:
+        a = torch.randint(0, 256, (128, 128), generator=g, dtype=torch.uint8)
+    else:
+        lo = 0 if mode == 1 else -127      # mode 1 is the P^ path (values in [0, 127])
+        a = torch.randint(lo, 128, (128, 128), generator=g, dtype=torch.int8)
     b = torch.randint(-127, 128, (128, N), generator=g, dtype=torch.int8)
     d = sage.debug_umma(mode, a.cuda(), b.cuda()).cpu().numpy()
     A = a.numpy().astype(np.int64)
@@ -167,6 +171,24 @@ def test_fwd_bwd_parity_small(B, H, N, d, causal, ks, qs, recipe):
     heads = list(range(B * H))
     f, b = _oracle(q, k, v, do, heads, causal, ks, qs)
     _assert_ok(_compare(gpu, f, b, heads, B, H, N, d), (B, H, N, d, causal, ks, qs, recipe))
+
+
+P_U8_CASES = [
+    (1, 2, 384, 64, True, True, False, "qknorm"),
+    (1, 2, 256, 64, False, True, False, "gauss"),
+    (1, 2, 384, 128, True, True, True, "outlier_kq"),
+    (1, 2, 256, 128, False, True, False, "qknorm"),
+]
+
+
+@pytest.mark.parametrize("B,H,N,d,causal,ks,qs,recipe", P_U8_CASES)
+def test_fwd_bwd_parity_p_u8(B, H, N, d, causal, ks, qs, recipe):
+    """SAGE_P_U8 (P^ in 0..255, u8 x s8 PV / dV MMAs) against the oracle's ORC_P_U8 mode."""
+    q, k, v, do = make_inputs(B, H, N, d, recipe, seed=200 + N + d)
+    gpu = _run(q, k, v, do, causal, ks, qs, p_u8=True)
+    heads = list(range(B * H))
+    f, b = _oracle(q, k, v, do, heads, causal, ks, qs, p_u8=True)
+    _assert_ok(_compare(gpu, f, b, heads, B, H, N, d), (B, H, N, d, causal, ks, qs, recipe, "u8"))
 
 
 def test_zero_do_gives_zero_grads():
