@@ -9,9 +9,11 @@ Parity status per function:
   * ``fwd`` / ``bwd`` with ``quant=False``       pinned (== FPA <= 1e-9; FPA pinned by finite differences)
   * ``fwd`` / ``bwd`` with ``quant=True``        pinned (Table 1 trend/values, smoothing identities, grid fixed points)
   * ``fpa``                                     pinned (finite differences, closed forms, App. B bound)
+  * ``qknorm.forward`` / ``qknorm.backward``    pinned (closed forms, unit RMS, finite differences)
 """
+from . import qknorm
 from .oracle import (CAUSAL, K_SMOOTH, Q_SMOOTH, QUANT_OFF, build, fpa, fwd, bwd,
                      psi_block, psi_token_row, set_threads, max_threads)
 
-__all__ = ["CAUSAL", "K_SMOOTH", "Q_SMOOTH", "QUANT_OFF", "build", "fpa", "fwd", "bwd",
+__all__ = ["qknorm", "CAUSAL", "K_SMOOTH", "Q_SMOOTH", "QUANT_OFF", "build", "fpa", "fwd", "bwd",
            "psi_block", "psi_token_row", "set_threads", "max_threads"]

@@ -348,3 +348,49 @@ def test_p_u8_variant(orc):
     assert errs[True]["o"] < 0.95 * errs[False]["o"], errs
     assert errs[True]["dv"] < 0.7 * errs[False]["dv"], errs
     assert abs(errs[True]["dq"] - errs[False]["dq"]) < 0.25 * errs[False]["dq"], errs
+
+
+# --------------------------------------------------------------------------- QK-norm
+def test_qknorm_forward_closed_forms(orc):
+    """RMSNorm (eps 1e-6 P:405; readings A24, A25): a constant row a gives
+    rstd = 1/sqrt(a^2 + eps); the unrounded output has mean square m/(m + eps) per row; the
+    output is bf16-valued and within half a bf16 ulp of x rstd gamma."""
+    qn = orc.qknorm
+    a = np.full((1, 64), 3.0)
+    y, r = qn.forward(a, np.ones(64), eps=1e-6)
+    assert float(r[0]) == np.float32(1.0 / math.sqrt(9.0 + 1e-6))
+    rng = np.random.default_rng(40)
+    x = torch.from_numpy(rng.standard_normal((4, 256, 128)) * 5).to(torch.bfloat16).double().numpy()
+    g = rng.uniform(0.5, 2.0, 128).astype(np.float32)
+    y0, r = qn.forward(x, np.ones(128), round_output=False)
+    m = (x * x).mean(-1)
+    np.testing.assert_allclose((y0 * y0).mean(-1), m / (m + 1e-6), rtol=1e-6)
+    y, _ = qn.forward(x, g)
+    exact = x * r[..., None].astype(np.float64) * g
+    assert np.all(np.abs(y - exact) <= np.abs(exact) * 2.0 ** -8 * 1.0001)
+    assert np.array_equal(y, torch.from_numpy(y).to(torch.bfloat16).double().numpy())
+
+
+def test_qknorm_backward_finite_differences(orc):
+    """dx and dgamma of y = x rstd(x) gamma (reading A26) against central finite differences of
+    L = sum(w o y) in double (rstd exact, unrounded output)."""
+    qn = orc.qknorm
+    rng = np.random.default_rng(41)
+    x = rng.standard_normal((3, 16))
+    g = rng.uniform(0.5, 2.0, 16)
+    w = rng.standard_normal((3, 16))
+    eps = 1e-3
+
+    def loss(xx, gg):
+        r = 1.0 / np.sqrt((xx * xx).mean(-1, keepdims=True) + eps)
+        return float((w * xx * r * gg).sum())
+    r = 1.0 / np.sqrt((x * x).mean(-1) + eps)
+    dx, dg = qn.backward(x, g, r, w)
+    h = 1e-6
+    fdx = np.zeros_like(x)
+    for idx in np.ndindex(*x.shape):
+        e = np.zeros_like(x)
+        e[idx] = h
+        fdx[idx] = (loss(x + e, g) - loss(x - e, g)) / (2 * h)
+    fdg = np.array([(loss(x, g + h * np.eye(16)[c]) - loss(x, g - h * np.eye(16)[c])) / (2 * h) for c in range(16)])
+    assert rel_l2(fdx, dx) < 1e-7 and rel_l2(fdg, dg) < 1e-7
