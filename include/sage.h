@@ -61,10 +61,12 @@ enum {
   SAGE_CAUSAL = 1u << 0,   /* mask key n > query r (reading A14) */
   SAGE_K_SMOOTH = 1u << 1, /* K-smoothing, P:136-147 (the paper's default) */
   SAGE_Q_SMOOTH = 1u << 2, /* block-wise Q-smoothing + bias */
-  SAGE_P_U8 = 1u << 3      /* variant: P^ unsigned in 0..255 with scale max/255,
+  SAGE_P_U8 = 1u << 3,     /* variant: P^ unsigned in 0..255 with scale max/255,
                               for the per-token P^ of Alg. 1 line 9 and psi(P) of Alg. 2 line 6 (the
                               paper's reading: 0..127, A2); the PV / dV MMAs run u8 x s8.  Halves P^'s
                               rounding step at no cost: lower O and dV error vs full precision. */
+  SAGE_QK_NORM = 1u << 4   /* QK-norm in front of the path: use
+                              sage_fwd_qknorm / sage_bwd_qknorm (sage_fwd / sage_bwd reject it) */
 };
 
 typedef struct {
@@ -93,6 +95,27 @@ SAGE_API sage_status sage_bwd(const sage_params* p, const void* v, const void* o
                      const void* ctx, size_t ctx_bytes, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
                      void* stream);
 
+/* QK-norm variant ("Stabilizing Outliers with QK-Norm"; eps P:405).  p->flags must hold
+ * SAGE_QK_NORM.  Instead of Q and K the caller passes the pre-norm X_q, X_k (bf16 [B,H,N,d]) and the
+ * RMSNorm scales gamma_q, gamma_k (fp32 [d], shared by all heads); the path then runs on
+ *     Q = bf16(fl32(fl32(X_q * rstd) * gamma_q)),  rstd = fl32(1 / sqrt(mean_c X^2 + eps))
+ * (and the same for K), i.e. exactly the BF16 values an unfused RMSNorm module would produce
+ * (readings A24-A25).  The normalisation is fused into the smoothing / quantisation
+ * passes (Q and K are never written to memory); rstd of every row is kept in ctx for the backward.
+ * eps > 0 (the paper uses 1e-6). */
+SAGE_API sage_status sage_fwd_qknorm(const sage_params* p, const void* xq, const void* xk, const void* v,
+                                     const float* gamma_q, const float* gamma_k, float eps, void* o, float* lse,
+                                     void* ctx, size_t ctx_bytes, void* ws, size_t ws_bytes, void* stream);
+/* Backward of sage_fwd_qknorm: Alg. 2 as sage_bwd, then the RMSNorm backward (reading A26) fused with
+ * the dQ finalisation: writes dX_q, dX_k (bf16 [B,H,N,d]) into dxq, dxk, dV into dv, and
+ * dgamma_q, dgamma_k (fp32 [d], summed over all B*H*N rows in a fixed order).  xq, xk, gamma_q,
+ * gamma_k must be the forward's. */
+SAGE_API sage_status sage_bwd_qknorm(const sage_params* p, const void* xq, const void* xk, const float* gamma_q,
+                                     const float* gamma_k, const void* v, const void* o, const float* lse,
+                                     const void* dO, const void* ctx, size_t ctx_bytes, void* dxq, void* dxk,
+                                     void* dv, float* dgamma_q, float* dgamma_k, void* ws, size_t ws_bytes,
+                                     void* stream);
+
 /* Device pointers into a context / workspace buffer (for tests and tracing; no launch). */
 typedef struct {
   int8_t *q_i8, *k_i8;        /* [B,H,N,d] psi(Q_sm or Q), psi(K_sm) */
@@ -100,6 +123,7 @@ typedef struct {
   float* mu_k;                /* [B,H,d] */
   float* mu_q;                /* [B,H,N/128,d] or NULL */
   float* bias;                /* [B,H,N/128,N] or NULL: bias_i[n] = mu_Qi . K_sm[n] */
+  float *rstd_q, *rstd_k;     /* [B,H,N] QK-norm rstd of X_q / X_k rows, or NULL */
 } sage_ctx_view;
 SAGE_API sage_status sage_ctx_get_view(const sage_params* p, void* ctx, sage_ctx_view* out);
 

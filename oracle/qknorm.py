@@ -4,7 +4,7 @@ PAPER.md P:212-234 (Sec. 4.1 "Stabilizing Outliers with QK-Norm"): RMS normalisa
 token of Q and K with a learned scale vector gamma, eps = 1e-6 ("a norm
 epsilon of 1e-6"), BF16 mixed precision.  Readings (A24-A26):
 
-  A24  rstd[r] = fl32(1 / sqrt(sum_c x[r,c]^2 / d + eps)): the sum of squares of the bf16 inputs
+  A24  rstd[r] = fl32(1 / sqrt(sum_c x[r,c]^2 / d + eps)), eps the fp32 value: the sum of squares of the bf16 inputs
        in double (exact, hence order-free, unless a row's squares span > 30 binades), the
        division and square root in double, one rounding to fp32.
   A25  y[r,c] = bf16(fl32(fl32(x[r,c] * rstd[r]) * gamma[c])): the module output is BF16, as in
@@ -31,6 +31,7 @@ def rstd(x, eps=1e-6):
     """A24: per-row reciprocal RMS of x [..., d] (bf16-valued), fp32."""
     x = np.asarray(x, dtype=np.float64)
     ss = (x * x).sum(-1)
+    eps = float(np.float32(eps))   # the ABI carries eps as an fp32 value
     return (1.0 / np.sqrt(ss / x.shape[-1] + eps)).astype(np.float32)
 
 

@@ -66,7 +66,7 @@ size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Dims {
   size_t BH, N, d, T;
-  bool causal, ks, qs, pu8;
+  bool causal, ks, qs, pu8, qkn;
   float tau;
 };
 
@@ -75,7 +75,7 @@ bool dims_of(const sage_params* p, Dims* o) {
   if (p->batch <= 0 || p->heads <= 0 || p->seqlen <= 0) return false;
   if (p->head_dim != 64 && p->head_dim != 128) return false;
   if (p->seqlen % kBlk || p->seqlen > kMaxSeqLen) return false;
-  if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH | SAGE_P_U8)) return false;
+  if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH | SAGE_P_U8 | SAGE_QK_NORM)) return false;
   if (!(p->softmax_scale >= 0.f) || std::isinf(p->softmax_scale)) return false;
   const size_t BH = (size_t)p->batch * p->heads;
   if (BH * p->seqlen > (size_t)INT32_MAX / 2) return false;  // TMA row coordinates are int32
@@ -87,13 +87,14 @@ bool dims_of(const sage_params* p, Dims* o) {
   o->ks = p->flags & SAGE_K_SMOOTH;
   o->qs = p->flags & SAGE_Q_SMOOTH;
   o->pu8 = p->flags & SAGE_P_U8;
+  o->qkn = p->flags & SAGE_QK_NORM;
   o->tau = p->softmax_scale > 0.f ? p->softmax_scale : 1.f / std::sqrt((float)p->head_dim);
   return true;
 }
 
 // ---- carving.  ctx: q_i8, k_i8, q_scale, k_scale, mu_k, [mu_q, bias]
 struct CtxLayout {
-  size_t q8, k8, sq, sk, muk, muq, bias, total;
+  size_t q8, k8, sq, sk, muk, muq, bias, rq, rk, total;
 };
 CtxLayout ctx_layout(const Dims& D) {
   CtxLayout L{};
@@ -105,6 +106,8 @@ CtxLayout ctx_layout(const Dims& D) {
   L.muk = off; off += up(D.BH * D.d * 4);
   L.muq = off; off += D.qs ? up(D.BH * D.T * D.d * 4) : 0;
   L.bias = off; off += D.qs ? up(D.BH * D.T * D.N * 4) : 0;
+  L.rq = off; off += D.qkn ? up(D.BH * D.N * 4) : 0;  // QK-norm rstd of X_q, X_k rows
+  L.rk = off; off += D.qkn ? up(D.BH * D.N * 4) : 0;
   L.total = off;
   return L;
 }
@@ -124,7 +127,7 @@ FwdWs fwd_ws(const Dims& D) {
 }
 // bwd ws: do_i8, do_scale, delta, l2, dq_acc
 struct BwdWs {
-  size_t do8, sdo, delta, l2, dq, total;
+  size_t do8, sdo, delta, l2, dq, gq, gk, total;
 };
 BwdWs bwd_ws(const Dims& D) {
   BwdWs W{};
@@ -134,6 +137,10 @@ BwdWs bwd_ws(const Dims& D) {
   W.delta = off; off += up(D.BH * D.N * 4);
   W.l2 = off; off += up(D.BH * D.N * 4);
   W.dq = off; off += up(nd * 4);
+  // QK-norm dgamma partials: per 128-row block (fp32), then per 64 blocks (fp64), see launch_norm_bwd
+  const size_t gbytes = D.BH * D.T * D.d * 4 + 8 + (D.BH * D.T + 63) / 64 * D.d * 8;
+  W.gq = off; off += D.qkn ? up(gbytes) : 0;
+  W.gk = off; off += D.qkn ? up(gbytes) : 0;
   W.total = off;
   return W;
 }
@@ -291,6 +298,8 @@ sage_status sage_ctx_get_view(const sage_params* p, void* ctx, sage_ctx_view* ou
   out->mu_k = at<float>(ctx, L.muk);
   out->mu_q = D.qs ? at<float>(ctx, L.muq) : nullptr;
   out->bias = D.qs ? at<float>(ctx, L.bias) : nullptr;
+  out->rstd_q = D.qkn ? at<float>(ctx, L.rq) : nullptr;
+  out->rstd_k = D.qkn ? at<float>(ctx, L.rk) : nullptr;
   return SAGE_OK;
 }
 
@@ -312,10 +321,14 @@ sage_status sage_ws_get_view(const sage_params* p, int backward, void* ws, sage_
   return SAGE_OK;
 }
 
-sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const void* v, void* o, float* lse,
-                     void* ctx, size_t ctx_bytes, void* ws, size_t ws_bytes, void* stream) {
-  Dims D;
-  if (!dims_of(p, &D) || !q || !k || !v || !o || !lse || !ctx || !ws) return SAGE_ERR_INVALID_VALUE;
+}  // extern "C"
+
+namespace {
+// Forward launch sequence; gq/gk non-null <=> QK-norm (q, k are then X_q, X_k).
+sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v, const float* gq, const float* gk,
+                     float eps, void* o, float* lse, void* ctx, size_t ctx_bytes, void* ws, size_t ws_bytes,
+                     void* stream) {
+  if (!q || !k || !v || !o || !lse || !ctx || !ws) return SAGE_ERR_INVALID_VALUE;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(lse) || !aligned16(ctx) ||
       !aligned16(ws))
     return SAGE_ERR_MISALIGNED;
@@ -336,6 +349,9 @@ sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const v
   float* bias = D.qs ? at<float>(ctx, C.bias) : nullptr;
   double* partk = at<double>(ws, W.partk);
   double* partq = D.qs ? at<double>(ws, W.partq) : nullptr;
+  float* rq = D.qkn ? at<float>(ctx, C.rq) : nullptr;
+  float* rk = D.qkn ? at<float>(ctx, C.rk) : nullptr;
+  const NormIn nq{rq, gq, eps}, nk{rk, gk, eps};
 
   FwdArgs a{};
   const uint64_t rows = D.BH * D.N;
@@ -344,24 +360,25 @@ sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const v
     return cuda_fail(cudaErrorInvalidValue);
 
   cudaError_t e = cudaSuccess;
+  // QK-norm: the row statistics and normalised values are formed on the fly in K0/K1
   // K0: smoothing statistics
   if (D.ks) {
-    if ((e = launch_colsum(kb, partk, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = launch_colsum(kb, partk, BH, N, d, s, nk)) != cudaSuccess) return cuda_fail(e);
     if ((e = launch_colmean(partk, muk, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
   }
   if (D.qs) {
-    if ((e = launch_colsum(qb, partq, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = launch_colsum(qb, partq, BH, N, d, s, nq)) != cudaSuccess) return cuda_fail(e);
     if ((e = launch_blockmean(partq, muq, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
   }
   // K1: per-block psi (Alg. 1 line 3)
   QuantJobs qj{};
-  qj.j[0] = QuantJob{qb, muq, D.qs ? 2 : 0, q8, sq};
-  qj.j[1] = QuantJob{kb, muk, D.ks ? 1 : 0, k8, sk};
-  qj.j[2] = QuantJob{vb, nullptr, 0, v8, sv};
+  qj.j[0] = QuantJob{qb, muq, D.qs ? 2 : 0, q8, sq, rq, gq, eps};
+  qj.j[1] = QuantJob{kb, muk, D.ks ? 1 : 0, k8, sk, rk, gk, eps};
+  qj.j[2] = QuantJob{vb, nullptr, 0, v8, sv, nullptr, nullptr, 0.f};
   if ((e = launch_quantize(qj, 3, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
   // mu_K is all-zero when K-smoothing is off (ctx is caller memory: make it so)
   if (!D.ks && (e = launch_fill(muk, D.BH * D.d, 0.f, s)) != cudaSuccess) return cuda_fail(e);
-  if (D.qs && (e = launch_qsmooth_bias(kb, muk, muq, bias, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+  if (D.qs && (e = launch_qsmooth_bias(kb, muk, muq, bias, BH, N, d, s, nk)) != cudaSuccess) return cuda_fail(e);
   // K2: fused INT8 forward (Alg. 1 lines 4-14)
   a.q_scale = sq;
   a.k_scale = sk;
@@ -382,11 +399,12 @@ sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const v
   return SAGE_OK;
 }
 
-sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const float* lse, const void* dO,
-                     const void* ctx, size_t ctx_bytes, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
-                     void* stream) {
-  Dims D;
-  if (!dims_of(p, &D) || !v || !o || !lse || !dO || !ctx || !dq || !dk || !dv || !ws) return SAGE_ERR_INVALID_VALUE;
+// Backward launch sequence; with QK-norm (D.qkn) dq/dk receive dX_q/dX_k and xq, xk, gq, gk, dgq, dgk
+// are the RMSNorm inputs and dgamma outputs.
+sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* lse, const void* dO, const void* ctx,
+                     size_t ctx_bytes, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, void* stream,
+                     const void* xq, const void* xk, const float* gq, const float* gk, float* dgq, float* dgk) {
+  if (!v || !o || !lse || !dO || !ctx || !dq || !dk || !dv || !ws) return SAGE_ERR_INVALID_VALUE;
   if (!aligned16(v) || !aligned16(o) || !aligned16(lse) || !aligned16(dO) || !aligned16(ctx) || !aligned16(dq) ||
       !aligned16(dk) || !aligned16(dv) || !aligned16(ws))
     return SAGE_ERR_MISALIGNED;
@@ -434,11 +452,71 @@ sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const f
   a.pu8 = D.pu8;
   a.ablate = ablate_flags() | (g_dump_heads > 0 ? 16 : 0);
   if ((e = timed(1, s, [&] { return launch_bwd(a, s); })) != cudaSuccess) return cuda_fail(e);
-  if (g_prof.on) g_prof.launches += 3;
+  if (g_prof.on) g_prof.launches += 2;  // K3, K4
+  if (D.qkn) {
+    // RMSNorm backward (reading A26), fused with the dQ finalisation; dK (w.r.t. the normalised K,
+    // bf16 from K4) is turned into dX_k in place
+    const auto* rq = at<const float>(cx, C.rq);
+    const auto* rk = at<const float>(cx, C.rk);
+    auto* dqb = static_cast<__nv_bfloat16*>(dq);
+    auto* dkb = static_cast<__nv_bfloat16*>(dk);
+    if ((e = launch_norm_bwd(dqacc, nullptr, static_cast<const __nv_bfloat16*>(xq), rq, gq, dqb, at<float>(ws, W.gq),
+                             dgq, D.BH * D.N, d, s)) != cudaSuccess)
+      return cuda_fail(e);
+    if ((e = launch_norm_bwd(nullptr, dkb, static_cast<const __nv_bfloat16*>(xk), rk, gk, dkb, at<float>(ws, W.gk),
+                             dgk, D.BH * D.N, d, s)) != cudaSuccess)
+      return cuda_fail(e);
+    if (g_prof.on) g_prof.launches += 6;  // 2 x (norm_bwd, dgamma stage 1, stage 2)
+    return SAGE_OK;
+  }
   // K5
   if ((e = launch_dq_finalize(dqacc, static_cast<__nv_bfloat16*>(dq), D.BH * D.N * D.d, s)) != cudaSuccess)
     return cuda_fail(e);
+  if (g_prof.on) g_prof.launches += 1;  // K5
   return SAGE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const void* v, void* o, float* lse,
+                     void* ctx, size_t ctx_bytes, void* ws, size_t ws_bytes, void* stream) {
+  Dims D;
+  if (!dims_of(p, &D) || D.qkn) return SAGE_ERR_INVALID_VALUE;  // QK-norm: sage_fwd_qknorm
+  return fwd_impl(D, q, k, v, nullptr, nullptr, 0.f, o, lse, ctx, ctx_bytes, ws, ws_bytes, stream);
+}
+
+sage_status sage_fwd_qknorm(const sage_params* p, const void* xq, const void* xk, const void* v, const float* gamma_q,
+                            const float* gamma_k, float eps, void* o, float* lse, void* ctx, size_t ctx_bytes,
+                            void* ws, size_t ws_bytes, void* stream) {
+  Dims D;
+  if (!dims_of(p, &D) || !D.qkn || !gamma_q || !gamma_k || !(eps > 0.f) || std::isinf(eps))
+    return SAGE_ERR_INVALID_VALUE;
+  if (!aligned16(gamma_q) || !aligned16(gamma_k)) return SAGE_ERR_MISALIGNED;
+  return fwd_impl(D, xq, xk, v, gamma_q, gamma_k, eps, o, lse, ctx, ctx_bytes, ws, ws_bytes, stream);
+}
+
+sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const float* lse, const void* dO,
+                     const void* ctx, size_t ctx_bytes, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
+                     void* stream) {
+  Dims D;
+  if (!dims_of(p, &D) || D.qkn) return SAGE_ERR_INVALID_VALUE;  // QK-norm: sage_bwd_qknorm
+  return bwd_impl(D, v, o, lse, dO, ctx, ctx_bytes, dq, dk, dv, ws, ws_bytes, stream, nullptr, nullptr, nullptr,
+                  nullptr, nullptr, nullptr);
+}
+
+sage_status sage_bwd_qknorm(const sage_params* p, const void* xq, const void* xk, const float* gamma_q,
+                            const float* gamma_k, const void* v, const void* o, const float* lse, const void* dO,
+                            const void* ctx, size_t ctx_bytes, void* dxq, void* dxk, void* dv, float* dgamma_q,
+                            float* dgamma_k, void* ws, size_t ws_bytes, void* stream) {
+  Dims D;
+  if (!dims_of(p, &D) || !D.qkn || !xq || !xk || !gamma_q || !gamma_k || !dgamma_q || !dgamma_k)
+    return SAGE_ERR_INVALID_VALUE;
+  if (!aligned16(xq) || !aligned16(xk) || !aligned16(gamma_q) || !aligned16(gamma_k) || !aligned16(dgamma_q) ||
+      !aligned16(dgamma_k))
+    return SAGE_ERR_MISALIGNED;
+  return bwd_impl(D, v, o, lse, dO, ctx, ctx_bytes, dxq, dxk, dv, ws, ws_bytes, stream, xq, xk, gamma_q, gamma_k,
+                  dgamma_q, dgamma_k);
 }
 
 sage_status sage_debug_trace(void* host_out, size_t bytes) {

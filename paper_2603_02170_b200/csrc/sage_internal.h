@@ -12,8 +12,24 @@ constexpr int kBlk = 128;  // B_q = B_kv = 128 (reading A5): tcgen05 M = 128 til
 constexpr int kMaxSeqLen = 32768;  // per-head scale rows are staged in shared memory (T <= 256)
 
 // ---- memory-bound passes (sage_prep.cu) ----
+// QK-norm input transform (readings A24/A25): when gamma is non-null, every kernel that
+// reads Q or K sees y = bf16(fl32(fl32(x * rstd[row]) * gamma[c])) instead of x, with
+// rstd[row] = fl32(1 / sqrt(mean(x^2) + eps)) computed from the row as it is loaded (K0, K1; K1
+// stores it for the backward) or read back (the Q-smoothing bias kernel, after K1).
+struct NormIn {
+  float* rstd;         // [BH*N]
+  const float* gamma;  // [d] or null (no QK-norm)
+  float eps;
+};
+// RMSNorm backward (reading A26): dx (bf16) from dy (fp32 dy32, or bf16 dy16 -- may alias dx), and
+// dgamma[d] via per-block partials gpart [rows/128][d] fp32 followed by [ceil(rows/128/64)][d] fp64
+// stage sums in the same buffer (fixed-order reduction).
+cudaError_t launch_norm_bwd(const float* dy32, const __nv_bfloat16* dy16, const __nv_bfloat16* x, const float* rstd,
+                            const float* gamma, __nv_bfloat16* dx, float* gpart, float* dgamma, size_t rows, int d,
+                            cudaStream_t s);
 // K0: per-(head, 128-row chunk) column sums in double, fixed order (reading A17).
-cudaError_t launch_colsum(const __nv_bfloat16* x, double* part, int BH, int N, int d, cudaStream_t s);
+cudaError_t launch_colsum(const __nv_bfloat16* x, double* part, int BH, int N, int d, cudaStream_t s,
+                          NormIn nrm = NormIn{nullptr, nullptr, 0.f});
 // K0b: mu[bh][c] = fl32(sum_t part[bh][t][c] / N)  (mu_K).
 cudaError_t launch_colmean(const double* part, float* mu, int BH, int N, int d, cudaStream_t s);
 // K0c: mu_Q[bh][t][c] = fl32(part[bh][t][c] / 128)  (block-wise mu_Qi).
@@ -26,6 +42,9 @@ struct QuantJob {
   int mu_mode;
   int8_t* xq;
   float* scale;
+  float* rstd;         // QK-norm (NormIn): rstd out [BH*N]
+  const float* gamma;  // or null
+  float eps;
 };
 struct QuantJobs {
   QuantJob j[3];
@@ -33,7 +52,7 @@ struct QuantJobs {
 cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int d, cudaStream_t s);
 // Q-smoothing bias_i[n] = mu_Qi . (K[n] - mu_K)  (reading A13), fp32.
 cudaError_t launch_qsmooth_bias(const __nv_bfloat16* k, const float* mu_k, const float* mu_q, float* bias, int BH,
-                                int N, int d, cudaStream_t s);
+                                int N, int d, cudaStream_t s, NormIn nrm = NormIn{nullptr, nullptr, 0.f});
 // K3: delta = rowsum(dO o O) (Alg. 2 line 2), psi(dO) (line 6, reading A22), l2 = lse*log2(e),
 //     dq_acc = 0.
 cudaError_t launch_bwd_prep(const __nv_bfloat16* o, const __nv_bfloat16* dO, const float* lse, float* delta,

@@ -4,6 +4,8 @@
 //   Q-smoothing bias mu_Qi . K_sm^T       (reading A13)
 //   K3  backward prep: delta, psi(dO), L*log2(e), zero dQ accumulator  (Alg. 2 lines 2, 6)
 //   K5  dQ fp32 -> bf16
+//   QK-norm: per-row rstd, the normalised bf16 Q/K computed on the fly inside K0 / K1 /
+//       the bias kernel, and the RMSNorm backward (dX, dgamma) fused with the dQ finalisation
 // Built without --use_fast_math; every FP32 op that decides a bit-exact INT8 value
 // is an explicit round-to-nearest intrinsic (__fsub_rn, __fmul_rn, __fdiv_rn) so
 // nvcc cannot contract it (reading A4).
@@ -13,6 +15,7 @@ namespace sage {
 namespace {
 
 constexpr int kVec = 8;  // bf16 elements per 16-byte vector
+constexpr int nrm_smem_rows = 128;  // QK-norm partial sums of squares: [128 rows][column groups] doubles
 
 __device__ __forceinline__ void load_bf16x8(const __nv_bfloat16* p, float (&f)[8]) {
   uint4 u = *reinterpret_cast<const uint4*>(p);
@@ -25,6 +28,23 @@ __device__ __forceinline__ void load_bf16x8(const __nv_bfloat16* p, float (&f)[8
   }
 }
 
+__device__ __forceinline__ void unpack_bf16x8(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    float2 t = __bfloat1622float2(h[e]);
+    f[2 * e] = t.x;
+    f[2 * e + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack_bf16x8(const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+  return u;
+}
+
 // q = RNE(fl32(x * inv)) for four values, packed as int8x4.  fl32(y + 1.5*2^23) holds RNE(y) in
 // its low bits (|y| < 2^22), so the rounding is an FADD instead of an XU-pipe F2I; |y| <= 127(1+2^-23)
 // because inv = fl32(127/amax), hence |RNE(y)| <= 127 and no clamp is needed (readings A1, A2, A4).
@@ -34,6 +54,45 @@ __device__ __forceinline__ uint32_t quant4(const float* x, float inv) {
 #pragma unroll
   for (int e = 0; e < 4; ++e) b[e] = __float_as_uint(__fadd_rn(__fmul_rn(x[e], inv), kMagic));
   return __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+}
+
+// QK-norm output (readings A24/A25): y = bf16(fl32(fl32(x * rstd) * gamma)), the value an unfused
+// BF16 RMSNorm module would hand to the attention; every later step sees exactly these values.
+__device__ __forceinline__ float qk_norm(float x, float r, float g) {
+  return __bfloat162float(__float2bfloat16_rn(__fmul_rn(__fmul_rn(x, r), g)));
+}
+
+// QK-norm row statistics of a 128-row chunk (reading A24): rstd = fl32(1 / sqrt(sum_c x^2 / D + eps)).
+// Each of the 256 threads holds NR rows x 8 columns (row r0 + k*RS, column group g of G); it writes
+// its partial sums of squares (double: bf16 squares and their sums are exact unless a row's squares
+// span > 30 binades, so the order is immaterial) to shared memory, then one thread per row adds the
+// G partials and takes the IEEE double sqrt and division once, rounding to fp32 once.  Result in
+// rs_s[128] (and rstd_out[128] if non-null).  All 256 threads must call it.
+template <int G, int D, int NR, int RS>
+__device__ __forceinline__ void chunk_rstd(const uint4 (&raw)[NR], int g, int r0, double* ssq, float* rs_s, float eps,
+                                           float* rstd_out) {
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[k]);
+    double ss = 0.0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 t = __bfloat1622float2(h[e]);
+      ss = fma((double)t.x, (double)t.x, ss);
+      ss = fma((double)t.y, (double)t.y, ss);
+    }
+    ssq[(r0 + k * RS) * G + g] = ss;
+  }
+  __syncthreads();
+  if (threadIdx.x < kBlk) {
+    double ss = 0.0;
+#pragma unroll
+    for (int j = 0; j < G; ++j) ss += ssq[threadIdx.x * G + j];
+    const float rs = __double2float_rn(1.0 / sqrt(ss / (double)D + (double)eps));
+    rs_s[threadIdx.x] = rs;
+    if (rstd_out) rstd_out[threadIdx.x] = rs;
+  }
+  __syncthreads();
 }
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -48,8 +107,9 @@ __device__ __forceinline__ float warp_max(float v) {
 // loads), then the R partials are combined in fixed order q = 0..R-1.  Sums of bf16 values in
 // double are exact unless a column spans > 53-8-log2(N) binades, so the order cannot change the
 // result for any realistic input; it is fixed anyway.
-template <int D>
-__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ x, double* __restrict__ part) {
+template <int D, bool QKN>
+__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ x, double* __restrict__ part,
+                                                     NormIn nrm) {
   constexpr int kGroups = D / kVec;        // 8 (d=64) or 16 (d=128)
   constexpr int kR = 256 / kGroups;        // 32 or 16 row phases
   __shared__ double red[kR][D];
@@ -57,12 +117,28 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
   const int g = threadIdx.x % kGroups, q = threadIdx.x / kGroups;
   const __nv_bfloat16* p = x + chunk * kBlk * D + g * kVec;
   double acc[kVec];
+  float gam[kVec];
 #pragma unroll
-  for (int e = 0; e < kVec; ++e) acc[e] = 0.0;
+  for (int e = 0; e < kVec; ++e) {
+    acc[e] = 0.0;
+    gam[e] = QKN ? nrm.gamma[g * kVec + e] : 1.f;
+  }
+  constexpr int kRows = kBlk / kR;  // rows per thread: all loads issued before any arithmetic
+  uint4 raw[kRows];
 #pragma unroll
-  for (int r = q; r < kBlk; r += kR) {
+  for (int k = 0; k < kRows; ++k) raw[k] = *reinterpret_cast<const uint4*>(p + (size_t)(q + k * kR) * D);
+  __shared__ double ssq[QKN ? nrm_smem_rows * kGroups : 1];
+  __shared__ float rs_s[QKN ? kBlk : 1];
+  if constexpr (QKN) chunk_rstd<kGroups, D, kRows, kR>(raw, g, q, ssq, rs_s, nrm.eps, nullptr);
+#pragma unroll
+  for (int k = 0; k < kRows; ++k) {
     float f[kVec];
-    load_bf16x8(p + (size_t)r * D, f);
+    unpack_bf16x8(raw[k], f);
+    if constexpr (QKN) {  // QK-norm (A24/A25)
+      const float rs = rs_s[q + k * kR];
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) f[e] = qk_norm(f[e], rs, gam[e]);
+    }
 #pragma unroll
     for (int e = 0; e < kVec; ++e) acc[e] += (double)f[e];
   }
@@ -97,8 +173,8 @@ __global__ void blockmean_kernel(const double* __restrict__ part, float* __restr
 // ---------------------------------------------------------------- K1: psi
 // One CTA quantises one 128 x d block: x_sm = fl32(x - mu); amax; scale = fl32(amax/127);
 // inv = fl32(127/amax) (0 for an all-zero block, A3); q = clamp(RNE(fl32(x_sm*inv)), +-127).
-template <int D>
-__global__ void __launch_bounds__(256) quantize_kernel(QuantJobs jobs, int T) {
+template <int D, bool QKN>
+__global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T) {
   // blockIdx.y selects the tensor (Q, K, V): one launch for all three psi passes
   const QuantJob& job = jobs.j[blockIdx.y];
   const __nv_bfloat16* __restrict__ x = job.x;
@@ -121,17 +197,34 @@ __global__ void __launch_bounds__(256) quantize_kernel(QuantJobs jobs, int T) {
     int c = g * kVec + e;
     m[e] = mu_mode == 0 ? 0.f : (mu_mode == 1 ? mu[(size_t)bh * D + c] : mu[((size_t)bh * T + t) * D + c]);
   }
-  float v[kIters][kVec];
+  // pass 1: every row's 16-byte vector is loaded before any arithmetic (kIters loads in flight);
+  // the (QK-normed) bf16 values stay packed in registers for pass 2, which recomputes x - mu
+  uint4 raw[kIters];
+#pragma unroll
+  for (int it = 0; it < kIters; ++it)
+    raw[it] = *reinterpret_cast<const uint4*>(xb + (size_t)(r0 + it * kRowsPerPass) * D + g * kVec);
+  // QK-norm row statistics (A24), kept for the backward (QKN launches: every job with gamma)
+  __shared__ double ssq[QKN ? nrm_smem_rows * kGroups : 1];
+  __shared__ float rs_s[QKN ? kBlk : 1];
+  if constexpr (QKN) {
+    if (job.gamma) chunk_rstd<kGroups, D, kIters, kRowsPerPass>(raw, g, r0, ssq, rs_s, job.eps, job.rstd + blk * kBlk);
+  }
   float amax = 0.f;
 #pragma unroll
   for (int it = 0; it < kIters; ++it) {
-    int r = r0 + it * kRowsPerPass;
-    load_bf16x8(xb + (size_t)r * D + g * kVec, v[it]);
+    float v[kVec];
+    unpack_bf16x8(raw[it], v);
+    if (QKN && job.gamma) {  // QK-norm (A25) before the smoothing subtraction
+      float gam[kVec];
 #pragma unroll
-    for (int e = 0; e < kVec; ++e) {
-      v[it][e] = __fsub_rn(v[it][e], m[e]);
-      amax = fmaxf(amax, fabsf(v[it][e]));
+      for (int e = 0; e < kVec; ++e) gam[e] = job.gamma[g * kVec + e];
+      const float rs = rs_s[r0 + it * kRowsPerPass];
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) v[e] = qk_norm(v[e], rs, gam[e]);
+      raw[it] = pack_bf16x8(v);  // exact: qk_norm values are bf16
     }
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) amax = fmaxf(amax, fabsf(__fsub_rn(v[e], m[e])));
   }
   amax = warp_max(amax);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
@@ -146,9 +239,13 @@ __global__ void __launch_bounds__(256) quantize_kernel(QuantJobs jobs, int T) {
 #pragma unroll
   for (int it = 0; it < kIters; ++it) {
     int r = r0 + it * kRowsPerPass;
+    float v[kVec];
+    unpack_bf16x8(raw[it], v);
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) v[e] = __fsub_rn(v[e], m[e]);
     uint32_t w[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) w[h] = quant4(v[it] + 4 * h, inv);
+    for (int h = 0; h < 2; ++h) w[h] = quant4(v + 4 * h, inv);
     *reinterpret_cast<uint2*>(qb + (size_t)r * D + g * kVec) = make_uint2(w[0], w[1]);
   }
 }
@@ -162,7 +259,7 @@ template <int D>
 __global__ void __launch_bounds__(128) qsmooth_bias_kernel(const __nv_bfloat16* __restrict__ k,
                                                            const float* __restrict__ mu_k,
                                                            const float* __restrict__ mu_q, float* __restrict__ bias,
-                                                           int N) {
+                                                           int N, NormIn nrm) {
   __shared__ float4 mq[kBiasI][D / 4];
   const int T = N / kBlk;
   const long long blk = blockIdx.x;    // bh * T + jn
@@ -174,10 +271,15 @@ __global__ void __launch_bounds__(128) qsmooth_bias_kernel(const __nv_bfloat16* 
   float ks[D];
   const __nv_bfloat16* krow = k + (blk * kBlk + n) * D;
   const float* mk = mu_k + (size_t)bh * D;
+  const float rs = nrm.gamma ? nrm.rstd[blk * kBlk + n] : 1.f;  // written by K1's K job
 #pragma unroll
   for (int c = 0; c < D; c += kVec) {
     float f[kVec];
     load_bf16x8(krow + c, f);
+    if (nrm.gamma) {
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) f[e] = qk_norm(f[e], rs, nrm.gamma[c + e]);
+    }
 #pragma unroll
     for (int e = 0; e < kVec; ++e) ks[c + e] = __fsub_rn(f[e], mk[c + e]);
   }
@@ -270,14 +372,155 @@ __global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16*
   reinterpret_cast<uint4*>(dq)[i] = *reinterpret_cast<uint4*>(h);
 }
 
+// ---------------------------------------------------------------- QK-norm backward
+// RMSNorm backward (reading A26) for one 128-row block per CTA, 16 rows per warp, D/32 consecutive
+// columns per lane (vector loads), the 16 rows loaded before any reduction so their loads overlap:
+// dy = bf16(attention gradient) (from the fp32 dQ accumulator, or the bf16 dK in place),
+// g = dy o gamma, xh = x rstd, dx = rstd (g - xh mean(g o xh)) -> bf16;  gpart[block][c] = sum
+// over the block's rows of dy o xh (fixed order: rows within a warp, then warps 0..7).
+template <int D>
+__global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__ dy32, const __nv_bfloat16* dy16,
+                                                       const __nv_bfloat16* __restrict__ x,
+                                                       const float* __restrict__ rstd, const float* __restrict__ gamma,
+                                                       __nv_bfloat16* dx, float* __restrict__ gpart) {
+  constexpr int kPer = D / 32;  // 4 or 2
+  constexpr int kRows = 16;
+  __shared__ float red[8][D];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const size_t blk = blockIdx.x;
+  const size_t row0 = blk * kBlk + warp * kRows;
+  float gam[kPer], gacc[kPer];
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    gam[e] = gamma[lane * kPer + e];
+    gacc[e] = 0.f;
+  }
+  float dy[kRows][kPer], xv[kRows][kPer], rs[kRows];
+#pragma unroll
+  for (int rr = 0; rr < kRows; ++rr) {
+    const size_t off = (row0 + rr) * D + lane * kPer;
+    rs[rr] = rstd[row0 + rr];
+    if constexpr (kPer == 4) {
+      const uint2 xu = *reinterpret_cast<const uint2*>(x + off);
+      const float2 x0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xu.x));
+      const float2 x1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xu.y));
+      xv[rr][0] = x0.x; xv[rr][1] = x0.y; xv[rr][2] = x1.x; xv[rr][3] = x1.y;
+      if (dy32) {
+        const float4 f = *reinterpret_cast<const float4*>(dy32 + off);
+        dy[rr][0] = f.x; dy[rr][1] = f.y; dy[rr][2] = f.z; dy[rr][3] = f.w;
+      } else {
+        const uint2 du = *reinterpret_cast<const uint2*>(dy16 + off);
+        const float2 d0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&du.x));
+        const float2 d1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&du.y));
+        dy[rr][0] = d0.x; dy[rr][1] = d0.y; dy[rr][2] = d1.x; dy[rr][3] = d1.y;
+      }
+    } else {
+      const float2 x0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + off));
+      xv[rr][0] = x0.x; xv[rr][1] = x0.y;
+      if (dy32) {
+        const float2 f = *reinterpret_cast<const float2*>(dy32 + off);
+        dy[rr][0] = f.x; dy[rr][1] = f.y;
+      } else {
+        const float2 d0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dy16 + off));
+        dy[rr][0] = d0.x; dy[rr][1] = d0.y;
+      }
+    }
+  }
+  float dot[kRows];
+#pragma unroll
+  for (int rr = 0; rr < kRows; ++rr) {
+    dot[rr] = 0.f;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      if (dy32) dy[rr][e] = __bfloat162float(__float2bfloat16_rn(dy[rr][e]));  // A26
+      xv[rr][e] *= rs[rr];                                                    // xh
+      gacc[e] = fmaf(dy[rr][e], xv[rr][e], gacc[e]);
+      dy[rr][e] *= gam[e];                                                    // g
+      dot[rr] = fmaf(dy[rr][e], xv[rr][e], dot[rr]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+#pragma unroll
+    for (int rr = 0; rr < kRows; ++rr) dot[rr] += __shfl_xor_sync(0xffffffffu, dot[rr], o);
+  }
+#pragma unroll
+  for (int rr = 0; rr < kRows; ++rr) {
+    const size_t off = (row0 + rr) * D + lane * kPer;
+    const float mean = dot[rr] * (1.f / D);
+    __nv_bfloat162 h[kPer / 2];
+#pragma unroll
+    for (int e = 0; e < kPer; e += 2)
+      h[e / 2] = __floats2bfloat162_rn(rs[rr] * fmaf(-xv[rr][e], mean, dy[rr][e]),
+                                       rs[rr] * fmaf(-xv[rr][e + 1], mean, dy[rr][e + 1]));
+    if constexpr (kPer == 4)
+      *reinterpret_cast<uint2*>(dx + off) = *reinterpret_cast<const uint2*>(h);
+    else
+      *reinterpret_cast<__nv_bfloat162*>(dx + off) = h[0];
+  }
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) red[warp][lane * kPer + e] = gacc[e];
+  __syncthreads();
+  if (threadIdx.x < D) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+    gpart[blk * D + threadIdx.x] = s;
+  }
+}
+
+// dgamma[c] = sum over blocks of gpart[block][c], fixed order, coalesced: stage 1 (one CTA per 64
+// consecutive blocks, thread = column) sums in block order into part2 (double); stage 2 sums
+// part2 in order.
+constexpr int kGBlk = 64;
+__global__ void dgamma_stage1_kernel(const float* __restrict__ gpart, double* __restrict__ part2, int nblk, int D) {
+  const int c = threadIdx.x;
+  const int b0 = blockIdx.x * kGBlk, b1 = min(nblk, b0 + kGBlk);
+  double s = 0.0;
+  for (int b = b0; b < b1; ++b) s += (double)gpart[(size_t)b * D + c];
+  part2[(size_t)blockIdx.x * D + c] = s;
+}
+__global__ void dgamma_stage2_kernel(const double* __restrict__ part2, float* __restrict__ dgamma, int n2, int D) {
+  const int c = threadIdx.x;
+  double s = 0.0;
+  for (int b = 0; b < n2; ++b) s += part2[(size_t)b * D + c];
+  dgamma[c] = __double2float_rn(s);
+}
+
 }  // namespace
 
-cudaError_t launch_colsum(const __nv_bfloat16* x, double* part, int BH, int N, int d, cudaStream_t s) {
+cudaError_t launch_colsum(const __nv_bfloat16* x, double* part, int BH, int N, int d, cudaStream_t s, NormIn nrm) {
   const unsigned grid = (unsigned)(BH * (N / kBlk));
+  if (nrm.gamma) {
+    if (d == 128)
+      colsum_kernel<128, true><<<grid, 256, 0, s>>>(x, part, nrm);
+    else
+      colsum_kernel<64, true><<<grid, 256, 0, s>>>(x, part, nrm);
+  } else {
+    if (d == 128)
+      colsum_kernel<128, false><<<grid, 256, 0, s>>>(x, part, nrm);
+    else
+      colsum_kernel<64, false><<<grid, 256, 0, s>>>(x, part, nrm);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm_bwd(const float* dy32, const __nv_bfloat16* dy16, const __nv_bfloat16* x, const float* rstd,
+                            const float* gamma, __nv_bfloat16* dx, float* gpart, float* dgamma, size_t rows, int d,
+                            cudaStream_t s) {
+  const unsigned nblk = (unsigned)(rows / kBlk);
   if (d == 128)
-    colsum_kernel<128><<<grid, 256, 0, s>>>(x, part);
+    norm_bwd_kernel<128><<<nblk, 256, 0, s>>>(dy32, dy16, x, rstd, gamma, dx, gpart);
   else
-    colsum_kernel<64><<<grid, 256, 0, s>>>(x, part);
+    norm_bwd_kernel<64><<<nblk, 256, 0, s>>>(dy32, dy16, x, rstd, gamma, dx, gpart);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // the stage-1 sums (double) follow the nblk x d block partials in the same workspace slot
+  const unsigned n2 = (nblk + kGBlk - 1) / kGBlk;
+  double* part2 = reinterpret_cast<double*>(gpart + (size_t)nblk * d + ((size_t)nblk * d & 1));
+  dgamma_stage1_kernel<<<n2, d, 0, s>>>(gpart, part2, (int)nblk, d);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  dgamma_stage2_kernel<<<1, d, 0, s>>>(part2, dgamma, (int)n2, d);
   return cudaGetLastError();
 }
 
@@ -296,21 +539,30 @@ cudaError_t launch_blockmean(const double* part, float* mu_q, int BH, int N, int
 cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int d, cudaStream_t s) {
   int T = N / kBlk;
   dim3 grid((unsigned)(BH * T), (unsigned)njobs);
-  if (d == 128)
-    quantize_kernel<128><<<grid, 256, 0, s>>>(jobs, T);
-  else
-    quantize_kernel<64><<<grid, 256, 0, s>>>(jobs, T);
+  bool qkn = false;
+  for (int i = 0; i < njobs; ++i) qkn = qkn || jobs.j[i].gamma;
+  if (qkn) {
+    if (d == 128)
+      quantize_kernel<128, true><<<grid, 256, 0, s>>>(jobs, T);
+    else
+      quantize_kernel<64, true><<<grid, 256, 0, s>>>(jobs, T);
+  } else {
+    if (d == 128)
+      quantize_kernel<128, false><<<grid, 256, 0, s>>>(jobs, T);
+    else
+      quantize_kernel<64, false><<<grid, 256, 0, s>>>(jobs, T);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_qsmooth_bias(const __nv_bfloat16* k, const float* mu_k, const float* mu_q, float* bias, int BH,
-                                int N, int d, cudaStream_t s) {
+                                int N, int d, cudaStream_t s, NormIn nrm) {
   const int T = N / kBlk;
   dim3 grid((unsigned)(BH * T), (unsigned)((T + kBiasI - 1) / kBiasI));
   if (d == 128)
-    qsmooth_bias_kernel<128><<<grid, 128, 0, s>>>(k, mu_k, mu_q, bias, N);
+    qsmooth_bias_kernel<128><<<grid, 128, 0, s>>>(k, mu_k, mu_q, bias, N, nrm);
   else
-    qsmooth_bias_kernel<64><<<grid, 128, 0, s>>>(k, mu_k, mu_q, bias, N);
+    qsmooth_bias_kernel<64><<<grid, 128, 0, s>>>(k, mu_k, mu_q, bias, N, nrm);
   return cudaGetLastError();
 }
 

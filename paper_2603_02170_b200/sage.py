@@ -14,12 +14,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # SAGE_LIB selects the profiling build (libsage_trace.so) for scripts/trace_bwd.py only.
 LIB_PATH = os.environ.get("SAGE_LIB") or os.path.join(_HERE, "libsage.so")
 
-SAGE_CAUSAL, SAGE_K_SMOOTH, SAGE_Q_SMOOTH, SAGE_P_U8 = 1, 2, 4, 8
+SAGE_CAUSAL, SAGE_K_SMOOTH, SAGE_Q_SMOOTH, SAGE_P_U8, SAGE_QK_NORM = 1, 2, 4, 8, 16
 _STATUS = {0: "SAGE_OK", 1: "SAGE_ERR_INVALID_VALUE", 2: "SAGE_ERR_UNSUPPORTED", 3: "SAGE_ERR_MISALIGNED",
            4: "SAGE_ERR_WORKSPACE", 5: "SAGE_ERR_CUDA", 6: "SAGE_ERR_ARCH"}
 
 # exported symbols of include/sage.h
-SYMBOLS = ("sage_ctx_bytes", "sage_workspace_bytes", "sage_fwd", "sage_bwd", "sage_ctx_get_view",
+SYMBOLS = ("sage_ctx_bytes", "sage_workspace_bytes", "sage_fwd", "sage_bwd", "sage_fwd_qknorm", "sage_bwd_qknorm",
+           "sage_ctx_get_view",
            "sage_ws_get_view", "sage_debug_umma", "sage_debug_trace", "sage_debug_dump", "sage_profile_enable", "sage_profile_read",
            "sage_status_string", "sage_last_cuda_error", "sage_version")
 
@@ -30,7 +31,8 @@ class SageParams(ctypes.Structure):
 
 
 class SageCtxView(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_void_p) for n in ("q_i8", "k_i8", "q_scale", "k_scale", "mu_k", "mu_q", "bias")]
+    _fields_ = [(n, ctypes.c_void_p) for n in ("q_i8", "k_i8", "q_scale", "k_scale", "mu_k", "mu_q", "bias",
+                                               "rstd_q", "rstd_k")]
 
 
 class SageWsView(ctypes.Structure):
@@ -59,6 +61,8 @@ def lib():
         L.sage_workspace_bytes.restype = S
         L.sage_fwd.argtypes = [pp, P, P, P, P, P, P, S, P, S, P]
         L.sage_bwd.argtypes = [pp, P, P, P, P, P, S, P, P, P, P, S, P]
+        L.sage_fwd_qknorm.argtypes = [pp, P, P, P, P, P, ctypes.c_float, P, P, P, S, P, S, P]
+        L.sage_bwd_qknorm.argtypes = [pp, P, P, P, P, P, P, P, P, P, S, P, P, P, P, P, P, S, P]
         L.sage_ctx_get_view.argtypes = [pp, P, ctypes.POINTER(SageCtxView)]
         L.sage_ws_get_view.argtypes = [pp, ctypes.c_int, P, ctypes.POINTER(SageWsView)]
         L.sage_debug_umma.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P]
@@ -88,9 +92,9 @@ def _check(status, what):
 
 
 def make_params(batch, heads, seqlen, head_dim, causal=False, k_smooth=True, q_smooth=False, softmax_scale=None,
-                p_u8=False):
+                p_u8=False, qk_norm=False):
     flags = (SAGE_CAUSAL if causal else 0) | (SAGE_K_SMOOTH if k_smooth else 0) | (SAGE_Q_SMOOTH if q_smooth else 0) | \
-        (SAGE_P_U8 if p_u8 else 0)
+        (SAGE_P_U8 if p_u8 else 0) | (SAGE_QK_NORM if qk_norm else 0)
     return SageParams(batch, heads, seqlen, head_dim, flags, 0.0 if softmax_scale is None else softmax_scale)
 
 
@@ -138,7 +142,9 @@ class SageCtx:
                    k_scale=sl(v.k_scale, B * H * T, torch.float32, (B, H, T)),
                    mu_k=sl(v.mu_k, B * H * d, torch.float32, (B, H, d)),
                    mu_q=sl(v.mu_q, B * H * T * d, torch.float32, (B, H, T, d)),
-                   bias=sl(v.bias, B * H * T * N, torch.float32, (B, H, T, N)))
+                   bias=sl(v.bias, B * H * T * N, torch.float32, (B, H, T, N)),
+                   rstd_q=sl(v.rstd_q, B * H * N, torch.float32, (B, H, N)),
+                   rstd_k=sl(v.rstd_k, B * H * N, torch.float32, (B, H, N)))
         return out
 
 
@@ -202,6 +208,76 @@ def backward(ctx, v, o, lse, do, dq=None, dk=None, dv=None, workspace=None, stre
                           ctx.buf.numel(), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream(stream)),
            "sage_bwd")
     return dq, dk, dv
+
+
+def _check_gamma(g, d, device):
+    if not (g.is_cuda and g.dtype == torch.float32 and g.is_contiguous() and g.shape == (d,) and g.device == device):
+        raise SageError("gamma must be a contiguous CUDA fp32 [d] tensor on the inputs' device")
+
+
+def forward_qknorm(xq, xk, v, gamma_q, gamma_k, eps=1e-6, causal=False, k_smooth=True, q_smooth=False,
+                   softmax_scale=None, p_u8=False, out=None, lse=None, ctx=None, workspace=None, stream=None):
+    """sage_fwd_qknorm: QK-norm fused in front of Alg. 1.  xq, xk: the pre-norm bf16
+    [B, H, N, d]; gamma_q, gamma_k: fp32 [d].  Returns (o, lse, SageCtx)."""
+    _check_io(xq, xk, v)
+    B, H, N, d = xq.shape
+    _check_gamma(gamma_q, d, xq.device)
+    _check_gamma(gamma_k, d, xq.device)
+    p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8, qk_norm=True)
+    nctx = lib().sage_ctx_bytes(ctypes.byref(p))
+    if nctx == 0:
+        raise SageError(f"unsupported shape/flags {tuple(xq.shape)}")
+    o = torch.empty_like(xq) if out is None else out
+    lse = torch.empty((B, H, N), dtype=torch.float32, device=xq.device) if lse is None else lse
+    ctxb = torch.empty(nctx, dtype=torch.uint8, device=xq.device) if ctx is None else ctx
+    ws = _ws.get(p, False, xq.device) if workspace is None else workspace
+    _check(lib().sage_fwd_qknorm(ctypes.byref(p), _ptr(xq), _ptr(xk), _ptr(v), _ptr(gamma_q), _ptr(gamma_k),
+                                 float(eps), _ptr(o), _ptr(lse), _ptr(ctxb), ctxb.numel(), _ptr(ws), ws.numel(),
+                                 _stream(stream)), "sage_fwd_qknorm")
+    return o, lse, SageCtx(p, ctxb, (B, H, N, d))
+
+
+def backward_qknorm(ctx, xq, xk, gamma_q, gamma_k, v, o, lse, do, out=None, workspace=None, stream=None):
+    """sage_bwd_qknorm: returns (dxq, dxk, dv, dgamma_q, dgamma_k) (into `out` if given)."""
+    _check_io(xq, xk, v, o, do)
+    d = xq.shape[-1]
+    _check_gamma(gamma_q, d, xq.device)
+    _check_gamma(gamma_k, d, xq.device)
+    if out is None:
+        out = (torch.empty_like(do), torch.empty_like(do), torch.empty_like(do),
+               torch.empty(d, dtype=torch.float32, device=do.device),
+               torch.empty(d, dtype=torch.float32, device=do.device))
+    dxq, dxk, dv, dgq, dgk = out
+    ws = _ws.get(ctx.params, True, do.device) if workspace is None else workspace
+    _check(lib().sage_bwd_qknorm(ctypes.byref(ctx.params), _ptr(xq), _ptr(xk), _ptr(gamma_q), _ptr(gamma_k), _ptr(v),
+                                 _ptr(o), _ptr(lse), _ptr(do), _ptr(ctx.buf), ctx.buf.numel(), _ptr(dxq), _ptr(dxk),
+                                 _ptr(dv), _ptr(dgq), _ptr(dgk), _ptr(ws), ws.numel(), _stream(stream)),
+           "sage_bwd_qknorm")
+    return dxq, dxk, dv, dgq, dgk
+
+
+class SageAttentionQKNormFn(torch.autograd.Function):
+    """autograd wrapper: O = SageBwd(RMSNorm(X_q) gamma_q, RMSNorm(X_k) gamma_k, V)."""
+
+    @staticmethod
+    def forward(fctx, xq, xk, v, gamma_q, gamma_k, eps, causal, k_smooth, q_smooth, softmax_scale):
+        xq, xk, v = xq.contiguous(), xk.contiguous(), v.contiguous()
+        gq, gk = gamma_q.contiguous(), gamma_k.contiguous()
+        o, lse, c = forward_qknorm(xq, xk, v, gq, gk, eps, causal, k_smooth, q_smooth, softmax_scale)
+        fctx.sage = c
+        fctx.save_for_backward(xq, xk, v, gq, gk, o, lse)
+        return o
+
+    @staticmethod
+    def backward(fctx, do):
+        xq, xk, v, gq, gk, o, lse = fctx.saved_tensors
+        dxq, dxk, dv, dgq, dgk = backward_qknorm(fctx.sage, xq, xk, gq, gk, v, o, lse, do.contiguous())
+        return dxq, dxk, dv, dgq, dgk, None, None, None, None, None
+
+
+def sage_attention_qknorm(xq, xk, v, gamma_q, gamma_k, eps=1e-6, causal=False, k_smooth=True, q_smooth=False,
+                          softmax_scale=None):
+    return SageAttentionQKNormFn.apply(xq, xk, v, gamma_q, gamma_k, eps, causal, k_smooth, q_smooth, softmax_scale)
 
 
 class SageAttentionFn(torch.autograd.Function):

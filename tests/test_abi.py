@@ -66,6 +66,21 @@ def test_error_paths_do_not_launch(L):
     assert L.sage_bwd(ctypes.byref(p), A, A, A, A, A, S(nctx), A, A, mis, A, S(nwb), z) == 3
     assert L.sage_debug_umma(8, 64, 128, A, A, A, z) == 1
     assert L.sage_debug_umma(1, 128, 96, A, A, A, z) == 1
+    # QK-norm params need the _qknorm entry points, which need gamma and eps > 0
+    pn = make_params(1, 2, 256, 64, qk_norm=True)
+    ncn = L.sage_ctx_bytes(ctypes.byref(pn))
+    assert ncn > nctx  # + rstd of the X_q, X_k rows
+    nwn = L.sage_workspace_bytes(ctypes.byref(pn), 0)
+    assert L.sage_fwd(ctypes.byref(pn), A, A, A, A, A, A, S(ncn), A, S(nwn), z) == 1
+    assert L.sage_bwd(ctypes.byref(pn), A, A, A, A, A, S(ncn), A, A, A, A, S(1 << 30), z) == 1
+    F = ctypes.c_float
+    assert L.sage_fwd_qknorm(ctypes.byref(p), A, A, A, A, A, F(1e-6), A, A, A, S(nctx), A, S(nws), z) == 1
+    assert L.sage_fwd_qknorm(ctypes.byref(pn), A, A, A, z, A, F(1e-6), A, A, A, S(ncn), A, S(nwn), z) == 1
+    assert L.sage_fwd_qknorm(ctypes.byref(pn), A, A, A, A, A, F(0.0), A, A, A, S(ncn), A, S(nwn), z) == 1
+    assert L.sage_fwd_qknorm(ctypes.byref(pn), A, A, A, mis, A, F(1e-6), A, A, A, S(ncn), A, S(nwn), z) == 3
+    assert L.sage_fwd_qknorm(ctypes.byref(pn), A, A, A, A, A, F(1e-6), A, A, A, S(ncn - 1), A, S(nwn), z) == 4
+    assert L.sage_bwd_qknorm(ctypes.byref(pn), A, A, A, A, A, A, A, A, A, S(ncn), A, A, A, z, A, A, S(1 << 30),
+                             z) == 1
     # the tile dump exists only in the test build (libsage_trace.so)
     assert L.sage_debug_dump(A, A, A, A, A, 1) == 2
 

@@ -232,3 +232,74 @@ def test_full_size_long_sampled_head(cfg, heads):
     gpu = _run(q, k, v, do, c.causal, c.k_smooth, c.q_smooth)
     f, b = _oracle(q, k, v, do, heads, c.causal, c.k_smooth, c.q_smooth)
     _assert_ok(_compare(gpu, f, b, heads, c.batch, c.heads, c.seqlen, c.head_dim), cfg)
+
+
+# ------------------------------------------------------------------ QK-norm variant
+QKN_CASES = [
+    # (B, H, N, d, causal, k_smooth, q_smooth)
+    (1, 2, 384, 64, True, True, False),
+    (1, 2, 256, 128, False, True, False),
+    (1, 2, 384, 128, True, True, True),
+]
+
+
+def _qkn_inputs(B, H, N, d, seed):
+    xq, xk, v, do = make_inputs(B, H, N, d, "noqknorm", seed=seed)
+    g = torch.Generator().manual_seed(seed + 7)
+    gq = (0.5 + 1.5 * torch.rand(d, generator=g)).float()
+    gk = (0.5 + 1.5 * torch.rand(d, generator=g)).float()
+    return xq, xk, v, do, gq, gk
+
+
+@pytest.mark.parametrize("B,H,N,d,causal,ks,qs", QKN_CASES)
+def test_qknorm_parity(B, H, N, d, causal, ks, qs):
+    """sage_fwd_qknorm / sage_bwd_qknorm against oracle.qknorm + the quantised oracle:
+    rstd, Q^, K^ and their scales bit-exact (Tier A: the fused normalisation produces exactly the
+    bf16 Q, K of readings A24/A25); O, dX_q, dX_k, dV within the tolerance; dgamma likewise."""
+    xq, xk, v, do, gq, gk = _qkn_inputs(B, H, N, d, seed=400 + N + d)
+    dev = "cuda"
+    xqd, xkd, vd, dod, gqd, gkd = (t.to(dev) for t in (xq, xk, v, do, gq, gk))
+    o, lse, ctx = sage.forward_qknorm(xqd, xkd, vd, gqd, gkd, 1e-6, causal=causal, k_smooth=ks, q_smooth=qs)
+    dxq, dxk, dv, dgq, dgk = sage.backward_qknorm(ctx, xqd, xkd, gqd, gkd, vd, o, lse, dod)
+    torch.cuda.synchronize()
+    BH = B * H
+    flat = lambda t: f64(t).reshape(BH, N, d)
+    qn_, rq = oracle.qknorm.forward(flat(xq), gq.numpy(), 1e-6)
+    kn_, rk = oracle.qknorm.forward(flat(xk), gk.numpy(), 1e-6)
+    view = ctx.view()
+    np.testing.assert_array_equal(view["rstd_q"].cpu().numpy().reshape(BH, N), rq)
+    np.testing.assert_array_equal(view["rstd_k"].cpu().numpy().reshape(BH, N), rk)
+    kw = dict(causal=causal, k_smooth=ks, q_smooth=qs)
+    f = oracle.fwd(qn_, kn_, flat(v), **kw)
+    np.testing.assert_array_equal(view["q_i8"].cpu().numpy().reshape(BH, N, d), f["q8"])
+    np.testing.assert_array_equal(view["k_i8"].cpu().numpy().reshape(BH, N, d), f["k8"])
+    np.testing.assert_array_equal(view["q_scale"].cpu().numpy().reshape(BH, -1), f["sq"])
+    np.testing.assert_array_equal(view["k_scale"].cpu().numpy().reshape(BH, -1), f["sk"])
+    np.testing.assert_array_equal(view["mu_k"].cpu().numpy().reshape(BH, d), f["mu_k"])
+    b = oracle.bwd(qn_, kn_, flat(v), round_bf16(f["o"]), flat(do), f["lse"], **kw)
+    # A26: the module chain hands the bf16-rounded attention gradients to the RMSNorm backward
+    dxq_r, dgq_r = oracle.qknorm.backward(flat(xq), gq.numpy(), rq, round_bf16(b["dq"]))
+    dxk_r, dgk_r = oracle.qknorm.backward(flat(xk), gk.numpy(), rk, round_bf16(b["dk"]))
+    for name, got, ref in (("o", o, f["o"]), ("dxq", dxq, dxq_r), ("dxk", dxk, dxk_r), ("dv", dv, b["dv"])):
+        ref = round_bf16(ref)
+        got = flat(got)
+        rl, cs = rel_l2(ref, got), cos_sim(ref, got)
+        assert rl <= REL_TOL and cs >= COS_TOL, (name, rl, cs)
+    for name, got, ref in (("dgq", dgq, dgq_r), ("dgk", dgk, dgk_r)):
+        got = f64(got)
+        rl, cs = rel_l2(ref, got), cos_sim(ref, got)
+        assert rl <= REL_TOL and cs >= COS_TOL, (name, rl, cs)
+
+
+def test_qknorm_autograd_and_rejections():
+    """The autograd wrapper returns the gamma gradients."""
+    xq, xk, v, do, gq, gk = (t.cuda() for t in _qkn_inputs(1, 2, 256, 64, seed=9))
+    for t in (xq, xk, v, gq, gk):
+        t.requires_grad_(True)
+    o = sage.sage_attention_qknorm(xq, xk, v, gq, gk, causal=True)
+    o.backward(do)
+    o2, lse, ctx = sage.forward_qknorm(xq.detach(), xk.detach(), v.detach(), gq.detach(), gk.detach(), causal=True)
+    ref = sage.backward_qknorm(ctx, xq.detach(), xk.detach(), gq.detach(), gk.detach(), v.detach(), o2, lse, do)
+    assert torch.equal(o, o2)
+    for g1, g2 in zip((xq.grad, xk.grad, v.grad, gq.grad, gk.grad), ref):
+        assert rel_l2(f64(g2), f64(g1)) < 1e-3
