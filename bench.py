@@ -290,28 +290,57 @@ def main():
     ms = total_ms / args.steps
     value = ops_of(c) * world / (ms * 1e-3) / 1e12
 
-    # e2e through the public API with host buffers: H2D of q, k, v, dO and D2H of o, dq, dk, dv
+    # e2e through the public API with host buffers: H2D of q, k, v, dO and D2H of o, dq, dk, dv every
+    # step.  The heads are independent, so the step is pipelined over head chunks on
+    # three streams: chunk k's H2D, chunk k-1's sage_fwd + sage_bwd and chunk k-2's D2H overlap (the
+    # copies are full duplex).  The QK-norm variant's dgamma sums over all heads: serial there.
     outs_h = [torch.empty_like(h).pin_memory() for h in host]
     e2e_ms = []
+    BH = c.batch * c.heads
+    n_chunks = 1 if args.qk_norm else min(8, BH)
+    bounds = [(BH * i // n_chunks, BH * (i + 1) // n_chunks) for i in range(n_chunks)]
+    flat = lambda t: t.view(BH, c.seqlen, c.head_dim)
+    chunk = lambda t, a, b: flat(t)[a:b].unsqueeze(0)  # [1, heads of the chunk, N, d], contiguous
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    if n_chunks > 1:
+        ctxs = [sage.forward(chunk(qd, a, b), chunk(kd, a, b), chunk(vd, a, b), **kw)[2] for a, b in bounds]
     for s in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for dst, src in zip((qd, kd, vd, dod), host):
-            dst.copy_(src, non_blocking=True)
-        step()
-        for dst, src in zip(outs_h, (o, dq, dk, dv)):
-            dst.copy_(src, non_blocking=True)
-        b.record(stream)
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record(s_in)
+        if n_chunks == 1:
+            stream.wait_stream(s_in)
+            for dst, src in zip((qd, kd, vd, dod), host):
+                dst.copy_(src, non_blocking=True)
+            step()
+            for dst, src in zip(outs_h, (o, dq, dk, dv)):
+                dst.copy_(src, non_blocking=True)
+            s_out.wait_stream(stream)
+        else:
+            for i, (lo, hi) in enumerate(bounds):
+                with torch.cuda.stream(s_in):
+                    for dst, src in zip((qd, kd, vd, dod), host):
+                        chunk(dst, lo, hi).copy_(chunk(src, lo, hi), non_blocking=True)
+                stream.wait_stream(s_in)
+                qc, kc, vc, oc, doc, dqc, dkc, dvc = (chunk(t, lo, hi) for t in (qd, kd, vd, o, dod, dq, dk, dv))
+                lc = lse.view(BH, c.seqlen)[lo:hi].unsqueeze(0)
+                sage.forward(qc, kc, vc, out=oc, lse=lc, ctx=ctxs[i].buf, **kw)
+                sage.backward(ctxs[i], vc, oc, lc, doc, dq=dqc, dk=dkc, dv=dvc)
+                s_out.wait_stream(stream)
+                with torch.cuda.stream(s_out):
+                    for dst, src in zip(outs_h, (o, dq, dk, dv)):
+                        chunk(dst, lo, hi).copy_(chunk(src, lo, hi), non_blocking=True)
+        b_ev.record(s_out)
         torch.cuda.synchronize()
         if s > 0:
-            e2e_ms.append(a.elapsed_time(b))
+            e2e_ms.append(a_ev.elapsed_time(b_ev))
     te_ms = max_over_ranks(sum(e2e_ms) / max(1, len(e2e_ms)), dist, dev)
     nbytes = sum(h.numel() * h.element_size() for h in host)
     e2e = None
     if e2e_ms:
         e2e = {"value": ops_of(c) * world / (te_ms * 1e-3) / 1e12, "unit": "TOPS",
-               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": te_ms,
+               "pipeline": f"{n_chunks} head chunks, H2D / compute / D2H on three streams"}
 
     if rank == 0:
         pk = peaks()

@@ -286,9 +286,21 @@ __global__ void __launch_bounds__(kThreads, 2)
           uint32_t v[32];
           tmem_ld32(tbuf(j) + c0 + lane_off, v);
           tmem_wait_ld();
+          if (diag) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (!diag || c0 + e <= r) rm = fmaxf(rm, fmaf(__int2float_rn((int)v[e]), c2, bj[c0 + e]));
+            for (int e = 0; e < 32; ++e)
+              if (c0 + e <= r) rm = fmaxf(rm, fmaf(__int2float_rn((int)v[e]), c2, bj[c0 + e]));
+          } else {  // packed: two logits per FFMA2, a three-input max per pair
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) {
+              const float4 b4 = *reinterpret_cast<const float4*>(bj + c0 + e);
+              const float2 a = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])),
+                                     make_float2(c2, c2), make_float2(b4.x, b4.y));
+              const float2 b = ffma2(make_float2(__int2float_rn((int)v[e + 2]), __int2float_rn((int)v[e + 3])),
+                                     make_float2(c2, c2), make_float2(b4.z, b4.w));
+              rm = fmax3(rm, fmax3(a.x, a.y, b.x), b.y);
+            }
+          }
         }
       }
       const float m_new = fmaxf(m, rm);
@@ -319,8 +331,8 @@ __global__ void __launch_bounds__(kThreads, 2)
           float2 b = make_float2(__int2float_rn((int)v[e + 2]), __int2float_rn((int)v[e + 3]));
           if constexpr (QSMOOTH) {
             const float4 b4 = *reinterpret_cast<const float4*>(bj + c0 + e);
-            a = ffma2(a, make_float2(c2, c2), make_float2(b4.x - sub, b4.y - sub));
-            b = ffma2(b, make_float2(c2, c2), make_float2(b4.z - sub, b4.w - sub));
+            a = ffma2(a, make_float2(c2, c2), fadd2(make_float2(b4.x, b4.y), make_float2(-sub, -sub)));
+            b = ffma2(b, make_float2(c2, c2), fadd2(make_float2(b4.z, b4.w), make_float2(-sub, -sub)));
           } else {
             a = ffma2(a, make_float2(c2, c2), make_float2(-sub, -sub));
             b = ffma2(b, make_float2(c2, c2), make_float2(-sub, -sub));
