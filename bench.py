@@ -297,7 +297,7 @@ def main():
     outs_h = [torch.empty_like(h).pin_memory() for h in host]
     e2e_ms = []
     BH = c.batch * c.heads
-    n_chunks = 1 if args.qk_norm else min(8, BH)
+    n_chunks = 1 if (args.qk_norm or args.e2e_steps == 0) else min(8, BH)
     bounds = [(BH * i // n_chunks, BH * (i + 1) // n_chunks) for i in range(n_chunks)]
     flat = lambda t: t.view(BH, c.seqlen, c.head_dim)
     chunk = lambda t, a, b: flat(t)[a:b].unsqueeze(0)  # [1, heads of the chunk, N, d], contiguous

@@ -1,5 +1,5 @@
 """Summarise an ncu --metrics gpu__time_duration.sum CSV launch list: per kernel, launches and the
-last launch's duration (us).  python scripts/launch_table.py gpurun_out/launches_X.csv [...]"""
+last and the longest launch's duration (us).  python scripts/launch_table.py gpurun_out/launches_X.csv [...]"""
 import collections
 import csv
 import sys
@@ -18,4 +18,4 @@ for path in sys.argv[1:]:
         agg.setdefault(d["Kernel Name"].split("(")[0][:60], []).append(float(d["Metric Value"].replace(",", "")))
     print(path)
     for k, v in agg.items():
-        print(f"  {k:60s} n={len(v):3d} last={v[-1] / 1e3:9.1f} us")
+        print(f"  {k:60s} n={len(v):3d} last={v[-1] / 1e3:9.1f} us  max={max(v) / 1e3:9.1f} us")
