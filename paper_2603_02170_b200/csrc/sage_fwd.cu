@@ -29,6 +29,12 @@ constexpr int kThreads = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLog2_127 = 6.988684686772166f;
 constexpr float kLog2_255 = 7.994353436858858f;
+// Groups of 4 (of the 8 per 32-column chunk) whose exponentials run on the FMA pipe (ex2_poly2), at
+// d=128 (measured: 1 group = 12.5% of the exponentials, C4 K2 4.52 -> 4.40 ms; 2 neutral, 3 slower;
+// none at d=64, where it does not help)
+#ifndef SAGE_K2_POLY
+#define SAGE_K2_POLY 1
+#endif
 
 #ifndef SAGE_TRACE
 #define SAGE_TRACE 0
@@ -337,8 +343,13 @@ __global__ void __launch_bounds__(kThreads, 2)
             a = ffma2(a, make_float2(c2, c2), make_float2(-sub, -sub));
             b = ffma2(b, make_float2(c2, c2), make_float2(-sub, -sub));
           }
-          a = make_float2(ex2(a.x), ex2(a.y));
-          b = make_float2(ex2(b.x), ex2(b.y));
+          if (e4 < (D == 128 ? SAGE_K2_POLY : 0)) {  // FMA-pipe exponentials (MUFU offload)
+            a = ex2_poly2(a);
+            b = ex2_poly2(b);
+          } else {
+            a = make_float2(ex2(a.x), ex2(a.y));
+            b = make_float2(ex2(b.x), ex2(b.y));
+          }
           if (diag) {  // causal mask (reading A14): key n > query r -> P = 0
             if (c0 + e > r) a.x = 0.f;
             if (c0 + e + 1 > r) a.y = 0.f;
