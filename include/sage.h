@@ -65,8 +65,14 @@ enum {
                               for the per-token P^ of Alg. 1 line 9 and psi(P) of Alg. 2 line 6 (the
                               paper's reading: 0..127, A2); the PV / dV MMAs run u8 x s8.  Halves P^'s
                               rounding step at no cost: lower O and dV error vs full precision. */
-  SAGE_QK_NORM = 1u << 4   /* QK-norm in front of the path: use
+  SAGE_QK_NORM = 1u << 4,  /* QK-norm in front of the path: use
                               sage_fwd_qknorm / sage_bwd_qknorm (sage_fwd / sage_bwd reject it) */
+  SAGE_DETERMINISTIC = 1u << 5 /* bitwise run-to-run reproducible dQ (reading A19; NEXT-4): the fp32
+                              dQ reduction across key blocks happens in a fixed order, enforced by
+                              per-(head, query block) flags in the workspace.  Slower backward.
+                              Non-causal requires N/128 <= the device's SM count
+                              (SAGE_ERR_UNSUPPORTED otherwise).  Every other output is always
+                              deterministic. */
 };
 
 typedef struct {

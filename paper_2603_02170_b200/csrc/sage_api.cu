@@ -66,7 +66,7 @@ size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Dims {
   size_t BH, N, d, T;
-  bool causal, ks, qs, pu8, qkn;
+  bool causal, ks, qs, pu8, qkn, det;
   float tau;
 };
 
@@ -75,7 +75,8 @@ bool dims_of(const sage_params* p, Dims* o) {
   if (p->batch <= 0 || p->heads <= 0 || p->seqlen <= 0) return false;
   if (p->head_dim != 64 && p->head_dim != 128) return false;
   if (p->seqlen % kBlk || p->seqlen > kMaxSeqLen) return false;
-  if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH | SAGE_P_U8 | SAGE_QK_NORM)) return false;
+  if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH | SAGE_P_U8 | SAGE_QK_NORM | SAGE_DETERMINISTIC))
+    return false;
   if (!(p->softmax_scale >= 0.f) || std::isinf(p->softmax_scale)) return false;
   const size_t BH = (size_t)p->batch * p->heads;
   if (BH * p->seqlen > (size_t)INT32_MAX / 2) return false;  // TMA row coordinates are int32
@@ -88,6 +89,7 @@ bool dims_of(const sage_params* p, Dims* o) {
   o->qs = p->flags & SAGE_Q_SMOOTH;
   o->pu8 = p->flags & SAGE_P_U8;
   o->qkn = p->flags & SAGE_QK_NORM;
+  o->det = p->flags & SAGE_DETERMINISTIC;
   o->tau = p->softmax_scale > 0.f ? p->softmax_scale : 1.f / std::sqrt((float)p->head_dim);
   return true;
 }
@@ -127,7 +129,7 @@ FwdWs fwd_ws(const Dims& D) {
 }
 // bwd ws: do_i8, do_scale, delta, l2, dq_acc
 struct BwdWs {
-  size_t do8, sdo, delta, l2, dq, gq, gk, total;
+  size_t do8, sdo, delta, l2, dq, gq, gk, flags, total;
 };
 BwdWs bwd_ws(const Dims& D) {
   BwdWs W{};
@@ -141,6 +143,7 @@ BwdWs bwd_ws(const Dims& D) {
   const size_t gbytes = D.BH * D.T * D.d * 4 + 8 + (D.BH * D.T + 63) / 64 * D.d * 8;
   W.gq = off; off += D.qkn ? up(gbytes) : 0;
   W.gk = off; off += D.qkn ? up(gbytes) : 0;
+  W.flags = off; off += D.det ? up(D.BH * D.T * 4 * 4) : 0;  // SAGE_DETERMINISTIC dQ ordering flags
   W.total = off;
   return W;
 }
@@ -413,6 +416,13 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
   if (ctx_bytes < C.total || ws_bytes < W.total) return SAGE_ERR_WORKSPACE;
   sage_status st = check_arch();
   if (st != SAGE_OK) return st;
+  if (D.det && !D.causal) {
+    // the rotated non-causal order needs all T key-block CTAs of a head resident at once
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return cuda_fail(cudaErrorInvalidValue);
+    if ((int)D.T > sms) return SAGE_ERR_UNSUPPORTED;
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int BH = (int)D.BH, N = (int)D.N, d = (int)D.d;
   void* cx = const_cast<void*>(ctx);
@@ -429,8 +439,9 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
     return cuda_fail(cudaErrorInvalidValue);
   cudaError_t e;
   // K3: delta, psi(dO), L*log2(e), zero dQ accumulator (Alg. 2 lines 2, 6)
+  unsigned* dqflags = D.det ? at<unsigned>(ws, W.flags) : nullptr;
   if ((e = launch_bwd_prep(static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dO), lse, delta,
-                           l2, do8, sdo, dqacc, BH, N, d, s)) != cudaSuccess)
+                           l2, do8, sdo, dqacc, BH, N, d, s, dqflags)) != cudaSuccess)
     return cuda_fail(e);
   // K4: fused INT8 backward (Alg. 2 lines 3-11)
   a.q_scale = sq;
@@ -450,6 +461,7 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
   a.causal = D.causal;
   a.qsmooth = D.qs;
   a.pu8 = D.pu8;
+  a.dq_flags = dqflags;
   a.ablate = ablate_flags() | (g_dump_heads > 0 ? 16 : 0);
   if ((e = timed(1, s, [&] { return launch_bwd(a, s); })) != cudaSuccess) return cuda_fail(e);
   if (g_prof.on) g_prof.launches += 2;  // K3, K4

@@ -116,7 +116,7 @@ __device__ __forceinline__ float compute_max(float v, int* red, int cw, int id) 
   return ford_inv(max(max(max(a.x, a.y), max(a.z, a.w)), max(max(b.x, b.y), max(b.z, b.w))));
 }
 
-template <int D, bool CAUSAL, bool QSMOOTH>
+template <int D, bool CAUSAL, bool QSMOOTH, bool DET>
 __global__ void __launch_bounds__(kThreads, 1)
     sage_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_doq, const __grid_constant__ CUtensorMap tm_v,
@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* __restrict__ k_scale, const float* __restrict__ do_scale,
                     const float* __restrict__ l2g, const float* __restrict__ deltag, const float* __restrict__ bias,
                     const float* __restrict__ mu_q, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dk,
-                    __nv_bfloat16* __restrict__ dv, int N, int BH, float tau, int pu8, int ablate_arg) {
+                    __nv_bfloat16* __restrict__ dv, int N, int BH, float tau, int pu8, unsigned* __restrict__ dq_flags,
+                    int ablate_arg) {
   const int ablate = SAGE_TRACE ? ablate_arg : 0;
   // psi(P) levels (Alg. 2 line 6): 127, or 255 for the unsigned P^ variant (SAGE_P_U8)
   const float pmax = pu8 ? 255.f : 127.f;
@@ -172,9 +173,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   // head-major order: the T CTAs of one head run together and share its Q^/dO/dO^ tiles and
   // its dQ accumulator through L2; within a head, low j (most query blocks when causal) first.
   const int bh = tile / T;
-  const int j = tile % T;
+  // SAGE_DETERMINISTIC (dq_flags != null): dQ_i receives its key-block contributions in a fixed order,
+  // enforced with per-(head, i, drain warp) flags.  Causal: descending j (j = i first), so the CTAs
+  // launch high j first and every CTA only waits on CTAs launched before it.  Non-causal: CTA j
+  // visits the query blocks rotated, i = (j + it) mod T, and dQ_i's contributions come in iteration
+  // order; all T CTAs of a head are co-resident (the API requires T <= SM count).
+  constexpr bool det = DET;  // (a template parameter: the flag logic costs ~2% when compiled in)
+  const int j = (det && CAUSAL) ? T - 1 - tile % T : tile % T;
   const int i0 = CAUSAL ? j : 0;
   const int n_it = T - i0;
+  auto i_of = [&](int it) { return (det && !CAUSAL) ? (j + it) % T : i0 + it; };
   const int krow = bh * N + j * kBlk;
 
   if (threadIdx.x == 0) {
@@ -236,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
       for (int it = 0; it < n_it; ++it) {
-        const int s = it % kStages, i = i0 + it;
+        const int s = it % kStages, i = i_of(it);
         const int qrow = bh * N + i * kBlk;
         uint8_t* st = smem + L::kStage + s * L::kStageBytes;
         mbar_wait(q_empty + s, ((it / kStages) & 1) ^ 1);
@@ -428,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     for (int it = 0; it < n_it; ++it) {
-      const int i = i0 + it, s = it % kStages;
+      const int i = i_of(it), s = it % kStages;
       const uint32_t ph = it & 1, pph = ph ^ 1;
       const uint8_t* st = smem + L::kStage + s * L::kStageBytes;
       const float4* Ls4 = reinterpret_cast<const float4*>(st + L::kSL) + qc0 / 4;
@@ -647,7 +655,7 @@ if (cm) {
     for (int c = 0; c < kRegV; ++c) dv_acc[c] = 0.f;
 
     for (int it = 0; it < n_it; ++it) {
-      const int i = i0 + it;
+      const int i = i_of(it);
       const uint32_t ph = it & 1;
       const float sq = sc_q[i];
       const float sdo = sc_do[i];
@@ -726,6 +734,11 @@ if (cm) {
         const float s_ds = __fdiv_rn(scl[(it & 3) * 2 + 1], 127.f);
         const float2 f = make_float2(s_ds * sk * tau, s_ds * sk * tau);
         uint8_t* wstage = smem + L::kDq + (warp % 4) * L::kDqWarp;
+        unsigned* flag = det ? dq_flags + ((size_t)bh * T + i) * kDrainWarps + (warp % 4) : nullptr;
+        if (det) {  // wait for the contributions ordered before this one: (i - j) mod T of them
+          if (lane == 0) flag_wait_geq(flag, (unsigned)((i - j + T) % T));
+          __syncwarp();
+        }
 #pragma unroll
         for (int qq = 0; qq < L::kDqRounds; ++qq) {
           const int rnd = it * L::kDqRounds + qq;
@@ -757,6 +770,13 @@ if (cm) {
                                 bh * N + i * kBlk + (warp % 4) * 32);
             bulk_commit();
           }
+        }
+        if (det) {  // this contribution complete in L2, then pass the turn on
+          if (lane == 0) {
+            bulk_wait_all();
+            flag_release_add(flag);
+          }
+          __syncwarp();
         }
       }
       tc_fence_before();
@@ -809,16 +829,16 @@ if (cm) {
   }
 }
 
-template <int D, bool C, bool QS>
+template <int D, bool C, bool QS, bool DET>
 cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
-  auto kern = sage_bwd_kernel<D, C, QS>;
+  auto kern = sage_bwd_kernel<D, C, QS, DET>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem<D>::kAlloc);
   if (e != cudaSuccess) return e;
   const int T = a.N / kBlk;
   kern<<<a.BH * T, kThreads, BwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_doq, a.tm_v, a.tm_do, a.tm_dq, a.q_scale,
                                                        a.k_scale, a.do_scale, a.l2, a.delta, a.bias, a.mu_q,
                                                        a.dq_acc, a.dk, a.dv, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
-                                                       a.ablate);
+                                                       a.dq_flags, a.ablate);
   return cudaGetLastError();
 }
 
@@ -831,13 +851,16 @@ cudaError_t read_bwd_trace(void* host, size_t bytes) {
   return cudaMemcpyFromSymbol(host, g_trace, bytes);
 }
 
+template <int D, bool DET>
+cudaError_t launch_d(const BwdArgs& a, cudaStream_t s) {
+  if (a.causal) return a.qsmooth ? launch_t<D, true, true, DET>(a, s) : launch_t<D, true, false, DET>(a, s);
+  return a.qsmooth ? launch_t<D, false, true, DET>(a, s) : launch_t<D, false, false, DET>(a, s);
+}
+
 cudaError_t launch_bwd(const BwdArgs& a, cudaStream_t s) {
-  if (a.d == 128) {
-    if (a.causal) return a.qsmooth ? launch_t<128, true, true>(a, s) : launch_t<128, true, false>(a, s);
-    return a.qsmooth ? launch_t<128, false, true>(a, s) : launch_t<128, false, false>(a, s);
-  }
-  if (a.causal) return a.qsmooth ? launch_t<64, true, true>(a, s) : launch_t<64, true, false>(a, s);
-  return a.qsmooth ? launch_t<64, false, true>(a, s) : launch_t<64, false, false>(a, s);
+  const bool det = a.dq_flags != nullptr;
+  if (a.d == 128) return det ? launch_d<128, true>(a, s) : launch_d<128, false>(a, s);
+  return det ? launch_d<64, true>(a, s) : launch_d<64, false>(a, s);
 }
 
 }  // namespace sage

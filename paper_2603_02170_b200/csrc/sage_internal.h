@@ -57,7 +57,7 @@ cudaError_t launch_qsmooth_bias(const __nv_bfloat16* k, const float* mu_k, const
 //     dq_acc = 0.
 cudaError_t launch_bwd_prep(const __nv_bfloat16* o, const __nv_bfloat16* dO, const float* lse, float* delta,
                             float* l2, int8_t* do_q, float* do_scale, float* dq_acc, int BH, int N, int d,
-                            cudaStream_t s);
+                            cudaStream_t s, unsigned* dq_flags = nullptr);
 cudaError_t launch_fill(float* x, size_t n, float v, cudaStream_t s);
 // K5: dQ fp32 -> bf16.
 cudaError_t launch_dq_finalize(const float* dq_acc, __nv_bfloat16* dq, size_t n, cudaStream_t s);
@@ -92,6 +92,7 @@ struct BwdArgs {
   float tau;
   bool causal, qsmooth;
   bool pu8;    // SAGE_P_U8: psi(P) in 0..255 (u8 x s8 dV)
+  unsigned* dq_flags;  // SAGE_DETERMINISTIC: [BH][T][4] zeroed ordering flags, or null
   int ablate;  // profiling only (SAGE_ABLATE): 1 drain math off, 2 compute math off, 4 dQ reduction off
 };
 cudaError_t launch_bwd(const BwdArgs& a, cudaStream_t s);

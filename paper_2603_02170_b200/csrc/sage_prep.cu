@@ -315,7 +315,8 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
                                                        const __nv_bfloat16* __restrict__ dO,
                                                        const float* __restrict__ lse, float* __restrict__ delta,
                                                        float* __restrict__ l2, int8_t* __restrict__ do_q,
-                                                       float* __restrict__ do_scale, float* __restrict__ dq_acc) {
+                                                       float* __restrict__ do_scale, float* __restrict__ dq_acc,
+                                                       unsigned* __restrict__ dq_flags) {
   constexpr int kGroups = D / kVec;            // threads per row
   constexpr int kRowsPerPass = 256 / kGroups;
   constexpr int kIters = kBlk / kRowsPerPass;
@@ -357,6 +358,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
   const float sc = __fdiv_rn(amax, 127.f);
   const float inv = amax > 0.f ? __fdiv_rn(127.f, amax) : 0.f;
   if (threadIdx.x == 0) do_scale[blk] = sc;
+  if (dq_flags && threadIdx.x < 4) dq_flags[blk * 4 + threadIdx.x] = 0u;  // SAGE_DETERMINISTIC flags
 #pragma unroll
   for (int it = 0; it < kIters; ++it) {
     const int r = r0 + it * kRowsPerPass;
@@ -578,12 +580,12 @@ cudaError_t launch_qsmooth_bias(const __nv_bfloat16* k, const float* mu_k, const
 
 cudaError_t launch_bwd_prep(const __nv_bfloat16* o, const __nv_bfloat16* dO, const float* lse, float* delta,
                             float* l2, int8_t* do_q, float* do_scale, float* dq_acc, int BH, int N, int d,
-                            cudaStream_t s) {
+                            cudaStream_t s, unsigned* dq_flags) {
   unsigned grid = (unsigned)(BH * (N / kBlk));
   if (d == 128)
-    bwd_prep_kernel<128><<<grid, 256, 0, s>>>(o, dO, lse, delta, l2, do_q, do_scale, dq_acc);
+    bwd_prep_kernel<128><<<grid, 256, 0, s>>>(o, dO, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
   else
-    bwd_prep_kernel<64><<<grid, 256, 0, s>>>(o, dO, lse, delta, l2, do_q, do_scale, dq_acc);
+    bwd_prep_kernel<64><<<grid, 256, 0, s>>>(o, dO, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
   return cudaGetLastError();
 }
 

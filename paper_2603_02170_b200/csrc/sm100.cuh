@@ -130,6 +130,24 @@ __device__ __forceinline__ void bulk_wait_read() {  // <= N groups may still be 
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// Inter-CTA ordering flags (SAGE_DETERMINISTIC dQ): acquire / release on a global u32 counter, with
+// async-proxy fences so that the TMA reduces issued after the acquire, and those completed before
+// the release, are ordered with the flag.
+__device__ __forceinline__ void flag_wait_geq(const unsigned* f, unsigned v) {
+  unsigned x, n = 0;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(f) : "memory");
+    if (x >= v) break;
+    __nanosleep(64);
+    if (++n == (1u << 25)) __trap();  // a lost predecessor: fail loudly instead of hanging
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void flag_release_add(unsigned* f) {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(f) : "memory");
+}
+
 // ----------------------------------------------------------------- TMEM
 // One full warp allocates `ncols` (power of two >= 32) columns; address written to *dst.
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {

@@ -27,10 +27,11 @@ def _gpu():
     oracle.build()
 
 
-def _run(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False):
+def _run(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, deterministic=False):
     dev = "cuda"
     qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
-    o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8)
+    o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8,
+                               deterministic=deterministic)
     dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
     torch.cuda.synchronize()
     return dict(o=o, lse=lse, dq=dq, dk=dk, dv=dv, ctx=ctx)
@@ -189,6 +190,40 @@ def test_fwd_bwd_parity_p_u8(B, H, N, d, causal, ks, qs, recipe):
     heads = list(range(B * H))
     f, b = _oracle(q, k, v, do, heads, causal, ks, qs, p_u8=True)
     _assert_ok(_compare(gpu, f, b, heads, B, H, N, d), (B, H, N, d, causal, ks, qs, recipe, "u8"))
+
+
+DET_CASES = [
+    (1, 2, 512, 64, True, False),
+    (1, 2, 384, 128, False, False),
+    (1, 2, 384, 128, True, True),
+]
+
+
+@pytest.mark.parametrize("B,H,N,d,causal,qs", DET_CASES)
+def test_deterministic_parity_and_repeatability(B, H, N, d, causal, qs):
+    """SAGE_DETERMINISTIC (reading A19): three runs give bitwise identical O, dQ, dK, dV, and the
+    result meets the same tolerance against the oracle."""
+    q, k, v, do = make_inputs(B, H, N, d, "outlier_kq" if qs else "qknorm", seed=600 + N + d)
+    runs = [_run(q, k, v, do, causal, True, qs, deterministic=True) for _ in range(3)]
+    for r in runs[1:]:
+        for name in ("o", "dq", "dk", "dv"):
+            assert torch.equal(runs[0][name], r[name]), name
+    heads = list(range(B * H))
+    f, b = _oracle(q, k, v, do, heads, causal, True, qs)
+    _assert_ok(_compare(runs[0], f, b, heads, B, H, N, d), ("det", B, H, N, d, causal, qs))
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_deterministic_full_size_repeatable(cfg):
+    """At the bench shapes (every CTA of a head racing for the same dQ rows) the deterministic dQ
+    is bitwise identical across runs, and equal to the default path within the tolerance."""
+    c = CONFIGS[cfg]
+    q, k, v, do = make_inputs(c.batch, c.heads, c.seqlen, c.head_dim, c.recipe, seed=c.seed)
+    r1 = _run(q, k, v, do, c.causal, c.k_smooth, c.q_smooth, deterministic=True)
+    r2 = _run(q, k, v, do, c.causal, c.k_smooth, c.q_smooth, deterministic=True)
+    assert torch.equal(r1["dq"], r2["dq"]) and torch.equal(r1["dk"], r2["dk"]) and torch.equal(r1["dv"], r2["dv"])
+    r0 = _run(q, k, v, do, c.causal, c.k_smooth, c.q_smooth)
+    assert rel_l2(f64(r0["dq"]), f64(r1["dq"])) < 1e-3
 
 
 def test_zero_do_gives_zero_grads():
