@@ -38,6 +38,8 @@
 #define ORC_QUANT_OFF 8   /* psi = identity, no FP32 emulation: tiled full-precision attention */
 #define ORC_P_U8     16   /* unsigned 8-bit P^ (0..255, scale max/255) instead of 0..127: the
                              u8 x s8 variant; psi(dS), psi(Q/K/V/dO) unchanged */
+#define ORC_P_COL    32   /* backward psi(P) per key column of the tile instead of per tile (the dV half
+                             of SURVEY.md 8(f) NEXT-2): dV_j += (P^^T dO^_i) with one scale per key */
 
 void oracle_set_threads(int n) {
 #ifdef _OPENMP
@@ -365,6 +367,9 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
   double *dS = malloc(bb * sizeof(double)), *Px = malloc(bb * sizeof(double)), *dSx = malloc(bb * sizeof(double));
   int8_t *dS8 = malloc(bb);
   double pmax = (flags & ORC_P_U8) ? 255.0 : 127.0;
+  int pcol = (flags & ORC_P_COL) != 0;
+  double *spcol = malloc(blk * sizeof(double));
+  double *colx = malloc(blk * sizeof(double)), *colq = malloc(blk * sizeof(double));
   memset(dq, 0, nd * sizeof(double));
   memset(dk, 0, nd * sizeof(double));
   memset(dv, 0, nd * sizeof(double));
@@ -380,7 +385,19 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
         }
       /* line 6: psi(P_ij) over the whole B_q x B_kv tile (A11). */
       double sp;
-      psi_block(P, (int)bb, 0, qo, pmax, NULL, &sp, Px);  /* Px: the integer P^ (0..pmax) */
+      if (pcol && !qo) {
+        /* psi over each key column n of the tile: s_P[n] = fl32(max_r P[r,n] / pmax) */
+        sp = 0.0;
+        for (int n = 0; n < blk; ++n) {
+          for (int r = 0; r < blk; ++r) colx[r] = P[(size_t)r * blk + n];
+          psi_block(colx, blk, 0, 0, pmax, NULL, &spcol[n], colq);
+          for (int r = 0; r < blk; ++r) Px[(size_t)r * blk + n] = colq[r];
+          if (spcol[n] > sp) sp = spcol[n];
+        }
+      } else {
+        psi_block(P, (int)bb, 0, qo, pmax, NULL, &sp, Px);  /* Px: the integer P^ (0..pmax) */
+        for (int n = 0; n < blk; ++n) spcol[n] = sp;
+      }
       /* line 7: dV_j += MM(P^_ij^T, dO^_i) x s_P x s_dO. */
       for (int n = 0; n < blk; ++n)
         for (int c = 0; c < d; ++c) {
@@ -393,7 +410,7 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
             int32_t a = 0;
             for (int r = 0; r < blk; ++r)
               a += (int32_t)Px[(size_t)r * blk + n] * (int32_t)do8[(size_t)(i * blk + r) * d + c];
-            val = (double)a * sp * sdo[i];
+            val = (double)a * spcol[n] * sdo[i];
           }
           dv[(size_t)(j * blk + n) * d + c] += val;
         }
@@ -460,7 +477,7 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
   if (do8_out) memcpy(do8_out, do8, nd);
   if (sdo_out) for (int t = 0; t < T; ++t) sdo_out[t] = (float)sdo[t];
   free(delta); free(dox); free(do8); free(sdo); free(S); free(P); free(dS); free(Px); free(dSx);
-  free(dS8);
+  free(dS8); free(spcol); free(colx); free(colq);
   prep_free(&h);
 }
 

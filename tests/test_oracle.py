@@ -394,3 +394,22 @@ def test_qknorm_backward_finite_differences(orc):
         fdx[idx] = (loss(x + e, g) - loss(x - e, g)) / (2 * h)
     fdg = np.array([(loss(x, g + h * np.eye(16)[c]) - loss(x, g - h * np.eye(16)[c])) / (2 * h) for c in range(16)])
     assert rel_l2(fdx, dx) < 1e-7 and rel_l2(fdg, dg) < 1e-7
+
+
+def test_p_col_variant(orc):
+    """Backward psi(P) per key column of the tile (ORC_P_COL, the dV half of SURVEY.md 8(f) NEXT-2):
+    every key column of every processed tile attains the full 0..127 range, the forward is untouched,
+    and dV's error against FPA drops well below the per-tile reading's (A11) at sigma = 1, the
+    Table 1 row where the per-tile psi(P) leaves dV ~3.5x above the paper."""
+    q, k, v, do = (f64(t).reshape(1, 512, 64) for t in make_inputs(1, 1, 512, 64, "gauss", seed=33, sigma=1.0))
+    ref = orc.fpa(q, k, v, do)
+    f = orc.fwd(q, k, v)
+    errs = {}
+    for pc in (False, True):
+        b = orc.bwd(q, k, v, f["o"], do, f["lse"], p_col=pc, tiles=True)
+        errs[pc] = {n: rel_l2(ref[n], b[n]) for n in ("dq", "dk", "dv")}
+        if pc:
+            p8 = b["p8"][0].reshape(4, 128, 4, 128)
+            assert np.all(p8.max(axis=1) == 127)  # max over the queries of each key column, every tile
+    assert errs[True]["dv"] < 0.5 * errs[False]["dv"], errs
+    assert errs[True]["dq"] == errs[False]["dq"] and errs[True]["dk"] == errs[False]["dk"], errs
