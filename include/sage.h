@@ -67,12 +67,17 @@ enum {
                               rounding step at no cost: lower O and dV error vs full precision. */
   SAGE_QK_NORM = 1u << 4,  /* QK-norm in front of the path: use
                               sage_fwd_qknorm / sage_bwd_qknorm (sage_fwd / sage_bwd reject it) */
-  SAGE_DETERMINISTIC = 1u << 5 /* bitwise run-to-run reproducible dQ (reading A19; NEXT-4): the fp32
+  SAGE_DETERMINISTIC = 1u << 5, /* bitwise run-to-run reproducible dQ (reading A19; NEXT-4): the fp32
                               dQ reduction across key blocks happens in a fixed order, enforced by
                               per-(head, query block) flags in the workspace.  Slower backward.
                               Non-causal requires N/128 <= the device's SM count
                               (SAGE_ERR_UNSUPPORTED otherwise).  Every other output is always
                               deterministic. */
+  SAGE_P_COLSCALE = 1u << 6 /* variant (the dV half of SURVEY.md 8(f) NEXT-2): the backward's psi(P)
+                              (Alg. 2 line 6) takes one scale per key of the tile (the max over its
+                              128 queries) instead of one per tile; dV_j's drain applies it per row.
+                              dV's error vs full precision drops ~2.6x at Table 1's sigma = 1.
+                              Not combinable with SAGE_DETERMINISTIC (SAGE_ERR_INVALID_VALUE). */
 };
 
 typedef struct {

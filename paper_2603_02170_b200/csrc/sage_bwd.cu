@@ -57,7 +57,9 @@ struct BwdSmem {
   static constexpr int kRed = kDSt + kBlk * kBlk;             // [2][8] floats (cross-warp max)
   static constexpr int kScl = kRed + 64;                      // [4][2] floats {s_P, s_dS} per tile slot
   static constexpr int kRowSum = kScl + 32;                   // [2 slots][2 wg][128] int (Q-smoothing colsum of dS^)
-  static constexpr int kScQ = kRowSum + 4 * kBlk * 4;          // s_Q[bh][0..T), s_dO[bh][0..T) (T <= kMaxT)
+  static constexpr int kRowX = kRowSum + 4 * kBlk * 4;         // [2 wg][128] per-row P maxima (SAGE_P_COLSCALE)
+  static constexpr int kSpRow = kRowX + 2 * kBlk * 4;          // [4 slots][128] per-key psi(P) maxima for the drain
+  static constexpr int kScQ = kSpRow + 4 * kBlk * 4;           // s_Q[bh][0..T), s_dO[bh][0..T) (T <= kMaxT)
   static constexpr int kScDO = kScQ + kMaxT * 4;
   // dQ staging for the TMA reduce-add, per drain warp (its 32 TMEM lanes = 32 query rows):
   // 2 buffers of [kDqBoxes][32 rows][32 cols] fp32 boxes, 128B-swizzled; d=64 stages the warp's
@@ -116,7 +118,9 @@ __device__ __forceinline__ float compute_max(float v, int* red, int cw, int id) 
   return ford_inv(max(max(max(a.x, a.y), max(a.z, a.w)), max(max(b.x, b.y), max(b.z, b.w))));
 }
 
-template <int D, bool CAUSAL, bool QSMOOTH, bool DET>
+// VAR: 0 the default path, 1 SAGE_DETERMINISTIC, 2 SAGE_P_COLSCALE -- separate instantiations, because
+// compiling the variants' logic into the default kernel costs 2-8% (measured)
+template <int D, bool CAUSAL, bool QSMOOTH, int VAR>
 __global__ void __launch_bounds__(kThreads, 1)
     sage_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_doq, const __grid_constant__ CUtensorMap tm_v,
@@ -125,8 +129,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* __restrict__ k_scale, const float* __restrict__ do_scale,
                     const float* __restrict__ l2g, const float* __restrict__ deltag, const float* __restrict__ bias,
                     const float* __restrict__ mu_q, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dk,
-                    __nv_bfloat16* __restrict__ dv, int N, int BH, float tau, int pu8, unsigned* __restrict__ dq_flags,
-                    int ablate_arg) {
+                    __nv_bfloat16* __restrict__ dv, int N, int BH, float tau, int pu8,
+                    unsigned* __restrict__ dq_flags, int ablate_arg) {
+  constexpr bool pcol = VAR == 2;
   const int ablate = SAGE_TRACE ? ablate_arg : 0;
   // psi(P) levels (Alg. 2 line 6): 127, or 255 for the unsigned P^ variant (SAGE_P_U8)
   const float pmax = pu8 ? 255.f : 127.f;
@@ -166,6 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* sc_q = reinterpret_cast<float*>(smem + L::kScQ);
   float* sc_do = reinterpret_cast<float*>(smem + L::kScDO);
   int* rowsum_s = reinterpret_cast<int*>(smem + L::kRowSum);
+  float* rowx = reinterpret_cast<float*>(smem + L::kRowX);
+  float* sp_row = reinterpret_cast<float*>(smem + L::kSpRow);
 
   const int T = N / kBlk;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -178,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // launch high j first and every CTA only waits on CTAs launched before it.  Non-causal: CTA j
   // visits the query blocks rotated, i = (j + it) mod T, and dQ_i's contributions come in iteration
   // order; all T CTAs of a head are co-resident (the API requires T <= SM count).
-  constexpr bool det = DET;  // (a template parameter: the flag logic costs ~2% when compiled in)
+  constexpr bool det = VAR == 1;
   const int j = (det && CAUSAL) ? T - 1 - tile % T : tile % T;
   const int i0 = CAUSAL ? j : 0;
   const int n_it = T - i0;
@@ -495,7 +502,17 @@ if (cm) {
 
       // -- step 2: psi(P) scale over the tile: amax = max P = 2^max(t)  (line 6, reading A11)
       if (threadIdx.x == 128) TR(19, it);
-      const float amax_p = ex2(compute_max(tmax, red, cw, 1));
+      // SAGE_P_COLSCALE: one scale per key row r of P^T (a key column of P, the dV contraction's free
+      // index), the max over this tile's 128 queries: this thread's 64 and the other warpgroup's 64
+      float amax_p;
+      if constexpr (pcol) {
+        rowx[wg * kBlk + r] = tmax;
+        named_bar_sync(1, 256);
+        amax_p = ex2(fmaxf(tmax, rowx[(wg ^ 1) * kBlk + r]));
+        if (wg == 0) sp_row[(it & 3) * kBlk + r] = amax_p;
+      } else {
+        amax_p = ex2(compute_max(tmax, red, cw, 1));
+      }
       if (threadIdx.x == 128) TR(21, it);
       // inv = 127/amax via the correctly rounded reciprocal (within 1 ulp of fl32(127/amax); P^ is
       // Tier C); the exact s_P = fl32(amax/127) is formed by the drain off this path
@@ -666,7 +683,8 @@ if (cm) {
         tc_fence_after();
         if (threadIdx.x == 384) TR(10, it);
         if (!(ablate & 1)) {
-          const float s_p = __fdiv_rn(scl[(it & 3) * 2], pmax);  // psi(P) scale = fl32(amax/127)
+          // psi(P) scale = fl32(amax/127): the tile's, or this key row's (SAGE_P_COLSCALE)
+          const float s_p = __fdiv_rn(pcol ? sp_row[(it & 3) * kBlk + r] : scl[(it & 3) * 2], pmax);
           const float2 f = make_float2(s_p * sdo, s_p * sdo);
 #pragma unroll
           for (int c0 = 0; c0 < D; c0 += 32) {
@@ -829,9 +847,9 @@ if (cm) {
   }
 }
 
-template <int D, bool C, bool QS, bool DET>
+template <int D, bool C, bool QS, int VAR>
 cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
-  auto kern = sage_bwd_kernel<D, C, QS, DET>;
+  auto kern = sage_bwd_kernel<D, C, QS, VAR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem<D>::kAlloc);
   if (e != cudaSuccess) return e;
   const int T = a.N / kBlk;
@@ -851,16 +869,20 @@ cudaError_t read_bwd_trace(void* host, size_t bytes) {
   return cudaMemcpyFromSymbol(host, g_trace, bytes);
 }
 
-template <int D, bool DET>
+template <int D, int VAR>
 cudaError_t launch_d(const BwdArgs& a, cudaStream_t s) {
-  if (a.causal) return a.qsmooth ? launch_t<D, true, true, DET>(a, s) : launch_t<D, true, false, DET>(a, s);
-  return a.qsmooth ? launch_t<D, false, true, DET>(a, s) : launch_t<D, false, false, DET>(a, s);
+  if (a.causal) return a.qsmooth ? launch_t<D, true, true, VAR>(a, s) : launch_t<D, true, false, VAR>(a, s);
+  return a.qsmooth ? launch_t<D, false, true, VAR>(a, s) : launch_t<D, false, false, VAR>(a, s);
+}
+
+template <int D>
+cudaError_t launch_v(const BwdArgs& a, cudaStream_t s) {
+  if (a.dq_flags != nullptr) return launch_d<D, 1>(a, s);  // the API rejects det + colscale
+  return a.pcol ? launch_d<D, 2>(a, s) : launch_d<D, 0>(a, s);
 }
 
 cudaError_t launch_bwd(const BwdArgs& a, cudaStream_t s) {
-  const bool det = a.dq_flags != nullptr;
-  if (a.d == 128) return det ? launch_d<128, true>(a, s) : launch_d<128, false>(a, s);
-  return det ? launch_d<64, true>(a, s) : launch_d<64, false>(a, s);
+  return a.d == 128 ? launch_v<128>(a, s) : launch_v<64>(a, s);
 }
 
 }  // namespace sage

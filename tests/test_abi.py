@@ -66,6 +66,9 @@ def test_error_paths_do_not_launch(L):
     assert L.sage_bwd(ctypes.byref(p), A, A, A, A, A, S(nctx), A, A, mis, A, S(nwb), z) == 3
     assert L.sage_debug_umma(8, 64, 128, A, A, A, z) == 1
     assert L.sage_debug_umma(1, 128, 96, A, A, A, z) == 1
+    # one backward variant at a time: SAGE_DETERMINISTIC with SAGE_P_COLSCALE is rejected
+    assert L.sage_ctx_bytes(ctypes.byref(make_params(1, 2, 256, 64, deterministic=True, p_colscale=True))) == 0
+    assert L.sage_ctx_bytes(ctypes.byref(make_params(1, 2, 256, 64, p_colscale=True))) == nctx
     # QK-norm params need the _qknorm entry points, which need gamma and eps > 0
     pn = make_params(1, 2, 256, 64, qk_norm=True)
     ncn = L.sage_ctx_bytes(ctypes.byref(pn))

@@ -27,17 +27,17 @@ def _gpu():
     oracle.build()
 
 
-def _run(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, deterministic=False):
+def _run(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, deterministic=False, p_colscale=False):
     dev = "cuda"
     qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
     o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8,
-                               deterministic=deterministic)
+                               deterministic=deterministic, p_colscale=p_colscale)
     dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
     torch.cuda.synchronize()
     return dict(o=o, lse=lse, dq=dq, dk=dk, dv=dv, ctx=ctx)
 
 
-def _oracle(q, k, v, do, heads, causal, k_smooth, q_smooth, p_u8=False):
+def _oracle(q, k, v, do, heads, causal, k_smooth, q_smooth, p_u8=False, p_col=False):
     """Oracle on the selected flattened heads; O is stored as bf16 before the backward (A15)."""
     B, H, N, d = q.shape
     sel = lambda t: f64(t).reshape(B * H, N, d)[heads]
@@ -45,7 +45,7 @@ def _oracle(q, k, v, do, heads, causal, k_smooth, q_smooth, p_u8=False):
     kw = dict(causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8)
     f = oracle.fwd(qn, kn, vn, **kw)
     o_st = round_bf16(f["o"])
-    b = oracle.bwd(qn, kn, vn, o_st, don, f["lse"], **kw)
+    b = oracle.bwd(qn, kn, vn, o_st, don, f["lse"], p_col=p_col, **kw)
     return f, b
 
 
@@ -190,6 +190,25 @@ def test_fwd_bwd_parity_p_u8(B, H, N, d, causal, ks, qs, recipe):
     heads = list(range(B * H))
     f, b = _oracle(q, k, v, do, heads, causal, ks, qs, p_u8=True)
     _assert_ok(_compare(gpu, f, b, heads, B, H, N, d), (B, H, N, d, causal, ks, qs, recipe, "u8"))
+
+
+PCOL_CASES = [
+    (1, 2, 384, 64, True, False, False, "gauss"),
+    (1, 2, 256, 128, False, False, False, "qknorm"),
+    (1, 2, 384, 128, True, True, True, "outlier_kq"),
+    (2, 1, 256, 64, False, True, False, "qknorm"),
+]
+
+
+@pytest.mark.parametrize("B,H,N,d,causal,qs,u8,recipe", PCOL_CASES)
+def test_fwd_bwd_parity_p_colscale(B, H, N, d, causal, qs, u8, recipe):
+    """SAGE_P_COLSCALE (per-key psi(P) in the backward) against the oracle's ORC_P_COL mode, also
+    combined with SAGE_P_U8."""
+    q, k, v, do = make_inputs(B, H, N, d, recipe, seed=700 + N + d)
+    gpu = _run(q, k, v, do, causal, True, qs, p_u8=u8, p_colscale=True)
+    heads = list(range(B * H))
+    f, b = _oracle(q, k, v, do, heads, causal, True, qs, p_u8=u8, p_col=True)
+    _assert_ok(_compare(gpu, f, b, heads, B, H, N, d), ("pcol", B, H, N, d, causal, qs, u8, recipe))
 
 
 DET_CASES = [
