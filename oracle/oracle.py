@@ -9,7 +9,7 @@ import subprocess
 
 import numpy as np
 
-CAUSAL, K_SMOOTH, Q_SMOOTH, QUANT_OFF, P_U8, P_COL = 1, 2, 4, 8, 16, 32
+CAUSAL, K_SMOOTH, Q_SMOOTH, QUANT_OFF, P_U8, P_COL, DS_FINE = 1, 2, 4, 8, 16, 32, 64
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sage_oracle.c")
@@ -83,9 +83,9 @@ def _default_tau(d, tau):
     return 1.0 / np.sqrt(d) if tau is None else float(tau)
 
 
-def _flags(causal, k_smooth, q_smooth, quant, p_u8, p_col=False):
+def _flags(causal, k_smooth, q_smooth, quant, p_u8, p_col=False, ds_fine=False):
     return (CAUSAL if causal else 0) | (K_SMOOTH if k_smooth else 0) | (Q_SMOOTH if q_smooth else 0) | \
-        (0 if quant else QUANT_OFF) | (P_U8 if p_u8 else 0) | (P_COL if p_col else 0)
+        (0 if quant else QUANT_OFF) | (P_U8 if p_u8 else 0) | (P_COL if p_col else 0) | (DS_FINE if ds_fine else 0)
 
 
 def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk=128, tau=None, p_u8=False):
@@ -111,17 +111,19 @@ def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk
 
 
 def bwd(q, k, v, o_stored, do, lse, *, causal=False, k_smooth=True, q_smooth=False, quant=True,
-        blk=128, tau=None, tiles=False, p_u8=False, p_col=False):
+        blk=128, tau=None, tiles=False, p_u8=False, p_col=False, ds_fine=False):
     """Alg. 2 per head.  o_stored is the O the forward stored (A15).
 
     tiles=True also returns the per-tile quantised P^ / dS^ ([BH, N q, N kv] uint8 / int8, tile (i, j) at
     rows i*blk.., columns j*blk..), their psi scales s_P / s_dS ([BH, T i, T j] fp32) and the
     pre-psi dS ([BH, N, N] double); tiles a causal run skips stay zero.  p_col=True: psi(P) per key
-    column of each tile (ORC_P_COL); the dumped s_P is then the tile's largest column scale."""
+    column of each tile (ORC_P_COL); the dumped s_P is then the tile's largest column scale.
+    ds_fine=True: psi(dS) per query row for dQ and per key column for dK (ORC_DS_FINE); the dumped dS^
+    is then the dK operand."""
     q, k, v, o_stored, do, lse = map(_f64, (q, k, v, o_stored, do, lse))
     BH, N, d = q.shape
     T = N // blk
-    flags = _flags(causal, k_smooth, q_smooth, quant, p_u8, p_col)
+    flags = _flags(causal, k_smooth, q_smooth, quant, p_u8, p_col, ds_fine)
     out = dict(dq=np.zeros((BH, N, d)), dk=np.zeros((BH, N, d)), dv=np.zeros((BH, N, d)),
                delta=np.zeros((BH, N)), do8=np.zeros((BH, N, d), np.int8),
                sdo=np.zeros((BH, T), np.float32))

@@ -40,6 +40,8 @@
                              u8 x s8 variant; psi(dS), psi(Q/K/V/dO) unchanged */
 #define ORC_P_COL    32   /* backward psi(P) per key column of the tile instead of per tile (the dV half
                              of SURVEY.md 8(f) NEXT-2): dV_j += (P^^T dO^_i) with one scale per key */
+#define ORC_DS_FINE  64   /* backward psi(dS) per query row for dQ and per key column for dK, two int8
+                             copies of the tile (the dS half of SURVEY.md 8(f) NEXT-2) */
 
 void oracle_set_threads(int n) {
 #ifdef _OPENMP
@@ -370,6 +372,9 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
   int pcol = (flags & ORC_P_COL) != 0;
   double *spcol = malloc(blk * sizeof(double));
   double *colx = malloc(blk * sizeof(double)), *colq = malloc(blk * sizeof(double));
+  int dsfine = (flags & ORC_DS_FINE) != 0;
+  int8_t *dSq8 = malloc(bb), *dSk8 = malloc(bb);
+  double *sq_row = malloc(blk * sizeof(double)), *sk_col = malloc(blk * sizeof(double));
   memset(dq, 0, nd * sizeof(double));
   memset(dk, 0, nd * sizeof(double));
   memset(dv, 0, nd * sizeof(double));
@@ -424,12 +429,26 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
         }
       double sds;
       psi_block(dS, (int)bb, 0, qo, 127.0, dS8, &sds, dSx);
+      /* the dQ operand (scale per query row r) and the dK operand (scale per key column n): the
+       * tile's dS^ and s_dS for both, or with ORC_DS_FINE a psi per row and a psi per column */
+      if (dsfine && !qo) {
+        for (int r = 0; r < blk; ++r) psi_block(dS + (size_t)r * blk, blk, 0, 0, 127.0, dSq8 + (size_t)r * blk, &sq_row[r], NULL);
+        for (int n = 0; n < blk; ++n) {
+          for (int r = 0; r < blk; ++r) colx[r] = dS[(size_t)r * blk + n];
+          psi_block(colx, blk, 0, 0, 127.0, NULL, &sk_col[n], colq);
+          for (int r = 0; r < blk; ++r) dSk8[(size_t)r * blk + n] = (int8_t)colq[r];
+        }
+      } else {
+        memcpy(dSq8, dS8, bb);
+        memcpy(dSk8, dS8, bb);
+        for (int e = 0; e < blk; ++e) sq_row[e] = sk_col[e] = sds;
+      }
       /* optional tile dumps (test infrastructure: Tier-C and fidelity reports), [N q][N kv] */
       for (int r = 0; r < blk; ++r)
         for (int n = 0; n < blk; ++n) {
           size_t g = (size_t)(i * blk + r) * N + (size_t)j * blk + n, t = (size_t)r * blk + n;
           if (p8_out) p8_out[g] = (uint8_t)Px[t];
-          if (ds8_out) ds8_out[g] = dS8[t];
+          if (ds8_out) ds8_out[g] = dSk8[t];  /* the dK operand (= the tile's dS^ unless ORC_DS_FINE) */
           if (ds_out) ds_out[g] = dS[t];
         }
       if (sp_out) sp_out[(size_t)i * T + j] = (float)sp;
@@ -445,8 +464,8 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
           } else {
             int32_t a = 0;
             for (int n = 0; n < blk; ++n)
-              a += (int32_t)dS8[(size_t)r * blk + n] * (int32_t)h.k8[(size_t)(j * blk + n) * d + c];
-            val = (double)a * sds * h.sk[j] * tau;
+              a += (int32_t)dSq8[(size_t)r * blk + n] * (int32_t)h.k8[(size_t)(j * blk + n) * d + c];
+            val = (double)a * sq_row[r] * h.sk[j] * tau;
           }
           dq[(size_t)(i * blk + r) * d + c] += val;
         }
@@ -454,7 +473,7 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
        * with Q-smoothing also dK_bias = (dS^T 1) mu_Q^T  (A13). */
       for (int n = 0; n < blk; ++n) {
         double colsum = 0.0;
-        for (int r = 0; r < blk; ++r) colsum += dSx[(size_t)r * blk + n];
+        for (int r = 0; r < blk; ++r) colsum += qo ? dSx[(size_t)r * blk + n] : (double)dSk8[(size_t)r * blk + n];
         for (int c = 0; c < d; ++c) {
           double val;
           if (qo) {
@@ -464,10 +483,10 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
           } else {
             int32_t a = 0;
             for (int r = 0; r < blk; ++r)
-              a += (int32_t)dS8[(size_t)r * blk + n] * (int32_t)h.q8[(size_t)(i * blk + r) * d + c];
-            val = (double)a * sds * h.sq[i] * tau;
+              a += (int32_t)dSk8[(size_t)r * blk + n] * (int32_t)h.q8[(size_t)(i * blk + r) * d + c];
+            val = (double)a * sk_col[n] * h.sq[i] * tau;
           }
-          if (flags & ORC_Q_SMOOTH) val += tau * (qo ? 1.0 : sds) * colsum * h.mu_q[(size_t)i * d + c];
+          if (flags & ORC_Q_SMOOTH) val += tau * (qo ? 1.0 : sk_col[n]) * colsum * h.mu_q[(size_t)i * d + c];
           dk[(size_t)(j * blk + n) * d + c] += val;
         }
       }
@@ -477,7 +496,7 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
   if (do8_out) memcpy(do8_out, do8, nd);
   if (sdo_out) for (int t = 0; t < T; ++t) sdo_out[t] = (float)sdo[t];
   free(delta); free(dox); free(do8); free(sdo); free(S); free(P); free(dS); free(Px); free(dSx);
-  free(dS8); free(spcol); free(colx); free(colq);
+  free(dS8); free(spcol); free(colx); free(colq); free(dSq8); free(dSk8); free(sq_row); free(sk_col);
   prep_free(&h);
 }
 

@@ -413,3 +413,29 @@ def test_p_col_variant(orc):
             assert np.all(p8.max(axis=1) == 127)  # max over the queries of each key column, every tile
     assert errs[True]["dv"] < 0.5 * errs[False]["dv"], errs
     assert errs[True]["dq"] == errs[False]["dq"] and errs[True]["dk"] == errs[False]["dk"], errs
+
+
+def test_ds_fine_variant(orc):
+    """psi(dS) per query row for dQ and per key column for dK (ORC_DS_FINE, the dS half of SURVEY.md
+    8(f) NEXT-2: the paper's named future work on the dS path, P:621-623): quant-off is unaffected;
+    at Table 1's sigma = 1 dQ and dK get well below the per-tile reading's error (A11), with dV and O
+    untouched; with Q-smoothing the dK bias pathway still holds."""
+    q, k, v, do = (f64(t).reshape(1, 512, 64) for t in make_inputs(1, 1, 512, 64, "gauss", seed=34, sigma=1.0))
+    ref = orc.fpa(q, k, v, do)
+    f = orc.fwd(q, k, v)
+    e = {}
+    for fine in (False, True):
+        b = orc.bwd(q, k, v, f["o"], do, f["lse"], ds_fine=fine)
+        e[fine] = {n: rel_l2(ref[n], b[n]) for n in ("dq", "dk", "dv")}
+    assert e[True]["dq"] < 0.6 * e[False]["dq"] and e[True]["dk"] < 0.6 * e[False]["dk"], e
+    assert e[True]["dv"] == e[False]["dv"], e
+    ex = orc.fwd(q, k, v, quant=False)
+    b0 = orc.bwd(q, k, v, ex["o"], do, ex["lse"], quant=False)
+    b1 = orc.bwd(q, k, v, ex["o"], do, ex["lse"], quant=False, ds_fine=True)
+    assert np.array_equal(b0["dq"], b1["dq"]) and np.array_equal(b0["dk"], b1["dk"])
+    q2, k2, v2, do2 = (f64(t).reshape(2, 256, 64) for t in make_inputs(1, 2, 256, 64, "outlier_kq", seed=13))
+    q2 = q2 + 20.0
+    ref2 = orc.fpa(q2, k2, v2, do2, causal=True)
+    f2 = orc.fwd(q2, k2, v2, causal=True, q_smooth=True)
+    b2 = orc.bwd(q2, k2, v2, f2["o"], do2, f2["lse"], causal=True, q_smooth=True, ds_fine=True)
+    assert rel_l2(ref2["dk"], b2["dk"]) < 0.15 and rel_l2(ref2["dq"], b2["dq"]) < 0.15
