@@ -73,11 +73,18 @@ enum {
                               Non-causal requires N/128 <= the device's SM count
                               (SAGE_ERR_UNSUPPORTED otherwise).  Every other output is always
                               deterministic. */
-  SAGE_P_COLSCALE = 1u << 6 /* variant (the dV half of SURVEY.md 8(f) NEXT-2): the backward's psi(P)
+  SAGE_P_COLSCALE = 1u << 6, /* variant (the dV half of SURVEY.md 8(f) NEXT-2): the backward's psi(P)
                               (Alg. 2 line 6) takes one scale per key of the tile (the max over its
                               128 queries) instead of one per tile; dV_j's drain applies it per row.
                               dV's error vs full precision drops ~2.6x at Table 1's sigma = 1.
                               Not combinable with SAGE_DETERMINISTIC (SAGE_ERR_INVALID_VALUE). */
+  SAGE_FINE_BWD = 1u << 7   /* variant (the paper's future work on the dS path,
+                              P:621-623): SAGE_P_COLSCALE plus psi(dS) (Alg. 2 line 9) taken twice,
+                              with one scale per key for the dK operand and one per query for the dQ
+                              operand (two int8 copies of the tile).  At Table 1's sigma = 1 it brings
+                              dQ / dK / dV to 0.022 / 0.022 / 0.021 vs the paper's 0.018 / 0.022 /
+                              0.016 (per-tile: 0.067 / 0.066 / 0.055).  Slower backward.  Not
+                              combinable with SAGE_DETERMINISTIC. */
 };
 
 typedef struct {

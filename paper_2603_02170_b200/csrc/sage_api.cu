@@ -66,7 +66,7 @@ size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Dims {
   size_t BH, N, d, T;
-  bool causal, ks, qs, pu8, qkn, det, pcol;
+  bool causal, ks, qs, pu8, qkn, det, pcol, fine;
   float tau;
 };
 
@@ -76,7 +76,7 @@ bool dims_of(const sage_params* p, Dims* o) {
   if (p->head_dim != 64 && p->head_dim != 128) return false;
   if (p->seqlen % kBlk || p->seqlen > kMaxSeqLen) return false;
   if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH | SAGE_P_U8 | SAGE_QK_NORM | SAGE_DETERMINISTIC |
-                             SAGE_P_COLSCALE))
+                             SAGE_P_COLSCALE | SAGE_FINE_BWD))
     return false;
   if (!(p->softmax_scale >= 0.f) || std::isinf(p->softmax_scale)) return false;
   const size_t BH = (size_t)p->batch * p->heads;
@@ -92,7 +92,8 @@ bool dims_of(const sage_params* p, Dims* o) {
   o->qkn = p->flags & SAGE_QK_NORM;
   o->det = p->flags & SAGE_DETERMINISTIC;
   o->pcol = p->flags & SAGE_P_COLSCALE;
-  if (o->det && o->pcol) return false;  // one backward variant at a time
+  o->fine = p->flags & SAGE_FINE_BWD;
+  if (o->det && (o->pcol || o->fine)) return false;  // one backward variant at a time
   o->tau = p->softmax_scale > 0.f ? p->softmax_scale : 1.f / std::sqrt((float)p->head_dim);
   return true;
 }
@@ -466,6 +467,7 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
   a.pu8 = D.pu8;
   a.dq_flags = dqflags;
   a.pcol = D.pcol;
+  a.fine = D.fine;
   a.ablate = ablate_flags() | (g_dump_heads > 0 ? 16 : 0);
   if ((e = timed(1, s, [&] { return launch_bwd(a, s); })) != cudaSuccess) return cuda_fail(e);
   if (g_prof.on) g_prof.launches += 2;  // K3, K4

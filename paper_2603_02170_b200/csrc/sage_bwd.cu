@@ -37,7 +37,7 @@ constexpr int kDrainWarps = 4;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kMaxT = kMaxSeqLen / kBlk;
 
-template <int D>
+template <int D, bool FINE = false>
 struct BwdSmem {
   static constexpr int kStages = D == 64 ? 4 : 2;
   static constexpr int kTile = kBlk * D;           // int8 [128][D]
@@ -54,22 +54,32 @@ struct BwdSmem {
   static constexpr int kDO = kStage + kStages * kStageBytes;    // d=128: dO_i bf16 panels
   static constexpr int kPt = kDO + (kSplitDO ? 2 * kTile : 0);  // P^^T [128 kv][128 q]
   static constexpr int kDSt = kPt + (D == 64 ? 0 : kBlk * kBlk);  // dS^^T [128 kv][128 q] (d=64: P^^T is in TMEM)
-  static constexpr int kRed = kDSt + kBlk * kBlk;             // [2][8] floats (cross-warp max)
-  static constexpr int kScl = kRed + 64;                      // [4][2] floats {s_P, s_dS} per tile slot
-  static constexpr int kRowSum = kScl + 32;                   // [2 slots][2 wg][128] int (Q-smoothing colsum of dS^)
-  static constexpr int kRowX = kRowSum + 4 * kBlk * 4;         // [2 wg][128] per-row P maxima (SAGE_P_COLSCALE)
-  static constexpr int kSpRow = kRowX + 2 * kBlk * 4;          // [4 slots][128] per-key psi(P) maxima for the drain
-  static constexpr int kScQ = kSpRow + 4 * kBlk * 4;           // s_Q[bh][0..T), s_dO[bh][0..T) (T <= kMaxT)
-  static constexpr int kScDO = kScQ + kMaxT * 4;
+  static constexpr int kDSq = kDSt + kBlk * kBlk;             // FINE: dS^ with per-query scales (A of dQ)
   // dQ staging for the TMA reduce-add, per drain warp (its 32 TMEM lanes = 32 query rows):
-  // 2 buffers of [kDqBoxes][32 rows][32 cols] fp32 boxes, 128B-swizzled; d=64 stages the warp's
+  // kDqBufs buffers of [kDqBoxes][32 rows][32 cols] fp32 boxes, 128B-swizzled; d=64 stages the warp's
   // whole row slice per round, d=128 a quarter of it (4 rounds per tile).  No cross-warp barrier.
+  // FINE gives one staging buffer to its second dS^ tile and puts the staging right after the tiles
+  // (1024-aligned without padding) to fit in 227 KB.
   static constexpr int kDqBox = 32 * 32 * 4;
   static constexpr int kDqBoxes = 1;
   static constexpr int kDqRounds = (D / 32) / kDqBoxes;
-  static constexpr int kDqWarp = 2 * kDqBoxes * kDqBox;  // per drain warp
-  static constexpr int kDq = (kScDO + kMaxT * 4 + 1023) / 1024 * 1024;
-  static constexpr int kBar = kDq + 4 * kDqWarp;
+  static constexpr int kDqBufs = FINE ? 1 : 2;
+  static constexpr int kDqWarp = kDqBufs * kDqBoxes * kDqBox;  // per drain warp
+  static constexpr int kSmall = FINE ? kDSq + kBlk * kBlk + 4 * kDqWarp : kDSq;  // the small arrays start here
+  static constexpr int kRed = kSmall;                         // [2][8] floats (cross-warp max)
+  static constexpr int kScl = kRed + 64;                      // [4][2] floats {s_P, s_dS} per tile slot
+  static constexpr int kRowSum = kScl + 32;                   // [2 slots][2 wg][128] int (Q-smoothing colsum of dS^)
+  static constexpr int kRowX = kRowSum + 4 * kBlk * 4;         // [P, dS][2 wg][128] per-row maxima (exchange)
+  static constexpr int kSpRow = kRowX + (FINE ? 2 : 1) * 2 * kBlk * 4;  // [4 slots][128] per-key psi(P) maxima
+  static constexpr int kSpK = kSpRow + 4 * kBlk * 4;           // FINE: [4 slots][128] per-key dS maxima (dK)
+  static constexpr int kSpQ = kSpK + (FINE ? 4 * kBlk * 4 : 0);  // FINE: [4 slots][128] per-query dS maxima (dQ)
+  static constexpr int kColMax = kSpQ + (FINE ? 4 * kBlk * 4 : 0);  // FINE: [2 wg][4 warps][64] column maxima
+  static constexpr int kInvQ = kColMax + (FINE ? 2 * 4 * 64 * 4 : 0);  // FINE: [2 wg][64] per-query inverses
+  // s_Q[bh][0..T), s_dO[bh][0..T) staged in smem (T <= kMaxT); FINE reads them from global instead
+  static constexpr int kScQ = kInvQ + (FINE ? 2 * 64 * 4 : 0);
+  static constexpr int kScDO = kScQ + (FINE ? 0 : kMaxT * 4);
+  static constexpr int kDq = FINE ? kDSq + kBlk * kBlk : (kScDO + kMaxT * 4 + 1023) / 1024 * 1024;
+  static constexpr int kBar = FINE ? kScDO : kDq + 4 * kDqWarp;
   static constexpr int kNumBars = 1 + 2 * kStages + 13;
   static constexpr int kTmemSlot = kBar + kNumBars * 8;
   static constexpr int kBytes = kTmemSlot + 16;
@@ -118,8 +128,9 @@ __device__ __forceinline__ float compute_max(float v, int* red, int cw, int id) 
   return ford_inv(max(max(max(a.x, a.y), max(a.z, a.w)), max(max(b.x, b.y), max(b.z, b.w))));
 }
 
-// VAR: 0 the default path, 1 SAGE_DETERMINISTIC, 2 SAGE_P_COLSCALE -- separate instantiations, because
-// compiling the variants' logic into the default kernel costs 2-8% (measured)
+// VAR: 0 the default path, 1 SAGE_DETERMINISTIC, 2 SAGE_P_COLSCALE, 3 SAGE_FINE_BWD (per-key psi(P),
+// per-key dS^ for dK, per-query dS^ for dQ) -- separate instantiations, because compiling the
+// variants' logic into the default kernel costs 2-8% (measured)
 template <int D, bool CAUSAL, bool QSMOOTH, int VAR>
 __global__ void __launch_bounds__(kThreads, 1)
     sage_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -131,11 +142,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* __restrict__ mu_q, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dk,
                     __nv_bfloat16* __restrict__ dv, int N, int BH, float tau, int pu8,
                     unsigned* __restrict__ dq_flags, int ablate_arg) {
-  constexpr bool pcol = VAR == 2;
+  constexpr bool fine = VAR == 3;
+  constexpr bool pcol = VAR == 2 || fine;
   const int ablate = SAGE_TRACE ? ablate_arg : 0;
   // psi(P) levels (Alg. 2 line 6): 127, or 255 for the unsigned P^ variant (SAGE_P_U8)
   const float pmax = pu8 ? 255.f : 127.f;
-  using L = BwdSmem<D>;
+  using L = BwdSmem<D, VAR == 3>;
   constexpr int kStages = L::kStages;
   constexpr bool kAlias = D == 128;
   // setmaxnreg budgets (x128 threads each; sum = 512 regs/thread-slot = the 64K register file)
@@ -168,11 +180,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
   int* red = reinterpret_cast<int*>(smem + L::kRed);
   float* scl = reinterpret_cast<float*>(smem + L::kScl);
-  float* sc_q = reinterpret_cast<float*>(smem + L::kScQ);
-  float* sc_do = reinterpret_cast<float*>(smem + L::kScDO);
+  float* sc_q_s = reinterpret_cast<float*>(smem + L::kScQ);
+  float* sc_do_s = reinterpret_cast<float*>(smem + L::kScDO);
   int* rowsum_s = reinterpret_cast<int*>(smem + L::kRowSum);
   float* rowx = reinterpret_cast<float*>(smem + L::kRowX);
   float* sp_row = reinterpret_cast<float*>(smem + L::kSpRow);
+  float* sp_k = reinterpret_cast<float*>(smem + L::kSpK);     // FINE
+  float* sp_q = reinterpret_cast<float*>(smem + L::kSpQ);     // FINE
+  int* colmax = reinterpret_cast<int*>(smem + L::kColMax);    // FINE
+  float* invq_s = reinterpret_cast<float*>(smem + L::kInvQ);  // FINE
 
   const int T = N / kBlk;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -213,9 +229,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(s_free, kComputeWarps);
     fence_mbar_init();
   }
-  for (int t = threadIdx.x; t < T; t += kThreads) {
-    sc_q[t] = q_scale[(size_t)bh * T + t];
-    sc_do[t] = do_scale[(size_t)bh * T + t];
+  // per-block scales s_Q, s_dO of this head: staged in smem (FINE, short of smem: read from global)
+  const float* sc_q = fine ? q_scale + (size_t)bh * T : sc_q_s;
+  const float* sc_do = fine ? do_scale + (size_t)bh * T : sc_do_s;
+  for (int t = threadIdx.x; !fine && t < T; t += kThreads) {
+    sc_q_s[t] = q_scale[(size_t)bh * T + t];
+    sc_do_s[t] = do_scale[(size_t)bh * T + t];
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -293,6 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t v_addr = smem_u32(smem + L::kV);
       const uint32_t pt_addr = smem_u32(smem + L::kPt);
       const uint32_t dst_addr = smem_u32(smem + L::kDSt);
+      const uint32_t dsq_addr = smem_u32(smem + (fine ? L::kDSq : L::kDSt));  // FINE: the per-query dS^
       auto soff = [&](int it) { return (uint32_t)((it % kStages) * L::kStageBytes); };
       auto issue_s = [&](int it) {
         mbar_wait(q_full + it % kStages, (it / kStages) & 1);
@@ -352,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_i8(tDK, desc_kmajor(dst_addr, 128, kk * 32), desc_mnmajor(q_addr, D, kk * 32), kIdDV, kk > 0);
 #pragma unroll
           for (int kk = 0; kk < kBlk / 32; ++kk)
-            mma_i8(tDQ, desc_mnmajor(dst_addr, 128, kk * 32), desc_mnmajor(k_addr, D, kk * 32), kIdDQ, kk > 0);
+            mma_i8(tDQ, desc_mnmajor(dsq_addr, 128, kk * 32), desc_mnmajor(k_addr, D, kk * 32), kIdDQ, kk > 0);
           mma_commit(dkq_full);
           mma_commit(q_empty + it % kStages);
           TR(3, it);
@@ -583,8 +603,32 @@ if (cm) {
       warp_arrive(p_ready);  // P^^T written; S^T and dP^T read (their TMEM columns may be reused)
       if (threadIdx.x == 128) TR(6, it);
 
-      // -- step 5: psi(dS) scale over the tile
-      const float amax_ds = compute_max(dsmax, red + 8, cw, 2);
+      // -- step 5: psi(dS) scale over the tile (FINE: one per key row for dK, one per query for dQ)
+      float amax_ds;
+      if constexpr (fine) {
+        // per key: this thread's 64 queries and the other warpgroup's 64 (second exchange slot)
+        rowx[2 * kBlk + wg * kBlk + r] = dsmax;
+        // per query: the max of |dS| over this warpgroup's 128 key rows, column by column
+        // (|x| as int is monotone), one redux per column and warp, lane 0 keeps the 64 results
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const int m = __reduce_max_sync(0xffffffffu, __float_as_int(fabsf(t[c])));
+          if (lane == 0) colmax[(wg * 4 + (warp % 4)) * 64 + c] = m;
+        }
+        named_bar_sync(2, 256);
+        amax_ds = fmaxf(dsmax, rowx[2 * kBlk + (wg ^ 1) * kBlk + r]);
+        if (wg == 0) sp_k[(it & 3) * kBlk + r] = amax_ds;
+        const int tw = threadIdx.x - 128 - wg * 128;  // 0..127 within the warpgroup
+        if (tw < 64) {
+          const int* cmx = colmax + wg * 4 * 64 + tw;
+          const float aq = __int_as_float(max(max(cmx[0], cmx[64]), max(cmx[128], cmx[192])));
+          invq_s[wg * 64 + tw] = aq > 0.f ? __fmul_rn(127.f, __frcp_rn(aq)) : 0.f;
+          sp_q[(it & 3) * kBlk + qc0 + tw] = aq;
+        }
+        named_bar_sync(3 + wg, 128);
+      } else {
+        amax_ds = compute_max(dsmax, red + 8, cw, 2);
+      }
       const float inv_ds = amax_ds > 0.f ? __fmul_rn(127.f, __frcp_rn(amax_ds)) : 0.f;
       if (threadIdx.x == 128) scl[(it & 3) * 2 + 1] = amax_ds;
       if (DUMPING) {
@@ -614,6 +658,19 @@ if (cm) {
           if constexpr (QSMOOTH) rsum = __dp4a((int)w[e4], 0x01010101, rsum);
         }
         *reinterpret_cast<uint4*>(dst + sw_offset(r, qc0 / 16 + c16, 128)) = make_uint4(w[0], w[1], w[2], w[3]);
+        if constexpr (fine) {  // the dQ operand: the same dS with per-query inverses
+          uint32_t wq[4];
+#pragma unroll
+          for (int e4 = 0; e4 < 4; ++e4) {
+            const int e = c16 * 16 + e4 * 4;
+            const float4 iq = *reinterpret_cast<const float4*>(invq_s + wg * 64 + e);
+            float2 qa = ffma2(make_float2(t[e], t[e + 1]), make_float2(iq.x, iq.y), make_float2(kMagic, kMagic));
+            float2 qb = ffma2(make_float2(t[e + 2], t[e + 3]), make_float2(iq.z, iq.w), make_float2(kMagic, kMagic));
+            wq[e4] = pack4_magic(qa.x, qa.y, qb.x, qb.y);
+          }
+          *reinterpret_cast<uint4*>(smem + L::kDSq + sw_offset(r, qc0 / 16 + c16, 128)) =
+              make_uint4(wq[0], wq[1], wq[2], wq[3]);
+        }
         if (DUMPING)
           *reinterpret_cast<uint4*>(g_dump.dst + ((size_t)bh * N + j * kBlk + r) * N + i * kBlk + qc0 + c16 * 16) =
               make_uint4(w[0], w[1], w[2], w[3]);
@@ -709,7 +766,8 @@ if (cm) {
       tc_fence_after();
       if (threadIdx.x == 384) TR(11, it);
       if (!(ablate & 1)) {
-        const float s_ds = __fdiv_rn(scl[(it & 3) * 2 + 1], 127.f);  // psi(dS) scale
+        // psi(dS) scale: the tile's, or this key row's (FINE)
+        const float s_ds = __fdiv_rn(fine ? sp_k[(it & 3) * kBlk + r] : scl[(it & 3) * 2 + 1], 127.f);
         const float2 f = make_float2(s_ds * sq * tau, s_ds * sq * tau);
         float fb = 0.f;
         const float* muq = nullptr;
@@ -749,7 +807,8 @@ if (cm) {
       if (threadIdx.x == 384) TR(12, it);
       {
         // scaled rows -> this warp's swizzled smem staging (2 buffers) -> TMA reduce-add per box
-        const float s_ds = __fdiv_rn(scl[(it & 3) * 2 + 1], 127.f);
+        // the tile's psi(dS) scale, or this query row's (FINE; TMEM lane r = query row of dQ_i)
+        const float s_ds = __fdiv_rn(fine ? sp_q[(it & 3) * kBlk + r] : scl[(it & 3) * 2 + 1], 127.f);
         const float2 f = make_float2(s_ds * sk * tau, s_ds * sk * tau);
         uint8_t* wstage = smem + L::kDq + (warp % 4) * L::kDqWarp;
         unsigned* flag = det ? dq_flags + ((size_t)bh * T + i) * kDrainWarps + (warp % 4) : nullptr;
@@ -760,8 +819,8 @@ if (cm) {
 #pragma unroll
         for (int qq = 0; qq < L::kDqRounds; ++qq) {
           const int rnd = it * L::kDqRounds + qq;
-          uint8_t* stage = wstage + (rnd & 1) * L::kDqBoxes * L::kDqBox;
-          if (lane == 0 && rnd >= 2) bulk_wait_read<1>();  // this warp's round rnd-2 has read `stage`
+          uint8_t* stage = wstage + (rnd % L::kDqBufs) * L::kDqBoxes * L::kDqBox;
+          if (lane == 0 && rnd >= L::kDqBufs) bulk_wait_read<L::kDqBufs - 1>();  // round rnd-kDqBufs has read `stage`
           __syncwarp();
           if (!(ablate & 1)) {
 #pragma unroll
@@ -850,10 +909,11 @@ if (cm) {
 template <int D, bool C, bool QS, int VAR>
 cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
   auto kern = sage_bwd_kernel<D, C, QS, VAR>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem<D>::kAlloc);
+  constexpr int kSmem = BwdSmem<D, VAR == 3>::kAlloc;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
   if (e != cudaSuccess) return e;
   const int T = a.N / kBlk;
-  kern<<<a.BH * T, kThreads, BwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_doq, a.tm_v, a.tm_do, a.tm_dq, a.q_scale,
+  kern<<<a.BH * T, kThreads, kSmem, s>>>(a.tm_q, a.tm_k, a.tm_doq, a.tm_v, a.tm_do, a.tm_dq, a.q_scale,
                                                        a.k_scale, a.do_scale, a.l2, a.delta, a.bias, a.mu_q,
                                                        a.dq_acc, a.dk, a.dv, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
                                                        a.dq_flags, a.ablate);
@@ -877,7 +937,8 @@ cudaError_t launch_d(const BwdArgs& a, cudaStream_t s) {
 
 template <int D>
 cudaError_t launch_v(const BwdArgs& a, cudaStream_t s) {
-  if (a.dq_flags != nullptr) return launch_d<D, 1>(a, s);  // the API rejects det + colscale
+  if (a.dq_flags != nullptr) return launch_d<D, 1>(a, s);  // the API rejects det + colscale / fine
+  if (a.fine) return launch_d<D, 3>(a, s);
   return a.pcol ? launch_d<D, 2>(a, s) : launch_d<D, 0>(a, s);
 }
 

@@ -93,6 +93,7 @@ struct BwdArgs {
   bool causal, qsmooth;
   bool pu8;    // SAGE_P_U8: psi(P) in 0..255 (u8 x s8 dV)
   bool pcol;   // SAGE_P_COLSCALE: psi(P) per key row of P^T instead of per tile
+  bool fine;   // SAGE_FINE_BWD: pcol + psi(dS) per key for dK and per query for dQ
   unsigned* dq_flags;  // SAGE_DETERMINISTIC: [BH][T][4] zeroed ordering flags, or null
   int ablate;  // profiling only (SAGE_ABLATE): 1 drain math off, 2 compute math off, 4 dQ reduction off
 };

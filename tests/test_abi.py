@@ -41,7 +41,7 @@ def test_sizes_and_invalid_params(L):
         assert L.sage_ctx_bytes(ctypes.byref(bad)) == 0
         assert L.sage_workspace_bytes(ctypes.byref(bad), 0) == 0
     bad = make_params(1, 1, 128, 64)
-    bad.flags = 1 << 7
+    bad.flags = 1 << 12
     assert L.sage_ctx_bytes(ctypes.byref(bad)) == 0
 
 
@@ -68,6 +68,7 @@ def test_error_paths_do_not_launch(L):
     assert L.sage_debug_umma(1, 128, 96, A, A, A, z) == 1
     # one backward variant at a time: SAGE_DETERMINISTIC with SAGE_P_COLSCALE is rejected
     assert L.sage_ctx_bytes(ctypes.byref(make_params(1, 2, 256, 64, deterministic=True, p_colscale=True))) == 0
+    assert L.sage_ctx_bytes(ctypes.byref(make_params(1, 2, 256, 64, deterministic=True, fine_bwd=True))) == 0
     assert L.sage_ctx_bytes(ctypes.byref(make_params(1, 2, 256, 64, p_colscale=True))) == nctx
     # QK-norm params need the _qknorm entry points, which need gamma and eps > 0
     pn = make_params(1, 2, 256, 64, qk_norm=True)

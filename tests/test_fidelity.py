@@ -43,13 +43,13 @@ def dump_lib():
     sage.use_library(old)
 
 
-def _gpu_with_dump(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, p_col=False):
+def _gpu_with_dump(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, p_col=False, fine=False):
     B, H, N, d = q.shape
     dev = torch.device("cuda")
     qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
     bufs = sage.debug_dump(B * H, N, dev)
     o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8,
-                               p_colscale=p_col)
+                               p_colscale=p_col, fine_bwd=fine)
     dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
     torch.cuda.synchronize()
     sage.debug_dump(0, 0, None)
@@ -65,13 +65,14 @@ def _gpu_with_dump(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, p_col=Fa
     return dict(o=flat(o), dq=flat(dq), dk=flat(dk), dv=flat(dv), delta=delta, **tiles)
 
 
-def _oracle_run(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, p_col=False):
+def _oracle_run(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, p_col=False, fine=False):
     B, H, N, d = q.shape
     qn, kn, vn, don = (f64(t).reshape(B * H, N, d) for t in (q, k, v, do))
     kw = dict(causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8)
     oracle.set_threads(min(8, os.cpu_count() or 1))
     f = oracle.fwd(qn, kn, vn, **kw)
-    b = oracle.bwd(qn, kn, vn, round_bf16(f["o"]), don, f["lse"], tiles=True, p_col=p_col, **kw)
+    b = oracle.bwd(qn, kn, vn, round_bf16(f["o"]), don, f["lse"], tiles=True, p_col=p_col or fine, ds_fine=fine,
+                   **kw)
     return f, b
 
 
@@ -257,3 +258,29 @@ def test_fidelity_p_colscale(dump_lib):
     assert rows["per_key"]["dv"]["gpu_rel_l2"] < 0.5 * rows["per_tile"]["dv"]["gpu_rel_l2"]
     for name in ("o", "dq", "dk"):
         assert rows["per_key"][name]["gpu_rel_l2"] == pytest.approx(rows["per_tile"][name]["gpu_rel_l2"], rel=0.02)
+
+
+def test_fidelity_fine_bwd_table1(dump_lib):
+    """SAGE_FINE_BWD on the GPU over Table 1's sigma sweep: at sigma = 1 (the row the literal per-tile
+    psi reading misses by 2.5-4x) dQ / dK / dV land within 1.45x of the paper's
+    0.0184 / 0.0220 / 0.0159; at sigma >= 3, where the error already sits in dS before
+    psi, the variant changes little; the GPU tracks the oracle's ORC_P_COL | ORC_DS_FINE mode."""
+    B, H, N, d = 1, 2, 1024, 64
+    rows = {}
+    for sigma in sorted(TABLE1):
+        q, k, v, do = make_inputs(B, H, N, d, "gauss", seed=11, sigma=sigma)
+        ref = _fpa(q, k, v, do, False)
+        g = _gpu_with_dump(q, k, v, do, False, True, False, fine=True)
+        f, b = _oracle_run(q, k, v, do, False, True, False, fine=True)
+        row = {}
+        for name in ("o", "dq", "dk", "dv"):
+            qo = f["o"] if name == "o" else b[name]
+            row[name] = dict(gpu_rel_l2=rel_l2(ref[name], g[name]), oracle_rel_l2=rel_l2(ref[name], qo))
+            gr, orr = row[name]["gpu_rel_l2"], row[name]["oracle_rel_l2"]
+            assert abs(gr - orr) <= 0.05 * orr + 1e-4, (sigma, name, gr, orr)
+        row["paper"] = dict(zip(("o", "dq", "dk", "dv"), TABLE1[sigma]))
+        rows[str(sigma)] = row
+    _write_report("fine_bwd_table1", dict(setting=f"B={B} H={H} N={N} d={d} non-causal K-smooth gauss(sigma), "
+                                                  "SAGE_FINE_BWD", rows=rows))
+    for name, paper in zip(("dq", "dk", "dv"), TABLE1[1.0][1:]):
+        assert rows["1.0"][name]["gpu_rel_l2"] <= 1.45 * paper, (name, rows["1.0"])

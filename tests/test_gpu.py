@@ -27,17 +27,18 @@ def _gpu():
     oracle.build()
 
 
-def _run(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, deterministic=False, p_colscale=False):
+def _run(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, deterministic=False, p_colscale=False,
+         fine_bwd=False):
     dev = "cuda"
     qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
     o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8,
-                               deterministic=deterministic, p_colscale=p_colscale)
+                               deterministic=deterministic, p_colscale=p_colscale, fine_bwd=fine_bwd)
     dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
     torch.cuda.synchronize()
     return dict(o=o, lse=lse, dq=dq, dk=dk, dv=dv, ctx=ctx)
 
 
-def _oracle(q, k, v, do, heads, causal, k_smooth, q_smooth, p_u8=False, p_col=False):
+def _oracle(q, k, v, do, heads, causal, k_smooth, q_smooth, p_u8=False, p_col=False, ds_fine=False):
     """Oracle on the selected flattened heads; O is stored as bf16 before the backward (A15)."""
     B, H, N, d = q.shape
     sel = lambda t: f64(t).reshape(B * H, N, d)[heads]
@@ -45,7 +46,7 @@ def _oracle(q, k, v, do, heads, causal, k_smooth, q_smooth, p_u8=False, p_col=Fa
     kw = dict(causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8)
     f = oracle.fwd(qn, kn, vn, **kw)
     o_st = round_bf16(f["o"])
-    b = oracle.bwd(qn, kn, vn, o_st, don, f["lse"], p_col=p_col, **kw)
+    b = oracle.bwd(qn, kn, vn, o_st, don, f["lse"], p_col=p_col, ds_fine=ds_fine, **kw)
     return f, b
 
 
@@ -209,6 +210,26 @@ def test_fwd_bwd_parity_p_colscale(B, H, N, d, causal, qs, u8, recipe):
     heads = list(range(B * H))
     f, b = _oracle(q, k, v, do, heads, causal, True, qs, p_u8=u8, p_col=True)
     _assert_ok(_compare(gpu, f, b, heads, B, H, N, d), ("pcol", B, H, N, d, causal, qs, u8, recipe))
+
+
+FINE_CASES = [
+    (1, 2, 384, 64, True, False, False, "gauss"),
+    (1, 2, 256, 64, False, True, False, "outlier_kq"),
+    (1, 2, 256, 128, False, False, False, "qknorm"),
+    (1, 2, 384, 128, True, True, True, "outlier_kq"),
+    (2, 1, 512, 128, True, False, False, "gauss"),
+]
+
+
+@pytest.mark.parametrize("B,H,N,d,causal,qs,u8,recipe", FINE_CASES)
+def test_fwd_bwd_parity_fine_bwd(B, H, N, d, causal, qs, u8, recipe):
+    """SAGE_FINE_BWD (per-key psi(P), per-key dS^ for dK, per-query dS^ for dQ) against the oracle's
+    ORC_P_COL | ORC_DS_FINE mode, also with Q-smoothing and SAGE_P_U8."""
+    q, k, v, do = make_inputs(B, H, N, d, recipe, seed=800 + N + d)
+    gpu = _run(q, k, v, do, causal, True, qs, p_u8=u8, fine_bwd=True)
+    heads = list(range(B * H))
+    f, b = _oracle(q, k, v, do, heads, causal, True, qs, p_u8=u8, p_col=True, ds_fine=True)
+    _assert_ok(_compare(gpu, f, b, heads, B, H, N, d), ("fine", B, H, N, d, causal, qs, u8, recipe))
 
 
 DET_CASES = [
