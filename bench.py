@@ -202,14 +202,14 @@ def run_reference(args, c, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(c, l2, qk_norm=False, p_u8=False, deterministic=False):
+def config_dict(c, l2, qk_norm=False, p_u8=False, deterministic=False, fine_bwd=False):
     return {"workload": f"{c.name}: B={c.batch} H={c.heads} N={c.seqlen} d={c.head_dim} "
                         f"{'causal' if c.causal else 'non-causal'} K-smooth={c.k_smooth} Q-smooth={c.q_smooth} "
                         f"inputs={c.recipe}" + (" +QK-norm (fused)" if qk_norm else "") + (" P^ u8" if p_u8 else "")
-                        + (" deterministic" if deterministic else ""),
+                        + (" deterministic" if deterministic else "") + (" fine-bwd" if fine_bwd else ""),
             "batch": c.batch, "heads": c.heads, "seqlen": c.seqlen, "head_dim": c.head_dim, "causal": c.causal,
             "k_smooth": c.k_smooth, "q_smooth": c.q_smooth, "qk_norm": qk_norm, "p_u8": p_u8,
-            "deterministic": deterministic, "l2": l2}
+            "deterministic": deterministic, "fine_bwd": fine_bwd, "l2": l2}
 
 
 # ---------------------------------------------------------------------- GPU arm
@@ -226,6 +226,7 @@ def main():
                     help="QK-norm fused in front of the path (sage_fwd_qknorm / sage_bwd_qknorm, C5's ablation)")
     ap.add_argument("--p-u8", action="store_true", help="unsigned P^ variant (SAGE_P_U8)")
     ap.add_argument("--deterministic", action="store_true", help="bitwise reproducible dQ (SAGE_DETERMINISTIC)")
+    ap.add_argument("--fine-bwd", action="store_true", help="per-key / per-query backward psi (SAGE_FINE_BWD)")
     args = ap.parse_args()
     assert args.warmup >= 3, "at least 3 warm-up steps"
     c = CONFIGS[args.config]
@@ -249,6 +250,8 @@ def main():
     kw = dict(causal=c.causal, k_smooth=c.k_smooth, q_smooth=c.q_smooth, p_u8=args.p_u8)
     if args.deterministic:
         kw["deterministic"] = True
+    if args.fine_bwd:
+        kw["fine_bwd"] = True
     if args.qk_norm:
         # the config's Q, K serve as the pre-norm X_q, X_k; gamma ~ U(0.5, 2) seeded
         g = torch.Generator().manual_seed(c.seed + 7)
@@ -364,7 +367,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "i8/bf16", "data": "synthetic",
                 "config": config_dict(c, "flushed between timed steps (256 MiB write, untimed)", args.qk_norm,
-                                      args.p_u8, args.deterministic),
+                                      args.p_u8, args.deterministic, args.fine_bwd),
                 "frac_of_int8_peak": value / world / pk["int8"], "int8_peak_tops": pk["int8"],
                 "roofline": roof, "e2e": e2e, "gpu_launches": prof["launches"], "clocks": clk.summary()}
         if not args.no_cpu_baseline and world == 1:

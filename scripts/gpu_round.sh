@@ -7,7 +7,7 @@ TAG=${TAG:-r01}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > gpurun_out/gpu_info.txt 2>&1
 timeout 900 python -m pytest tests/ -m gpu -q -rA 2>&1 | tail -80 > gpurun_out/t_gpu_all.log
 TAG=$TAG CONFIGS="C3 C4 C5" bash scripts/gpu_bench_all.sh > /dev/null 2>&1
-for a in --qk-norm --p-u8; do
+for a in --qk-norm --p-u8 --fine-bwd --deterministic; do
   timeout 600 python bench.py --config C5 --steps 10 --warmup 3 --no-cpu-baseline $a > gpurun_out/bench_${TAG}_C5${a//-/_}.json 2> /dev/null
 done
 TAG=$TAG CONFIGS="${NCU_CONFIGS:-C2 C3 C4}" bash scripts/gpu_evidence.sh > /dev/null 2>&1
