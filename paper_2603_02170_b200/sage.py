@@ -223,14 +223,16 @@ def _check_gamma(g, d, device):
 
 
 def forward_qknorm(xq, xk, v, gamma_q, gamma_k, eps=1e-6, causal=False, k_smooth=True, q_smooth=False,
-                   softmax_scale=None, p_u8=False, out=None, lse=None, ctx=None, workspace=None, stream=None):
+                   softmax_scale=None, p_u8=False, out=None, lse=None, ctx=None, workspace=None, stream=None,
+                   deterministic=False, p_colscale=False, fine_bwd=False):
     """sage_fwd_qknorm: QK-norm fused in front of Alg. 1.  xq, xk: the pre-norm bf16
     [B, H, N, d]; gamma_q, gamma_k: fp32 [d].  Returns (o, lse, SageCtx)."""
     _check_io(xq, xk, v)
     B, H, N, d = xq.shape
     _check_gamma(gamma_q, d, xq.device)
     _check_gamma(gamma_k, d, xq.device)
-    p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8, qk_norm=True)
+    p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8, qk_norm=True,
+                    deterministic=deterministic, p_colscale=p_colscale, fine_bwd=fine_bwd)
     nctx = lib().sage_ctx_bytes(ctypes.byref(p))
     if nctx == 0:
         raise SageError(f"unsupported shape/flags {tuple(xq.shape)}")

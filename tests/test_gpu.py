@@ -311,10 +311,11 @@ def test_full_size_long_sampled_head(cfg, heads):
 
 # ------------------------------------------------------------------ QK-norm variant
 QKN_CASES = [
-    # (B, H, N, d, causal, k_smooth, q_smooth)
-    (1, 2, 384, 64, True, True, False),
-    (1, 2, 256, 128, False, True, False),
-    (1, 2, 384, 128, True, True, True),
+    # (B, H, N, d, causal, k_smooth, q_smooth, fine_bwd)
+    (1, 2, 384, 64, True, True, False, False),
+    (1, 2, 256, 128, False, True, False, False),
+    (1, 2, 384, 128, True, True, True, False),
+    (1, 2, 256, 64, True, True, False, True),
 ]
 
 
@@ -326,15 +327,16 @@ def _qkn_inputs(B, H, N, d, seed):
     return xq, xk, v, do, gq, gk
 
 
-@pytest.mark.parametrize("B,H,N,d,causal,ks,qs", QKN_CASES)
-def test_qknorm_parity(B, H, N, d, causal, ks, qs):
+@pytest.mark.parametrize("B,H,N,d,causal,ks,qs,fine", QKN_CASES)
+def test_qknorm_parity(B, H, N, d, causal, ks, qs, fine):
     """sage_fwd_qknorm / sage_bwd_qknorm against oracle.qknorm + the quantised oracle:
     rstd, Q^, K^ and their scales bit-exact (Tier A: the fused normalisation produces exactly the
     bf16 Q, K of readings A24/A25); O, dX_q, dX_k, dV within the tolerance; dgamma likewise."""
     xq, xk, v, do, gq, gk = _qkn_inputs(B, H, N, d, seed=400 + N + d)
     dev = "cuda"
     xqd, xkd, vd, dod, gqd, gkd = (t.to(dev) for t in (xq, xk, v, do, gq, gk))
-    o, lse, ctx = sage.forward_qknorm(xqd, xkd, vd, gqd, gkd, 1e-6, causal=causal, k_smooth=ks, q_smooth=qs)
+    o, lse, ctx = sage.forward_qknorm(xqd, xkd, vd, gqd, gkd, 1e-6, causal=causal, k_smooth=ks, q_smooth=qs,
+                                      fine_bwd=fine)
     dxq, dxk, dv, dgq, dgk = sage.backward_qknorm(ctx, xqd, xkd, gqd, gkd, vd, o, lse, dod)
     torch.cuda.synchronize()
     BH = B * H
@@ -351,7 +353,7 @@ def test_qknorm_parity(B, H, N, d, causal, ks, qs):
     np.testing.assert_array_equal(view["q_scale"].cpu().numpy().reshape(BH, -1), f["sq"])
     np.testing.assert_array_equal(view["k_scale"].cpu().numpy().reshape(BH, -1), f["sk"])
     np.testing.assert_array_equal(view["mu_k"].cpu().numpy().reshape(BH, d), f["mu_k"])
-    b = oracle.bwd(qn_, kn_, flat(v), round_bf16(f["o"]), flat(do), f["lse"], **kw)
+    b = oracle.bwd(qn_, kn_, flat(v), round_bf16(f["o"]), flat(do), f["lse"], p_col=fine, ds_fine=fine, **kw)
     # A26: the module chain hands the bf16-rounded attention gradients to the RMSNorm backward
     dxq_r, dgq_r = oracle.qknorm.backward(flat(xq), gq.numpy(), rq, round_bf16(b["dq"]))
     dxk_r, dgk_r = oracle.qknorm.backward(flat(xk), gk.numpy(), rk, round_bf16(b["dk"]))
