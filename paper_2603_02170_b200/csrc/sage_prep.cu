@@ -254,9 +254,10 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T)
 // ---------------------------------------------------------------- Q-smoothing bias
 // bias[bh][i][n] = sum_c mu_Q[bh][i][c] * fl32(K[n][c] - mu_K[c]) in fp32, four partial sums over
 // c mod 4 (reading A13; fp32, so compared to the fp64 oracle within 1e-5 relative).  K2 and K4 read
-// the same stored bias, so the forward and the backward see identical logits.  CTA = (bh, 128-key block, group of kBiasI query blocks); thread = key n holds
-// its smoothed K row in registers, the group's mu_Q rows are broadcast from shared memory.
-constexpr int kBiasI = 16;
+// the same stored bias, so the forward and the backward see identical logits.
+// CTA = (bh, 128-key block, group of kBiasI query blocks); thread = key n holds its smoothed K row in
+// registers, the group's mu_Q rows are broadcast from shared memory.
+constexpr int kBiasI = 32;
 template <int D>
 __global__ void __launch_bounds__(128) qsmooth_bias_kernel(const __nv_bfloat16* __restrict__ k,
                                                            const float* __restrict__ mu_k,

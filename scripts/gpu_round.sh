@@ -12,3 +12,9 @@ for a in --qk-norm --p-u8 --fine-bwd --deterministic; do
 done
 TAG=$TAG CONFIGS="${NCU_CONFIGS:-C2 C3 C4}" bash scripts/gpu_evidence.sh > /dev/null 2>&1
 ls gpurun_out
+# summaries here (the .ncu-rep files are too large to bring back: gpurun_out is capped at 64 MiB)
+python scripts/ncu_summary.py json gpurun_out/ncu_summary_$TAG.json gpurun_out/prof_*.ncu-rep > /dev/null 2>&1
+for f in gpurun_out/prof_*.ncu-rep; do python scripts/ncu_summary.py rep $f; done > gpurun_out/ncu_$TAG.txt 2>&1
+ls -la gpurun_out/prof_*.ncu-rep > gpurun_out/ncu_reports_$TAG.txt
+rm -f gpurun_out/prof_*.ncu-rep
+du -sh gpurun_out

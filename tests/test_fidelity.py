@@ -284,3 +284,42 @@ def test_fidelity_fine_bwd_table1(dump_lib):
                                                   "SAGE_FINE_BWD", rows=rows))
     for name, paper in zip(("dq", "dk", "dv"), TABLE1[1.0][1:]):
         assert rows["1.0"][name]["gpu_rel_l2"] <= 1.45 * paper, (name, rows["1.0"])
+
+
+@pytest.mark.slow
+def test_fidelity_c5_qknorm_on_off(dump_lib):
+    """BASELINE.json C5 ("QK-norm on vs off ablation", N=8192 d=128 causal, K-smoothing) on one head:
+    the same pre-norm activations X (heterogeneous channels, sigma = 3: the recipe without RMSNorm)
+    fed to the path directly ("off") or through the fused QK-norm (sage_fwd_qknorm, gamma = 1, "on").
+    Errors against FPA in fp64 (for "on": FPA of the normalised Q, K, then the RMSNorm backward).
+    QK-norm must lower every gradient's error."""
+    B, H, N, d = 1, 1, 8192, 128
+    xq, xk, v, do = make_inputs(B, H, N, d, "noqknorm", seed=5000)
+    dev = torch.device("cuda")
+    xqd, xkd, vd, dod = (t.to(dev) for t in (xq, xk, v, do))
+    ones = torch.ones(d, dtype=torch.float32, device=dev)
+    flat = lambda t: f64(t).reshape(1, N, d)
+    oracle.set_threads(1)
+    rows = {}
+    # off: X is Q, K
+    o, lse, ctx = sage.forward(xqd, xkd, vd, causal=True)
+    dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
+    torch.cuda.synchronize()
+    ref = oracle.fpa(flat(xq), flat(xk), flat(v), flat(do), causal=True)
+    rows["off"] = {n: rel_l2(ref[n], flat(g)) for n, g in (("o", o), ("dq", dq), ("dk", dk), ("dv", dv))}
+    # on: fused QK-norm; FPA on the bf16 normalised Q, K (A25), RMSNorm backward of FPA's dQ, dK in fp64
+    o, lse, ctx = sage.forward_qknorm(xqd, xkd, vd, ones, ones, 1e-6, causal=True)
+    dxq, dxk, dv, _, _ = sage.backward_qknorm(ctx, xqd, xkd, ones, ones, vd, o, lse, dod)
+    torch.cuda.synchronize()
+    qn, rq = oracle.qknorm.forward(flat(xq), np.ones(d), 1e-6)
+    kn, rk = oracle.qknorm.forward(flat(xk), np.ones(d), 1e-6)
+    ref = oracle.fpa(qn, kn, flat(v), flat(do), causal=True)
+    dxq_r, _ = oracle.qknorm.backward(flat(xq), np.ones(d), rq, ref["dq"])
+    dxk_r, _ = oracle.qknorm.backward(flat(xk), np.ones(d), rk, ref["dk"])
+    rows["on"] = {"o": rel_l2(ref["o"], flat(o)), "dq": rel_l2(dxq_r, flat(dxq)), "dk": rel_l2(dxk_r, flat(dxk)),
+                  "dv": rel_l2(ref["dv"], flat(dv))}
+    _write_report("c5_qknorm_on_off", dict(setting="C5 shape, one head: B=1 H=1 N=8192 d=128 causal K-smooth, "
+                                                   "X = noqknorm recipe; 'on' = fused QK-norm (gamma = 1); "
+                                                   "dq/dk of 'on' are dX_q/dX_k", rows=rows))
+    for name in ("dq", "dk", "o"):
+        assert rows["on"][name] < rows["off"][name], rows
