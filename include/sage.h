@@ -19,7 +19,7 @@
  * all-zero blocks, causal masking, ...) are listed in DESIGN.md section 3.
  *
  * Conventions
- *   - Tensors Q, K, V, O, dO, dQ, dK, dV: bf16, contiguous [B, H, N, d] (d innermost),
+ *   - Tensors Q, K, V, O, dO, dQ, dK, dV: bf16 (fp16 with SAGE_FP16), contiguous [B, H, N, d] (d innermost),
  *     16-byte aligned device pointers.  N % 128 == 0, d in {64, 128}.
  *   - lse: fp32 [B, H, N], natural log (Alg. 1 line 14).
  *   - Ownership: the caller allocates every buffer (device memory), including the
@@ -78,13 +78,16 @@ enum {
                               128 queries) instead of one per tile; dV_j's drain applies it per row.
                               dV's error vs full precision drops ~2.6x at Table 1's sigma = 1.
                               Not combinable with SAGE_DETERMINISTIC (SAGE_ERR_INVALID_VALUE). */
-  SAGE_FINE_BWD = 1u << 7   /* variant (the paper's future work on the dS path,
+  SAGE_FINE_BWD = 1u << 7,  /* variant (the paper's future work on the dS path,
                               P:621-623): SAGE_P_COLSCALE plus psi(dS) (Alg. 2 line 9) taken twice,
                               with one scale per key for the dK operand and one per query for the dQ
                               operand (two int8 copies of the tile).  At Table 1's sigma = 1 it brings
                               dQ / dK / dV to 0.022 / 0.022 / 0.021 vs the paper's 0.018 / 0.022 /
                               0.016 (per-tile: 0.067 / 0.066 / 0.055).  Slower backward.  Not
                               combinable with SAGE_DETERMINISTIC. */
+  SAGE_FP16 = 1u << 8       /* fp16 instead of bf16 for Q, K, V, O, dO, dQ, dK, dV (and X_q, X_k, dX_q,
+                              dX_k with QK-norm, whose module output is then fp16): dP = dO V^T runs
+                              as an fp16 kind::f16 MMA, the paper's "FP16" option */
 };
 
 typedef struct {

@@ -66,7 +66,7 @@ size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Dims {
   size_t BH, N, d, T;
-  bool causal, ks, qs, pu8, qkn, det, pcol, fine;
+  bool causal, ks, qs, pu8, qkn, det, pcol, fine, fp16;
   float tau;
 };
 
@@ -76,7 +76,7 @@ bool dims_of(const sage_params* p, Dims* o) {
   if (p->head_dim != 64 && p->head_dim != 128) return false;
   if (p->seqlen % kBlk || p->seqlen > kMaxSeqLen) return false;
   if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH | SAGE_P_U8 | SAGE_QK_NORM | SAGE_DETERMINISTIC |
-                             SAGE_P_COLSCALE | SAGE_FINE_BWD))
+                             SAGE_P_COLSCALE | SAGE_FINE_BWD | SAGE_FP16))
     return false;
   if (!(p->softmax_scale >= 0.f) || std::isinf(p->softmax_scale)) return false;
   const size_t BH = (size_t)p->batch * p->heads;
@@ -93,6 +93,7 @@ bool dims_of(const sage_params* p, Dims* o) {
   o->det = p->flags & SAGE_DETERMINISTIC;
   o->pcol = p->flags & SAGE_P_COLSCALE;
   o->fine = p->flags & SAGE_FINE_BWD;
+  o->fp16 = p->flags & SAGE_FP16;
   if (o->det && (o->pcol || o->fine)) return false;  // one backward variant at a time
   o->tau = p->softmax_scale > 0.f ? p->softmax_scale : 1.f / std::sqrt((float)p->head_dim);
   return true;
@@ -208,9 +209,10 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, TmapType type, uint64_t rows
                   uint32_t box_cols) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
-  const uint32_t esz = type == kF32 ? 4 : type == kBF16 ? 2 : 1;
+  const uint32_t esz = type == kF32 ? 4 : (type == kBF16 || type == kF16) ? 2 : 1;
   const CUtensorMapDataType dt = type == kF32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                  : type == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                 : type == kF16  ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT8;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * esz};
@@ -346,9 +348,8 @@ sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v,
   if (st != SAGE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int BH = (int)D.BH, N = (int)D.N, d = (int)D.d;
-  const auto* qb = static_cast<const __nv_bfloat16*>(q);
-  const auto* kb = static_cast<const __nv_bfloat16*>(k);
-  const auto* vb = static_cast<const __nv_bfloat16*>(v);
+  const void *qb = q, *kb = k, *vb = v;  // bf16, or fp16 with SAGE_FP16
+  const bool h = D.fp16;
   int8_t *q8 = at<int8_t>(ctx, C.q8), *k8 = at<int8_t>(ctx, C.k8), *v8 = at<int8_t>(ws, W.v8);
   float *sq = at<float>(ctx, C.sq), *sk = at<float>(ctx, C.sk), *sv = at<float>(ws, W.sv);
   float* muk = at<float>(ctx, C.muk);
@@ -370,11 +371,11 @@ sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v,
   // QK-norm: the row statistics and normalised values are formed on the fly in K0/K1
   // K0: smoothing statistics
   if (D.ks) {
-    if ((e = launch_colsum(kb, partk, BH, N, d, s, nk)) != cudaSuccess) return cuda_fail(e);
+    if ((e = launch_colsum(kb, partk, BH, N, d, s, nk, h)) != cudaSuccess) return cuda_fail(e);
     if ((e = launch_colmean(partk, muk, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
   }
   if (D.qs) {
-    if ((e = launch_colsum(qb, partq, BH, N, d, s, nq)) != cudaSuccess) return cuda_fail(e);
+    if ((e = launch_colsum(qb, partq, BH, N, d, s, nq, h)) != cudaSuccess) return cuda_fail(e);
     if ((e = launch_blockmean(partq, muq, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
   }
   // K1: per-block psi (Alg. 1 line 3)
@@ -382,16 +383,17 @@ sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v,
   qj.j[0] = QuantJob{qb, muq, D.qs ? 2 : 0, q8, sq, rq, gq, eps};
   qj.j[1] = QuantJob{kb, muk, D.ks ? 1 : 0, k8, sk, rk, gk, eps};
   qj.j[2] = QuantJob{vb, nullptr, 0, v8, sv, nullptr, nullptr, 0.f};
-  if ((e = launch_quantize(qj, 3, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
+  if ((e = launch_quantize(qj, 3, BH, N, d, s, h)) != cudaSuccess) return cuda_fail(e);
   // mu_K is all-zero when K-smoothing is off (ctx is caller memory: make it so)
   if (!D.ks && (e = launch_fill(muk, D.BH * D.d, 0.f, s)) != cudaSuccess) return cuda_fail(e);
-  if (D.qs && (e = launch_qsmooth_bias(kb, muk, muq, bias, BH, N, d, s, nk)) != cudaSuccess) return cuda_fail(e);
+  if (D.qs && (e = launch_qsmooth_bias(kb, muk, muq, bias, BH, N, d, s, nk, h)) != cudaSuccess) return cuda_fail(e);
   // K2: fused INT8 forward (Alg. 1 lines 4-14)
   a.q_scale = sq;
   a.k_scale = sk;
   a.v_scale = sv;
   a.bias = bias;
-  a.o = static_cast<__nv_bfloat16*>(o);
+  a.o = o;
+  a.fp16 = D.fp16;
   a.lse = lse;
   a.BH = BH;
   a.N = N;
@@ -437,15 +439,14 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
   BwdArgs a{};
   const uint64_t rows = D.BH * D.N;
   if (!make_tmap_2d(&a.tm_q, q8, kU8, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_k, k8, kU8, rows, d, kBlk, d) ||
-      !make_tmap_2d(&a.tm_doq, do8, kU8, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_v, v, kBF16, rows, d, kBlk, 64) ||
-      !make_tmap_2d(&a.tm_do, dO, kBF16, rows, d, kBlk, 64) ||
+      !make_tmap_2d(&a.tm_doq, do8, kU8, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_v, v, D.fp16 ? kF16 : kBF16, rows, d, kBlk, 64) ||
+      !make_tmap_2d(&a.tm_do, dO, D.fp16 ? kF16 : kBF16, rows, d, kBlk, 64) ||
       !make_tmap_2d(&a.tm_dq, dqacc, kF32, rows, d, 32, 32))
     return cuda_fail(cudaErrorInvalidValue);
   cudaError_t e;
   // K3: delta, psi(dO), L*log2(e), zero dQ accumulator (Alg. 2 lines 2, 6)
   unsigned* dqflags = D.det ? at<unsigned>(ws, W.flags) : nullptr;
-  if ((e = launch_bwd_prep(static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dO), lse, delta,
-                           l2, do8, sdo, dqacc, BH, N, d, s, dqflags)) != cudaSuccess)
+  if ((e = launch_bwd_prep(o, dO, lse, delta, l2, do8, sdo, dqacc, BH, N, d, s, dqflags, D.fp16)) != cudaSuccess)
     return cuda_fail(e);
   // K4: fused INT8 backward (Alg. 2 lines 3-11)
   a.q_scale = sq;
@@ -456,8 +457,9 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
   a.bias = D.qs ? at<float>(cx, C.bias) : nullptr;
   a.mu_q = D.qs ? at<float>(cx, C.muq) : nullptr;
   a.dq_acc = dqacc;
-  a.dk = static_cast<__nv_bfloat16*>(dk);
-  a.dv = static_cast<__nv_bfloat16*>(dv);
+  a.dk = dk;
+  a.dv = dv;
+  a.fp16 = D.fp16;
   a.BH = BH;
   a.N = N;
   a.d = d;
@@ -476,19 +478,17 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
     // bf16 from K4) is turned into dX_k in place
     const auto* rq = at<const float>(cx, C.rq);
     const auto* rk = at<const float>(cx, C.rk);
-    auto* dqb = static_cast<__nv_bfloat16*>(dq);
-    auto* dkb = static_cast<__nv_bfloat16*>(dk);
-    if ((e = launch_norm_bwd(dqacc, nullptr, static_cast<const __nv_bfloat16*>(xq), rq, gq, dqb, at<float>(ws, W.gq),
-                             dgq, D.BH * D.N, d, s)) != cudaSuccess)
+    if ((e = launch_norm_bwd(dqacc, nullptr, xq, rq, gq, dq, at<float>(ws, W.gq),
+                             dgq, D.BH * D.N, d, s, D.fp16)) != cudaSuccess)
       return cuda_fail(e);
-    if ((e = launch_norm_bwd(nullptr, dkb, static_cast<const __nv_bfloat16*>(xk), rk, gk, dkb, at<float>(ws, W.gk),
-                             dgk, D.BH * D.N, d, s)) != cudaSuccess)
+    if ((e = launch_norm_bwd(nullptr, dk, xk, rk, gk, dk, at<float>(ws, W.gk),
+                             dgk, D.BH * D.N, d, s, D.fp16)) != cudaSuccess)
       return cuda_fail(e);
     if (g_prof.on) g_prof.launches += 6;  // 2 x (norm_bwd, dgamma stage 1, stage 2)
     return SAGE_OK;
   }
   // K5
-  if ((e = launch_dq_finalize(dqacc, static_cast<__nv_bfloat16*>(dq), D.BH * D.N * D.d, s)) != cudaSuccess)
+  if ((e = launch_dq_finalize(dqacc, dq, D.BH * D.N * D.d, s, D.fp16)) != cudaSuccess)
     return cuda_fail(e);
   if (g_prof.on) g_prof.launches += 1;  // K5
   return SAGE_OK;

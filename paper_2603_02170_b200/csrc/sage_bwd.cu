@@ -139,8 +139,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* __restrict__ q_scale,
                     const float* __restrict__ k_scale, const float* __restrict__ do_scale,
                     const float* __restrict__ l2g, const float* __restrict__ deltag, const float* __restrict__ bias,
-                    const float* __restrict__ mu_q, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dk,
-                    __nv_bfloat16* __restrict__ dv, int N, int BH, float tau, int pu8,
+                    const float* __restrict__ mu_q, float* __restrict__ dq_acc, void* __restrict__ dk_out,
+                    void* __restrict__ dv_out, int N, int BH, float tau, int pu8, int fp16,
                     unsigned* __restrict__ dq_flags, int ablate_arg) {
   constexpr bool fine = VAR == 3;
   constexpr bool pcol = VAR == 2 || fine;
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer (whole warp, one elected lane issues)
       constexpr uint32_t kIdS = idesc_i8(128, 128, false, false);     // S^T
-      constexpr uint32_t kIdDP = idesc_bf16(128, 128, false, false);  // dP^T
+      const uint32_t kIdDP = idesc_bf16(128, 128, false, false, fp16 != 0);  // dP^T (bf16 or fp16 V, dO)
       constexpr uint32_t kIdDV = idesc_i8(128, D, false, true);       // dK (B MN-major)
       const uint32_t kIdDVp = pu8 ? idesc_i8(128, D, false, true, true) : kIdDV;  // dV: A = P^^T, s8 or u8
       constexpr uint32_t kIdDQ = idesc_i8(128, D, true, true);        // dQ (A, B MN-major)
@@ -886,14 +886,14 @@ if (cm) {
       }
 #pragma unroll
       for (int e8 = 0; e8 < 32; e8 += 8) {
-        __nv_bfloat162 hk[4], hv[4];
+        uint32_t hk[4], hv[4];  // the I/O type: bf16, or fp16 with SAGE_FP16
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          hk[e] = __floats2bfloat162_rn(dk_acc[c0 + e8 + 2 * e], dk_acc[c0 + e8 + 2 * e + 1]);
-          hv[e] = __floats2bfloat162_rn(vv[e8 + 2 * e], vv[e8 + 2 * e + 1]);
+          hk[e] = pack2_io(dk_acc[c0 + e8 + 2 * e], dk_acc[c0 + e8 + 2 * e + 1], fp16);
+          hv[e] = pack2_io(vv[e8 + 2 * e], vv[e8 + 2 * e + 1], fp16);
         }
-        *reinterpret_cast<uint4*>(dk + orow + c0 + e8) = *reinterpret_cast<uint4*>(hk);
-        *reinterpret_cast<uint4*>(dv + orow + c0 + e8) = *reinterpret_cast<uint4*>(hv);
+        *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dk_out) + orow + c0 + e8) = make_uint4(hk[0], hk[1], hk[2], hk[3]);
+        *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dv_out) + orow + c0 + e8) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
       }
     }
   }
@@ -916,7 +916,7 @@ cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
   kern<<<a.BH * T, kThreads, kSmem, s>>>(a.tm_q, a.tm_k, a.tm_doq, a.tm_v, a.tm_do, a.tm_dq, a.q_scale,
                                                        a.k_scale, a.do_scale, a.l2, a.delta, a.bias, a.mu_q,
                                                        a.dq_acc, a.dk, a.dv, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
-                                                       a.dq_flags, a.ablate);
+                                                       a.fp16 ? 1 : 0, a.dq_flags, a.ablate);
   return cudaGetLastError();
 }
 

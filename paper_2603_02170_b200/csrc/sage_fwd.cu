@@ -70,8 +70,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     sage_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ q_scale,
                     const float* __restrict__ k_scale, const float* __restrict__ v_scale,
-                    const float* __restrict__ bias, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, int N,
-                    int BH, float tau, int pu8, int ablate_arg) {
+                    const float* __restrict__ bias, void* __restrict__ o_out, float* __restrict__ lse, int N,
+                    int BH, float tau, int pu8, int fp16, int ablate_arg) {
   const int ablate = SAGE_TRACE ? ablate_arg : 0;
   using L = FwdSmem<D>;
   constexpr int kStages = L::kStages;
@@ -391,13 +391,14 @@ __global__ void __launch_bounds__(kThreads, 2)
     correct(nj - 1, prev_alpha, prev_spv);
     // epilogue: O = acc / l (Alg. 1 line 13), L = m + ln l (line 14, natural log)
     const float inv_l = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* orow = o + ((size_t)row0 + r) * D;
+    // O in the I/O type (bf16, or fp16 with SAGE_FP16): 8 values per 16-byte store
+    uint4* orow = reinterpret_cast<uint4*>(static_cast<uint16_t*>(o_out) + ((size_t)row0 + r) * D);
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 8) {
-      __nv_bfloat162 h[4];
+      uint32_t h[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(oacc[c0 + 2 * e] * inv_l, oacc[c0 + 2 * e + 1] * inv_l);
-      *reinterpret_cast<uint4*>(orow + c0) = *reinterpret_cast<uint4*>(h);
+      for (int e = 0; e < 4; ++e) h[e] = pack2_io(oacc[c0 + 2 * e] * inv_l, oacc[c0 + 2 * e + 1] * inv_l, fp16);
+      orow[c0 / 8] = make_uint4(h[0], h[1], h[2], h[3]);
     }
     lse[(size_t)row0 + r] = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
   }
@@ -418,7 +419,7 @@ cudaError_t launch_t(const FwdArgs& a, cudaStream_t s) {
   const int T = a.N / kBlk;
   kern<<<a.BH * T, kThreads, FwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_v, a.q_scale, a.k_scale, a.v_scale,
                                                        a.bias, a.o, a.lse, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
-                                                       a.ablate);
+                                                       a.fp16 ? 1 : 0, a.ablate);
   return cudaGetLastError();
 }
 

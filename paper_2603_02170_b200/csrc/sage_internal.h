@@ -24,12 +24,11 @@ struct NormIn {
 // RMSNorm backward (reading A26): dx (bf16) from dy (fp32 dy32, or bf16 dy16 -- may alias dx), and
 // dgamma[d] via per-block partials gpart [rows/128][d] fp32 followed by [ceil(rows/128/64)][d] fp64
 // stage sums in the same buffer (fixed-order reduction).
-cudaError_t launch_norm_bwd(const float* dy32, const __nv_bfloat16* dy16, const __nv_bfloat16* x, const float* rstd,
-                            const float* gamma, __nv_bfloat16* dx, float* gpart, float* dgamma, size_t rows, int d,
-                            cudaStream_t s);
+cudaError_t launch_norm_bwd(const float* dy32, const void* dy16, const void* x, const float* rstd, const float* gamma,
+                            void* dx, float* gpart, float* dgamma, size_t rows, int d, cudaStream_t s, bool fp16);
 // K0: per-(head, 128-row chunk) column sums in double, fixed order (reading A17).
-cudaError_t launch_colsum(const __nv_bfloat16* x, double* part, int BH, int N, int d, cudaStream_t s,
-                          NormIn nrm = NormIn{nullptr, nullptr, 0.f});
+// Q, K, V, O, dO, dQ, dK, dV are bf16, or fp16 with SAGE_FP16 (`fp16` in the launchers below).
+cudaError_t launch_colsum(const void* x, double* part, int BH, int N, int d, cudaStream_t s, NormIn nrm, bool fp16);
 // K0b: mu[bh][c] = fl32(sum_t part[bh][t][c] / N)  (mu_K).
 cudaError_t launch_colmean(const double* part, float* mu, int BH, int N, int d, cudaStream_t s);
 // K0c: mu_Q[bh][t][c] = fl32(part[bh][t][c] / 128)  (block-wise mu_Qi).
@@ -37,7 +36,7 @@ cudaError_t launch_blockmean(const double* part, float* mu_q, int BH, int N, int
 // K1: per-block psi of x - mu (mu per column: mu_mode 0 none, 1 per head [BH][d], 2 per block [BH][T][d]),
 // up to three tensors in one launch.
 struct QuantJob {
-  const __nv_bfloat16* x;
+  const void* x;
   const float* mu;
   int mu_mode;
   int8_t* xq;
@@ -49,30 +48,31 @@ struct QuantJob {
 struct QuantJobs {
   QuantJob j[3];
 };
-cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int d, cudaStream_t s);
+cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int d, cudaStream_t s, bool fp16);
 // Q-smoothing bias_i[n] = mu_Qi . (K[n] - mu_K)  (reading A13), fp32.
-cudaError_t launch_qsmooth_bias(const __nv_bfloat16* k, const float* mu_k, const float* mu_q, float* bias, int BH,
-                                int N, int d, cudaStream_t s, NormIn nrm = NormIn{nullptr, nullptr, 0.f});
+cudaError_t launch_qsmooth_bias(const void* k, const float* mu_k, const float* mu_q, float* bias, int BH, int N, int d,
+                                cudaStream_t s, NormIn nrm, bool fp16);
 // K3: delta = rowsum(dO o O) (Alg. 2 line 2), psi(dO) (line 6, reading A22), l2 = lse*log2(e),
 //     dq_acc = 0.
-cudaError_t launch_bwd_prep(const __nv_bfloat16* o, const __nv_bfloat16* dO, const float* lse, float* delta,
-                            float* l2, int8_t* do_q, float* do_scale, float* dq_acc, int BH, int N, int d,
-                            cudaStream_t s, unsigned* dq_flags = nullptr);
+cudaError_t launch_bwd_prep(const void* o, const void* dO, const float* lse, float* delta, float* l2, int8_t* do_q,
+                            float* do_scale, float* dq_acc, int BH, int N, int d, cudaStream_t s, unsigned* dq_flags,
+                            bool fp16);
 cudaError_t launch_fill(float* x, size_t n, float v, cudaStream_t s);
 // K5: dQ fp32 -> bf16.
-cudaError_t launch_dq_finalize(const float* dq_acc, __nv_bfloat16* dq, size_t n, cudaStream_t s);
+cudaError_t launch_dq_finalize(const float* dq_acc, void* dq, size_t n, cudaStream_t s, bool fp16);
 
 // ---- fused tensor-core kernels ----
 struct FwdArgs {
   CUtensorMap tm_q, tm_k, tm_v;  // int8 [BH*N][d], box [128][d]
   const float *q_scale, *k_scale, *v_scale;
   const float* bias;  // [BH][T][N] or null
-  __nv_bfloat16* o;
+  void* o;     // bf16, or fp16 with SAGE_FP16
   float* lse;
   int BH, N, d;
   float tau;
   bool causal, qsmooth;
   bool pu8;    // SAGE_P_U8: P^ in 0..255 (u8 x s8 PV)
+  bool fp16;   // SAGE_FP16: fp16 I/O
   int ablate;  // profiling only (SAGE_ABLATE bit 8: timeline)
 };
 cudaError_t launch_fwd(const FwdArgs& a, cudaStream_t s);
@@ -87,11 +87,12 @@ struct BwdArgs {
   const float* bias;               // [BH][T][N] or null
   const float* mu_q;               // [BH][T][d] or null
   float* dq_acc;                   // [BH][N][d]
-  __nv_bfloat16 *dk, *dv;
+  void *dk, *dv;  // bf16, or fp16 with SAGE_FP16
   int BH, N, d;
   float tau;
   bool causal, qsmooth;
   bool pu8;    // SAGE_P_U8: psi(P) in 0..255 (u8 x s8 dV)
+  bool fp16;   // SAGE_FP16: fp16 V, dO (dP MMA kind::f16 with f16 operands) and outputs
   bool pcol;   // SAGE_P_COLSCALE: psi(P) per key row of P^T instead of per tile
   bool fine;   // SAGE_FINE_BWD: pcol + psi(dS) per key for dK and per query for dQ
   unsigned* dq_flags;  // SAGE_DETERMINISTIC: [BH][T][4] zeroed ordering flags, or null
@@ -113,7 +114,7 @@ cudaError_t launch_debug_umma(int mode, int K, int N, const CUtensorMap* tma, co
                               const void* a, void* d, cudaStream_t s);
 
 // Tensor-map helpers (sage_api.cu)
-enum TmapType { kU8 = 0, kBF16 = 1, kF32 = 2 };
+enum TmapType { kU8 = 0, kBF16 = 1, kF32 = 2, kF16 = 3 };
 bool make_tmap_2d(CUtensorMap* m, const void* base, TmapType type, uint64_t rows, uint64_t cols, uint32_t box_rows,
                   uint32_t box_cols);
 

@@ -9,6 +9,8 @@
 // Built without --use_fast_math; every FP32 op that decides a bit-exact INT8 value
 // is an explicit round-to-nearest intrinsic (__fsub_rn, __fmul_rn, __fdiv_rn) so
 // nvcc cannot contract it (reading A4).
+#include <cuda_fp16.h>
+
 #include "sage_internal.h"
 #include "sm100.cuh"
 
@@ -18,31 +20,46 @@ namespace {
 constexpr int kVec = 8;  // bf16 elements per 16-byte vector
 constexpr int nrm_smem_rows = 128;  // QK-norm partial sums of squares: [128 rows][column groups] doubles
 
-__device__ __forceinline__ void load_bf16x8(const __nv_bfloat16* p, float (&f)[8]) {
-  uint4 u = *reinterpret_cast<const uint4*>(p);
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    float2 t = __bfloat1622float2(h[e]);
-    f[2 * e] = t.x;
-    f[2 * e + 1] = t.y;
-  }
-}
+// I/O element type (bf16, or fp16 with SAGE_FP16): conversions of packed pairs and single values.
+template <typename T>
+struct Io;
+template <>
+struct Io<__nv_bfloat16> {
+  using T2 = __nv_bfloat162;
+  static __device__ __forceinline__ float2 to2(T2 h) { return __bfloat1622float2(h); }
+  static __device__ __forceinline__ T2 from2(float a, float b) { return __floats2bfloat162_rn(a, b); }
+  static __device__ __forceinline__ float to1(__nv_bfloat16 x) { return __bfloat162float(x); }
+  static __device__ __forceinline__ float round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+};
+template <>
+struct Io<__half> {
+  using T2 = __half2;
+  static __device__ __forceinline__ float2 to2(T2 h) { return __half22float2(h); }
+  static __device__ __forceinline__ T2 from2(float a, float b) { return __floats2half2_rn(a, b); }
+  static __device__ __forceinline__ float to1(__half x) { return __half2float(x); }
+  static __device__ __forceinline__ float round(float x) { return __half2float(__float2half_rn(x)); }
+};
 
-__device__ __forceinline__ void unpack_bf16x8(const uint4& u, float (&f)[8]) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+template <typename T>
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const typename Io<T>::T2* h = reinterpret_cast<const typename Io<T>::T2*>(&u);
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    float2 t = __bfloat1622float2(h[e]);
+    float2 t = Io<T>::to2(h[e]);
     f[2 * e] = t.x;
     f[2 * e + 1] = t.y;
   }
 }
-__device__ __forceinline__ uint4 pack_bf16x8(const float (&f)[8]) {
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float (&f)[8]) {
+  unpack8<T>(*reinterpret_cast<const uint4*>(p), f);
+}
+template <typename T>
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   uint4 u;
-  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+  typename Io<T>::T2* h = reinterpret_cast<typename Io<T>::T2*>(&u);
 #pragma unroll
-  for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+  for (int e = 0; e < 4; ++e) h[e] = Io<T>::from2(f[2 * e], f[2 * e + 1]);
   return u;
 }
 
@@ -57,10 +74,12 @@ __device__ __forceinline__ uint32_t quant4(const float* x, float inv) {
   return __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
 }
 
-// QK-norm output (readings A24/A25): y = bf16(fl32(fl32(x * rstd) * gamma)), the value an unfused
-// BF16 RMSNorm module would hand to the attention; every later step sees exactly these values.
+// QK-norm output (readings A24/A25): y = io(fl32(fl32(x * rstd) * gamma)), io = the I/O type (bf16, or
+// fp16 with SAGE_FP16): the value an unfused RMSNorm module would hand to the attention; every later
+// step sees exactly these values.
+template <typename T>
 __device__ __forceinline__ float qk_norm(float x, float r, float g) {
-  return __bfloat162float(__float2bfloat16_rn(__fmul_rn(__fmul_rn(x, r), g)));
+  return Io<T>::round(__fmul_rn(__fmul_rn(x, r), g));
 }
 
 // QK-norm row statistics of a 128-row chunk (reading A24): rstd = fl32(1 / sqrt(sum_c x^2 / D + eps)).
@@ -69,16 +88,16 @@ __device__ __forceinline__ float qk_norm(float x, float r, float g) {
 // span > 30 binades, so the order is immaterial) to shared memory, then one thread per row adds the
 // G partials and takes the IEEE double sqrt and division once, rounding to fp32 once.  Result in
 // rs_s[128] (and rstd_out[128] if non-null).  All 256 threads must call it.
-template <int G, int D, int NR, int RS>
+template <typename T, int G, int D, int NR, int RS>
 __device__ __forceinline__ void chunk_rstd(const uint4 (&raw)[NR], int g, int r0, double* ssq, float* rs_s, float eps,
                                            float* rstd_out) {
 #pragma unroll
   for (int k = 0; k < NR; ++k) {
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[k]);
+    const typename Io<T>::T2* h = reinterpret_cast<const typename Io<T>::T2*>(&raw[k]);
     double ss = 0.0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const float2 t = __bfloat1622float2(h[e]);
+      const float2 t = Io<T>::to2(h[e]);
       ss = fma((double)t.x, (double)t.x, ss);
       ss = fma((double)t.y, (double)t.y, ss);
     }
@@ -108,15 +127,15 @@ __device__ __forceinline__ float warp_max(float v) {
 // loads), then the R partials are combined in fixed order q = 0..R-1.  Sums of bf16 values in
 // double are exact unless a column spans > 53-8-log2(N) binades, so the order cannot change the
 // result for any realistic input; it is fixed anyway.
-template <int D, bool QKN>
-__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ x, double* __restrict__ part,
+template <typename T, int D, bool QKN>
+__global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, double* __restrict__ part,
                                                      NormIn nrm) {
   constexpr int kGroups = D / kVec;        // 8 (d=64) or 16 (d=128)
   constexpr int kR = 256 / kGroups;        // 32 or 16 row phases
   __shared__ double red[kR][D];
   const long long chunk = blockIdx.x;      // bh * T + t
   const int g = threadIdx.x % kGroups, q = threadIdx.x / kGroups;
-  const __nv_bfloat16* p = x + chunk * kBlk * D + g * kVec;
+  const T* p = x + chunk * kBlk * D + g * kVec;
   double acc[kVec];
   float gam[kVec];
 #pragma unroll
@@ -130,15 +149,15 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
   for (int k = 0; k < kRows; ++k) raw[k] = *reinterpret_cast<const uint4*>(p + (size_t)(q + k * kR) * D);
   __shared__ double ssq[QKN ? nrm_smem_rows * kGroups : 1];
   __shared__ float rs_s[QKN ? kBlk : 1];
-  if constexpr (QKN) chunk_rstd<kGroups, D, kRows, kR>(raw, g, q, ssq, rs_s, nrm.eps, nullptr);
+  if constexpr (QKN) chunk_rstd<T, kGroups, D, kRows, kR>(raw, g, q, ssq, rs_s, nrm.eps, nullptr);
 #pragma unroll
   for (int k = 0; k < kRows; ++k) {
     float f[kVec];
-    unpack_bf16x8(raw[k], f);
+    unpack8<T>(raw[k], f);
     if constexpr (QKN) {  // QK-norm (A24/A25)
       const float rs = rs_s[q + k * kR];
 #pragma unroll
-      for (int e = 0; e < kVec; ++e) f[e] = qk_norm(f[e], rs, gam[e]);
+      for (int e = 0; e < kVec; ++e) f[e] = qk_norm<T>(f[e], rs, gam[e]);
     }
 #pragma unroll
     for (int e = 0; e < kVec; ++e) acc[e] += (double)f[e];
@@ -174,11 +193,11 @@ __global__ void blockmean_kernel(const double* __restrict__ part, float* __restr
 // ---------------------------------------------------------------- K1: psi
 // One CTA quantises one 128 x d block: x_sm = fl32(x - mu); amax; scale = fl32(amax/127);
 // inv = fl32(127/amax) (0 for an all-zero block, A3); q = clamp(RNE(fl32(x_sm*inv)), +-127).
-template <int D, bool QKN>
+template <typename TI, int D, bool QKN>
 __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T) {
   // blockIdx.y selects the tensor (Q, K, V): one launch for all three psi passes
   const QuantJob& job = jobs.j[blockIdx.y];
-  const __nv_bfloat16* __restrict__ x = job.x;
+  const TI* __restrict__ x = static_cast<const TI*>(job.x);
   const float* __restrict__ mu = job.mu;
   const int mu_mode = job.mu_mode;
   int8_t* __restrict__ xq = job.xq;
@@ -191,7 +210,7 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T)
   const long long blk = blockIdx.x;               // bh * T + t
   const int bh = (int)(blk / T), t = (int)(blk % T);
   const int g = threadIdx.x % kGroups, r0 = threadIdx.x / kGroups;
-  const __nv_bfloat16* xb = x + blk * kBlk * D;
+  const TI* xb = x + blk * kBlk * D;
   float m[kVec];
 #pragma unroll
   for (int e = 0; e < kVec; ++e) {
@@ -208,21 +227,22 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T)
   __shared__ double ssq[QKN ? nrm_smem_rows * kGroups : 1];
   __shared__ float rs_s[QKN ? kBlk : 1];
   if constexpr (QKN) {
-    if (job.gamma) chunk_rstd<kGroups, D, kIters, kRowsPerPass>(raw, g, r0, ssq, rs_s, job.eps, job.rstd + blk * kBlk);
+    if (job.gamma)
+      chunk_rstd<TI, kGroups, D, kIters, kRowsPerPass>(raw, g, r0, ssq, rs_s, job.eps, job.rstd + blk * kBlk);
   }
   float amax = 0.f;
 #pragma unroll
   for (int it = 0; it < kIters; ++it) {
     float v[kVec];
-    unpack_bf16x8(raw[it], v);
+    unpack8<TI>(raw[it], v);
     if (QKN && job.gamma) {  // QK-norm (A25) before the smoothing subtraction
       float gam[kVec];
 #pragma unroll
       for (int e = 0; e < kVec; ++e) gam[e] = job.gamma[g * kVec + e];
       const float rs = rs_s[r0 + it * kRowsPerPass];
 #pragma unroll
-      for (int e = 0; e < kVec; ++e) v[e] = qk_norm(v[e], rs, gam[e]);
-      raw[it] = pack_bf16x8(v);  // exact: qk_norm values are bf16
+      for (int e = 0; e < kVec; ++e) v[e] = qk_norm<TI>(v[e], rs, gam[e]);
+      raw[it] = pack8<TI>(v);  // exact: qk_norm values are I/O-type values
     }
 #pragma unroll
     for (int e = 0; e < kVec; ++e) amax = fmaxf(amax, fabsf(__fsub_rn(v[e], m[e])));
@@ -241,7 +261,7 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T)
   for (int it = 0; it < kIters; ++it) {
     int r = r0 + it * kRowsPerPass;
     float v[kVec];
-    unpack_bf16x8(raw[it], v);
+    unpack8<TI>(raw[it], v);
 #pragma unroll
     for (int e = 0; e < kVec; ++e) v[e] = __fsub_rn(v[e], m[e]);
     uint32_t w[2];
@@ -258,8 +278,8 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T)
 // CTA = (bh, 128-key block, group of kBiasI query blocks); thread = key n holds its smoothed K row in
 // registers, the group's mu_Q rows are broadcast from shared memory.
 constexpr int kBiasI = 32;
-template <int D>
-__global__ void __launch_bounds__(128) qsmooth_bias_kernel(const __nv_bfloat16* __restrict__ k,
+template <typename TI, int D>
+__global__ void __launch_bounds__(128) qsmooth_bias_kernel(const TI* __restrict__ k,
                                                            const float* __restrict__ mu_k,
                                                            const float* __restrict__ mu_q, float* __restrict__ bias,
                                                            int N, NormIn nrm) {
@@ -272,16 +292,19 @@ __global__ void __launch_bounds__(128) qsmooth_bias_kernel(const __nv_bfloat16* 
   for (int e = threadIdx.x; e < ni * (D / 4); e += blockDim.x)
     mq[e / (D / 4)][e % (D / 4)] = reinterpret_cast<const float4*>(mu_q + ((size_t)bh * T + i0) * D)[e];
   float ks[D];
-  const __nv_bfloat16* krow = k + (blk * kBlk + n) * D;
+  const TI* krow = k + (blk * kBlk + n) * D;
   const float* mk = mu_k + (size_t)bh * D;
   const float rs = nrm.gamma ? nrm.rstd[blk * kBlk + n] : 1.f;  // written by K1's K job
+  uint4 raw[D / kVec];  // the whole K row in flight before any use (the loads' latency dominates)
+#pragma unroll
+  for (int c8 = 0; c8 < D / kVec; ++c8) raw[c8] = *reinterpret_cast<const uint4*>(krow + c8 * kVec);
 #pragma unroll
   for (int c = 0; c < D; c += kVec) {
     float f[kVec];
-    load_bf16x8(krow + c, f);
+    unpack8<TI>(raw[c / kVec], f);
     if (nrm.gamma) {
 #pragma unroll
-      for (int e = 0; e < kVec; ++e) f[e] = qk_norm(f[e], rs, nrm.gamma[c + e]);
+      for (int e = 0; e < kVec; ++e) f[e] = qk_norm<TI>(f[e], rs, nrm.gamma[c + e]);
     }
     const float4 m0 = *reinterpret_cast<const float4*>(mk + c), m1 = *reinterpret_cast<const float4*>(mk + c + 4);
     const float mm[kVec] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
@@ -292,6 +315,7 @@ __global__ void __launch_bounds__(128) qsmooth_bias_kernel(const __nv_bfloat16* 
   float* out = bias + ((size_t)bh * T + i0) * N + (size_t)jn * kBlk + n;
   // FFMA2 over column pairs (c, c+1): mu_Q's float4 and the K row are already register pairs, so no
   // repacking; two query blocks per pass and two accumulator pairs each (8 partial sums) for ILP
+#pragma unroll 1
   for (int ii = 0; ii < ni; ii += 2) {
     const int i1 = ii + 1 < ni ? ii + 1 : ii;
     float2 a0 = make_float2(0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
@@ -311,9 +335,8 @@ __global__ void __launch_bounds__(128) qsmooth_bias_kernel(const __nv_bfloat16* 
 }
 
 // ---------------------------------------------------------------- K3: backward prep
-template <int D>
-__global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
-                                                       const __nv_bfloat16* __restrict__ dO,
+template <typename T, int D>
+__global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, const T* __restrict__ dO,
                                                        const float* __restrict__ lse, float* __restrict__ delta,
                                                        float* __restrict__ l2, int8_t* __restrict__ do_q,
                                                        float* __restrict__ do_scale, float* __restrict__ dq_acc,
@@ -327,13 +350,18 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
   const size_t base = (size_t)blk * kBlk * D;
   float v[kIters][kVec];
   float amax = 0.f;
+  // dO rows in flight before any arithmetic (kIters 16-byte loads per thread); O's alongside
+  uint4 rdo[kIters];
+#pragma unroll
+  for (int it = 0; it < kIters; ++it)
+    rdo[it] = *reinterpret_cast<const uint4*>(dO + base + (size_t)(r0 + it * kRowsPerPass) * D + g * kVec);
 #pragma unroll
   for (int it = 0; it < kIters; ++it) {
     const int r = r0 + it * kRowsPerPass;
     const size_t off = base + (size_t)r * D + g * kVec;
     float fo[kVec];
-    load_bf16x8(dO + off, v[it]);
-    load_bf16x8(o + off, fo);
+    unpack8<T>(rdo[it], v[it]);
+    load8<T>(o + off, fo);
     float dot = 0.f;
 #pragma unroll
     for (int e = 0; e < kVec; ++e) {
@@ -375,14 +403,14 @@ __global__ void fill_kernel(float* __restrict__ x, size_t n, float v) {
   if (i < n) x[i] = v;
 }
 
-__global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq, size_t n8) {
+template <typename T>
+__global__ void dq_finalize_kernel(const float* __restrict__ acc, T* __restrict__ dq, size_t n8) {
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n8) return;
   float4 a = reinterpret_cast<const float4*>(acc)[2 * i];
   float4 b = reinterpret_cast<const float4*>(acc)[2 * i + 1];
-  __nv_bfloat162 h[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
-                         __floats2bfloat162_rn(b.x, b.y), __floats2bfloat162_rn(b.z, b.w)};
-  reinterpret_cast<uint4*>(dq)[i] = *reinterpret_cast<uint4*>(h);
+  const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  reinterpret_cast<uint4*>(dq)[i] = pack8<T>(f);
 }
 
 // ---------------------------------------------------------------- QK-norm backward
@@ -391,11 +419,11 @@ __global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16*
 // dy = bf16(attention gradient) (from the fp32 dQ accumulator, or the bf16 dK in place),
 // g = dy o gamma, xh = x rstd, dx = rstd (g - xh mean(g o xh)) -> bf16;  gpart[block][c] = sum
 // over the block's rows of dy o xh (fixed order: rows within a warp, then warps 0..7).
-template <int D>
-__global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__ dy32, const __nv_bfloat16* dy16,
-                                                       const __nv_bfloat16* __restrict__ x,
+template <typename T, int D>
+__global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__ dy32, const T* dy16,
+                                                       const T* __restrict__ x,
                                                        const float* __restrict__ rstd, const float* __restrict__ gamma,
-                                                       __nv_bfloat16* dx, float* __restrict__ gpart) {
+                                                       T* dx, float* __restrict__ gpart) {
   constexpr int kPer = D / 32;  // 4 or 2
   constexpr int kRows = 16;
   __shared__ float red[8][D];
@@ -415,26 +443,26 @@ __global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__
     rs[rr] = rstd[row0 + rr];
     if constexpr (kPer == 4) {
       const uint2 xu = *reinterpret_cast<const uint2*>(x + off);
-      const float2 x0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xu.x));
-      const float2 x1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xu.y));
+      const float2 x0 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(&xu.x));
+      const float2 x1 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(&xu.y));
       xv[rr][0] = x0.x; xv[rr][1] = x0.y; xv[rr][2] = x1.x; xv[rr][3] = x1.y;
       if (dy32) {
         const float4 f = *reinterpret_cast<const float4*>(dy32 + off);
         dy[rr][0] = f.x; dy[rr][1] = f.y; dy[rr][2] = f.z; dy[rr][3] = f.w;
       } else {
         const uint2 du = *reinterpret_cast<const uint2*>(dy16 + off);
-        const float2 d0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&du.x));
-        const float2 d1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&du.y));
+        const float2 d0 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(&du.x));
+        const float2 d1 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(&du.y));
         dy[rr][0] = d0.x; dy[rr][1] = d0.y; dy[rr][2] = d1.x; dy[rr][3] = d1.y;
       }
     } else {
-      const float2 x0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + off));
+      const float2 x0 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(x + off));
       xv[rr][0] = x0.x; xv[rr][1] = x0.y;
       if (dy32) {
         const float2 f = *reinterpret_cast<const float2*>(dy32 + off);
         dy[rr][0] = f.x; dy[rr][1] = f.y;
       } else {
-        const float2 d0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dy16 + off));
+        const float2 d0 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(dy16 + off));
         dy[rr][0] = d0.x; dy[rr][1] = d0.y;
       }
     }
@@ -445,7 +473,7 @@ __global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__
     dot[rr] = 0.f;
 #pragma unroll
     for (int e = 0; e < kPer; ++e) {
-      if (dy32) dy[rr][e] = __bfloat162float(__float2bfloat16_rn(dy[rr][e]));  // A26
+      if (dy32) dy[rr][e] = Io<T>::round(dy[rr][e]);  // A26
       xv[rr][e] *= rs[rr];                                                    // xh
       gacc[e] = fmaf(dy[rr][e], xv[rr][e], gacc[e]);
       dy[rr][e] *= gam[e];                                                    // g
@@ -461,15 +489,15 @@ __global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__
   for (int rr = 0; rr < kRows; ++rr) {
     const size_t off = (row0 + rr) * D + lane * kPer;
     const float mean = dot[rr] * (1.f / D);
-    __nv_bfloat162 h[kPer / 2];
+    typename Io<T>::T2 h[kPer / 2];
 #pragma unroll
     for (int e = 0; e < kPer; e += 2)
-      h[e / 2] = __floats2bfloat162_rn(rs[rr] * fmaf(-xv[rr][e], mean, dy[rr][e]),
+      h[e / 2] = Io<T>::from2(rs[rr] * fmaf(-xv[rr][e], mean, dy[rr][e]),
                                        rs[rr] * fmaf(-xv[rr][e + 1], mean, dy[rr][e + 1]));
     if constexpr (kPer == 4)
       *reinterpret_cast<uint2*>(dx + off) = *reinterpret_cast<const uint2*>(h);
     else
-      *reinterpret_cast<__nv_bfloat162*>(dx + off) = h[0];
+      *reinterpret_cast<typename Io<T>::T2*>(dx + off) = h[0];
   }
 #pragma unroll
   for (int e = 0; e < kPer; ++e) red[warp][lane * kPer + e] = gacc[e];
@@ -502,30 +530,49 @@ __global__ void dgamma_stage2_kernel(const double* __restrict__ part2, float* __
 
 }  // namespace
 
-cudaError_t launch_colsum(const __nv_bfloat16* x, double* part, int BH, int N, int d, cudaStream_t s, NormIn nrm) {
+// I/O type dispatch: every launcher takes void pointers and the SAGE_FP16 choice
+#define SAGE_IO_DISPATCH(fp16, ...)        \
+  do {                                     \
+    if (fp16) {                            \
+      using IoT = __half;                  \
+      __VA_ARGS__;                         \
+    } else {                               \
+      using IoT = __nv_bfloat16;           \
+      __VA_ARGS__;                         \
+    }                                      \
+  } while (0)
+
+cudaError_t launch_colsum(const void* x, double* part, int BH, int N, int d, cudaStream_t s, NormIn nrm, bool fp16) {
   const unsigned grid = (unsigned)(BH * (N / kBlk));
-  if (nrm.gamma) {
-    if (d == 128)
-      colsum_kernel<128, true><<<grid, 256, 0, s>>>(x, part, nrm);
-    else
-      colsum_kernel<64, true><<<grid, 256, 0, s>>>(x, part, nrm);
-  } else {
-    if (d == 128)
-      colsum_kernel<128, false><<<grid, 256, 0, s>>>(x, part, nrm);
-    else
-      colsum_kernel<64, false><<<grid, 256, 0, s>>>(x, part, nrm);
-  }
+  SAGE_IO_DISPATCH(fp16, {
+    const IoT* xt = static_cast<const IoT*>(x);
+    if (nrm.gamma) {
+      if (d == 128)
+        colsum_kernel<IoT, 128, true><<<grid, 256, 0, s>>>(xt, part, nrm);
+      else
+        colsum_kernel<IoT, 64, true><<<grid, 256, 0, s>>>(xt, part, nrm);
+    } else {
+      if (d == 128)
+        colsum_kernel<IoT, 128, false><<<grid, 256, 0, s>>>(xt, part, nrm);
+      else
+        colsum_kernel<IoT, 64, false><<<grid, 256, 0, s>>>(xt, part, nrm);
+    }
+  });
   return cudaGetLastError();
 }
 
-cudaError_t launch_norm_bwd(const float* dy32, const __nv_bfloat16* dy16, const __nv_bfloat16* x, const float* rstd,
-                            const float* gamma, __nv_bfloat16* dx, float* gpart, float* dgamma, size_t rows, int d,
-                            cudaStream_t s) {
+cudaError_t launch_norm_bwd(const float* dy32, const void* dy16, const void* x, const float* rstd, const float* gamma,
+                            void* dx, float* gpart, float* dgamma, size_t rows, int d, cudaStream_t s, bool fp16) {
   const unsigned nblk = (unsigned)(rows / kBlk);
-  if (d == 128)
-    norm_bwd_kernel<128><<<nblk, 256, 0, s>>>(dy32, dy16, x, rstd, gamma, dx, gpart);
-  else
-    norm_bwd_kernel<64><<<nblk, 256, 0, s>>>(dy32, dy16, x, rstd, gamma, dx, gpart);
+  SAGE_IO_DISPATCH(fp16, {
+    const IoT* dyt = static_cast<const IoT*>(dy16);
+    const IoT* xt = static_cast<const IoT*>(x);
+    IoT* dxt = static_cast<IoT*>(dx);
+    if (d == 128)
+      norm_bwd_kernel<IoT, 128><<<nblk, 256, 0, s>>>(dy32, dyt, xt, rstd, gamma, dxt, gpart);
+    else
+      norm_bwd_kernel<IoT, 64><<<nblk, 256, 0, s>>>(dy32, dyt, xt, rstd, gamma, dxt, gpart);
+  });
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // the stage-1 sums (double) follow the nblk x d block partials in the same workspace slot
@@ -549,44 +596,53 @@ cudaError_t launch_blockmean(const double* part, float* mu_q, int BH, int N, int
   return cudaGetLastError();
 }
 
-cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int d, cudaStream_t s) {
+cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int d, cudaStream_t s, bool fp16) {
   int T = N / kBlk;
   dim3 grid((unsigned)(BH * T), (unsigned)njobs);
   bool qkn = false;
   for (int i = 0; i < njobs; ++i) qkn = qkn || jobs.j[i].gamma;
-  if (qkn) {
-    if (d == 128)
-      quantize_kernel<128, true><<<grid, 256, 0, s>>>(jobs, T);
-    else
-      quantize_kernel<64, true><<<grid, 256, 0, s>>>(jobs, T);
-  } else {
-    if (d == 128)
-      quantize_kernel<128, false><<<grid, 256, 0, s>>>(jobs, T);
-    else
-      quantize_kernel<64, false><<<grid, 256, 0, s>>>(jobs, T);
-  }
+  SAGE_IO_DISPATCH(fp16, {
+    if (qkn) {
+      if (d == 128)
+        quantize_kernel<IoT, 128, true><<<grid, 256, 0, s>>>(jobs, T);
+      else
+        quantize_kernel<IoT, 64, true><<<grid, 256, 0, s>>>(jobs, T);
+    } else {
+      if (d == 128)
+        quantize_kernel<IoT, 128, false><<<grid, 256, 0, s>>>(jobs, T);
+      else
+        quantize_kernel<IoT, 64, false><<<grid, 256, 0, s>>>(jobs, T);
+    }
+  });
   return cudaGetLastError();
 }
 
-cudaError_t launch_qsmooth_bias(const __nv_bfloat16* k, const float* mu_k, const float* mu_q, float* bias, int BH,
-                                int N, int d, cudaStream_t s, NormIn nrm) {
+cudaError_t launch_qsmooth_bias(const void* k, const float* mu_k, const float* mu_q, float* bias, int BH, int N, int d,
+                                cudaStream_t s, NormIn nrm, bool fp16) {
   const int T = N / kBlk;
   dim3 grid((unsigned)(BH * T), (unsigned)((T + kBiasI - 1) / kBiasI));
-  if (d == 128)
-    qsmooth_bias_kernel<128><<<grid, 128, 0, s>>>(k, mu_k, mu_q, bias, N, nrm);
-  else
-    qsmooth_bias_kernel<64><<<grid, 128, 0, s>>>(k, mu_k, mu_q, bias, N, nrm);
+  SAGE_IO_DISPATCH(fp16, {
+    const IoT* kt = static_cast<const IoT*>(k);
+    if (d == 128)
+      qsmooth_bias_kernel<IoT, 128><<<grid, 128, 0, s>>>(kt, mu_k, mu_q, bias, N, nrm);
+    else
+      qsmooth_bias_kernel<IoT, 64><<<grid, 128, 0, s>>>(kt, mu_k, mu_q, bias, N, nrm);
+  });
   return cudaGetLastError();
 }
 
-cudaError_t launch_bwd_prep(const __nv_bfloat16* o, const __nv_bfloat16* dO, const float* lse, float* delta,
-                            float* l2, int8_t* do_q, float* do_scale, float* dq_acc, int BH, int N, int d,
-                            cudaStream_t s, unsigned* dq_flags) {
+cudaError_t launch_bwd_prep(const void* o, const void* dO, const float* lse, float* delta, float* l2, int8_t* do_q,
+                            float* do_scale, float* dq_acc, int BH, int N, int d, cudaStream_t s, unsigned* dq_flags,
+                            bool fp16) {
   unsigned grid = (unsigned)(BH * (N / kBlk));
-  if (d == 128)
-    bwd_prep_kernel<128><<<grid, 256, 0, s>>>(o, dO, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
-  else
-    bwd_prep_kernel<64><<<grid, 256, 0, s>>>(o, dO, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
+  SAGE_IO_DISPATCH(fp16, {
+    const IoT* ot = static_cast<const IoT*>(o);
+    const IoT* dot = static_cast<const IoT*>(dO);
+    if (d == 128)
+      bwd_prep_kernel<IoT, 128><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
+    else
+      bwd_prep_kernel<IoT, 64><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
+  });
   return cudaGetLastError();
 }
 
@@ -595,9 +651,10 @@ cudaError_t launch_fill(float* x, size_t n, float v, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_dq_finalize(const float* dq_acc, __nv_bfloat16* dq, size_t n, cudaStream_t s) {
+cudaError_t launch_dq_finalize(const float* dq_acc, void* dq, size_t n, cudaStream_t s, bool fp16) {
   size_t n8 = n / 8;
-  dq_finalize_kernel<<<(unsigned)((n8 + 255) / 256), 256, 0, s>>>(dq_acc, dq, n8);
+  SAGE_IO_DISPATCH(fp16, dq_finalize_kernel<IoT><<<(unsigned)((n8 + 255) / 256), 256, 0, s>>>(
+                             dq_acc, static_cast<IoT*>(dq), n8));
   return cudaGetLastError();
 }
 

@@ -6,6 +6,7 @@
 // and "instruction descriptor" tables (restated in CUTLASS's
 // cute/arch/mma_sm100_desc.hpp, used as reference material only).
 #pragma once
+#include <cuda_fp16.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -287,8 +288,9 @@ __host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N, bool a_m
   return (2u << 4) | ((a_u8 ? 0u : 1u) << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
          ((N >> 3) << 17) | ((M >> 4) << 24);
 }
-__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, bool a_mn, bool b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+// kind::f16 A/B formats: 0 = f16, 1 = bf16 (bits 7-9 / 10-12); fp16 for SAGE_FP16's dP
+__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, bool a_mn, bool b_mn, bool fp16 = false) {
+  return (1u << 4) | ((fp16 ? 0u : 1u) << 7) | ((fp16 ? 0u : 1u) << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
          ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
@@ -409,6 +411,15 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   p = ffma2(p, f, make_float2(1.0f, 1.0f));
   return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(j.x) << 23)),
                      __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(j.y) << 23)));
+}
+// two fp32 values -> one 32-bit word of the I/O type: bf16x2, or fp16x2 with SAGE_FP16 (RNE)
+__device__ __forceinline__ uint32_t pack2_io(float a, float b, bool fp16) {
+  if (fp16) {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;

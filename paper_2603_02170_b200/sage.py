@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("SAGE_LIB") or os.path.join(_HERE, "libsage.so")
 
 SAGE_CAUSAL, SAGE_K_SMOOTH, SAGE_Q_SMOOTH, SAGE_P_U8, SAGE_QK_NORM, SAGE_DETERMINISTIC, SAGE_P_COLSCALE = \
     1, 2, 4, 8, 16, 32, 64
-SAGE_FINE_BWD = 128
+SAGE_FINE_BWD, SAGE_FP16 = 128, 256
 _STATUS = {0: "SAGE_OK", 1: "SAGE_ERR_INVALID_VALUE", 2: "SAGE_ERR_UNSUPPORTED", 3: "SAGE_ERR_MISALIGNED",
            4: "SAGE_ERR_WORKSPACE", 5: "SAGE_ERR_CUDA", 6: "SAGE_ERR_ARCH"}
 
@@ -94,10 +94,10 @@ def _check(status, what):
 
 
 def make_params(batch, heads, seqlen, head_dim, causal=False, k_smooth=True, q_smooth=False, softmax_scale=None,
-                p_u8=False, qk_norm=False, deterministic=False, p_colscale=False, fine_bwd=False):
+                p_u8=False, qk_norm=False, deterministic=False, p_colscale=False, fine_bwd=False, fp16=False):
     flags = (SAGE_CAUSAL if causal else 0) | (SAGE_K_SMOOTH if k_smooth else 0) | (SAGE_Q_SMOOTH if q_smooth else 0) | \
         (SAGE_P_U8 if p_u8 else 0) | (SAGE_QK_NORM if qk_norm else 0) | (SAGE_DETERMINISTIC if deterministic else 0) | \
-        (SAGE_P_COLSCALE if p_colscale else 0) | (SAGE_FINE_BWD if fine_bwd else 0)
+        (SAGE_P_COLSCALE if p_colscale else 0) | (SAGE_FINE_BWD if fine_bwd else 0) | (SAGE_FP16 if fp16 else 0)
     return SageParams(batch, heads, seqlen, head_dim, flags, 0.0 if softmax_scale is None else softmax_scale)
 
 
@@ -111,12 +111,13 @@ def _stream(stream):
 
 
 def _check_io(*ts):
+    """All tensors contiguous CUDA [B, H, N, d] of one I/O dtype: bf16, or fp16 (SAGE_FP16)."""
     ref = ts[0]
     for t in ts:
-        if not (t.is_cuda and t.dtype == torch.bfloat16 and t.is_contiguous() and t.dim() == 4):
-            raise SageError("tensors must be contiguous CUDA bf16 [B, H, N, d]")
-        if t.shape != ref.shape or t.device != ref.device:
-            raise SageError("shape/device mismatch")
+        if not (t.is_cuda and t.dtype in (torch.bfloat16, torch.float16) and t.is_contiguous() and t.dim() == 4):
+            raise SageError("tensors must be contiguous CUDA bf16 or fp16 [B, H, N, d]")
+        if t.shape != ref.shape or t.device != ref.device or t.dtype != ref.dtype:
+            raise SageError("shape/device/dtype mismatch")
 
 
 class SageCtx:
@@ -191,7 +192,7 @@ def forward(q, k, v, causal=False, k_smooth=True, q_smooth=False, softmax_scale=
     _check_io(q, k, v)
     B, H, N, d = q.shape
     p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8, deterministic=deterministic,
-                    p_colscale=p_colscale, fine_bwd=fine_bwd)
+                    p_colscale=p_colscale, fine_bwd=fine_bwd, fp16=q.dtype == torch.float16)
     nctx = lib().sage_ctx_bytes(ctypes.byref(p))
     if nctx == 0:
         raise SageError(f"unsupported shape/flags {tuple(q.shape)} (N % 128 == 0, d in {{64, 128}})")
@@ -205,8 +206,10 @@ def forward(q, k, v, causal=False, k_smooth=True, q_smooth=False, softmax_scale=
 
 
 def backward(ctx, v, o, lse, do, dq=None, dk=None, dv=None, workspace=None, stream=None):
-    """sage_bwd (Alg. 2): returns (dq, dk, dv) in bf16."""
+    """sage_bwd (Alg. 2): returns (dq, dk, dv) in the I/O dtype."""
     _check_io(v, o, do)
+    if (do.dtype == torch.float16) != bool(ctx.params.flags & SAGE_FP16):
+        raise SageError("the backward's dtype differs from the forward's")
     dq = torch.empty_like(do) if dq is None else dq
     dk = torch.empty_like(do) if dk is None else dk
     dv = torch.empty_like(do) if dv is None else dv
@@ -232,7 +235,8 @@ def forward_qknorm(xq, xk, v, gamma_q, gamma_k, eps=1e-6, causal=False, k_smooth
     _check_gamma(gamma_q, d, xq.device)
     _check_gamma(gamma_k, d, xq.device)
     p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8, qk_norm=True,
-                    deterministic=deterministic, p_colscale=p_colscale, fine_bwd=fine_bwd)
+                    deterministic=deterministic, p_colscale=p_colscale, fine_bwd=fine_bwd,
+                    fp16=xq.dtype == torch.float16)
     nctx = lib().sage_ctx_bytes(ctypes.byref(p))
     if nctx == 0:
         raise SageError(f"unsupported shape/flags {tuple(xq.shape)}")

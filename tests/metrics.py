@@ -31,3 +31,8 @@ def f64(t):
 def round_bf16(x):
     """Round a float64 array to bf16 (RNE) and back, for comparison after identical rounding (A18)."""
     return torch.from_numpy(np.asarray(x, dtype=np.float64)).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+def round_fp16(x):
+    """Round a float64 array to fp16 (RNE) and back (the SAGE_FP16 I/O type)."""
+    return torch.from_numpy(np.asarray(x, dtype=np.float64)).to(torch.float16).to(torch.float64).numpy()

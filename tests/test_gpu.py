@@ -12,7 +12,7 @@ import torch
 import oracle
 from paper_2603_02170_b200 import sage
 from paper_2603_02170_b200.inputs import CONFIGS, make_inputs
-from tests.metrics import cos_sim, f64, rel_l2, round_bf16
+from tests.metrics import cos_sim, f64, rel_l2, round_bf16, round_fp16
 
 pytestmark = pytest.mark.gpu
 
@@ -380,3 +380,65 @@ def test_qknorm_autograd_and_rejections():
     assert torch.equal(o, o2)
     for g1, g2 in zip((xq.grad, xk.grad, v.grad, gq.grad, gk.grad), ref):
         assert rel_l2(f64(g2), f64(g1)) < 1e-3
+
+
+
+# ------------------------------------------------------------------ fp16 I/O (SAGE_FP16)
+FP16_CASES = [
+    (1, 2, 384, 64, True, True, False, "qknorm"),
+    (1, 2, 256, 128, False, True, False, "gauss"),
+    (1, 2, 384, 128, True, True, True, "outlier_kq"),
+]
+
+
+@pytest.mark.parametrize("B,H,N,d,causal,ks,qs,recipe", FP16_CASES)
+def test_fp16_parity(B, H, N, d, causal, ks, qs, recipe):
+    """fp16 Q, K, V, dO (the paper's "FP16" dP option): Q^, K^ and their scales bit-exact
+    (Tier A); O, dQ, dK, dV within the tolerance against the oracle, O stored as fp16 (A15) and both
+    sides rounded to fp16 for the comparison (A18)."""
+    q, k, v, do = make_inputs(B, H, N, d, recipe, seed=900 + N + d, dtype=torch.float16)
+    gpu = _run(q, k, v, do, causal, ks, qs)
+    assert gpu["o"].dtype == torch.float16 and gpu["dq"].dtype == torch.float16
+    BH = B * H
+    flat = lambda t: f64(t).reshape(BH, N, d)
+    kw = dict(causal=causal, k_smooth=ks, q_smooth=qs)
+    f = oracle.fwd(flat(q), flat(k), flat(v), **kw)
+    b = oracle.bwd(flat(q), flat(k), flat(v), round_fp16(f["o"]), flat(do), f["lse"], **kw)
+    view = gpu["ctx"].view()
+    np.testing.assert_array_equal(view["q_i8"].cpu().numpy().reshape(BH, N, d), f["q8"])
+    np.testing.assert_array_equal(view["k_i8"].cpu().numpy().reshape(BH, N, d), f["k8"])
+    np.testing.assert_array_equal(view["k_scale"].cpu().numpy().reshape(BH, -1), f["sk"])
+    for name, ref in (("o", f["o"]), ("dq", b["dq"]), ("dk", b["dk"]), ("dv", b["dv"])):
+        ref = round_fp16(ref)
+        got = flat(gpu[name])
+        rl, cs = rel_l2(ref, got), cos_sim(ref, got)
+        assert rl <= REL_TOL and cs >= COS_TOL, (name, rl, cs)
+
+
+def test_fp16_qknorm_and_dtype_checks():
+    """fp16 through the fused QK-norm (the module output is then fp16, A25) against the oracle, and
+    the binding's dtype checks."""
+    B, H, N, d = 1, 2, 256, 64
+    xq, xk, v, do, gq, gk = _qkn_inputs(B, H, N, d, seed=77)
+    xq, xk, v, do = (t.to(torch.float16) for t in (xq, xk, v, do))
+    dev = "cuda"
+    xqd, xkd, vd, dod, gqd, gkd = (t.to(dev) for t in (xq, xk, v, do, gq, gk))
+    o, lse, ctx = sage.forward_qknorm(xqd, xkd, vd, gqd, gkd, 1e-6, causal=True)
+    dxq, dxk, dv, dgq, dgk = sage.backward_qknorm(ctx, xqd, xkd, gqd, gkd, vd, o, lse, dod)
+    torch.cuda.synchronize()
+    flat = lambda t: f64(t).reshape(B * H, N, d)
+    # the oracle's QK-norm with an fp16 module output (A25 with the I/O type)
+    rq = oracle.qknorm.rstd(flat(xq), 1e-6)
+    rk = oracle.qknorm.rstd(flat(xk), 1e-6)
+    qn = round_fp16((flat(xq).astype(np.float32) * rq[..., None]).astype(np.float32) * gq.numpy())
+    kn = round_fp16((flat(xk).astype(np.float32) * rk[..., None]).astype(np.float32) * gk.numpy())
+    np.testing.assert_array_equal(ctx.view()["rstd_q"].cpu().numpy().reshape(B * H, N), rq)
+    f = oracle.fwd(qn, kn, flat(v), causal=True)
+    np.testing.assert_array_equal(ctx.view()["q_i8"].cpu().numpy().reshape(B * H, N, d), f["q8"])
+    b = oracle.bwd(qn, kn, flat(v), round_fp16(f["o"]), flat(do), f["lse"], causal=True)
+    dxq_r, _ = oracle.qknorm.backward(flat(xq), gq.numpy(), rq, round_fp16(b["dq"]))
+    for name, got, ref in (("o", o, f["o"]), ("dxq", dxq, dxq_r), ("dv", dv, b["dv"])):
+        rl = rel_l2(round_fp16(ref), flat(got))
+        assert rl <= REL_TOL, (name, rl)
+    with pytest.raises(sage.SageError):
+        sage.forward(xqd, xkd.to(torch.bfloat16), vd)
