@@ -40,6 +40,11 @@ CONFIGS = {
     "C4": Config("C4", 2, 32, 16384, 128, True, True, False, "qknorm", 4000),
     "C5": Config("C5", 16, 16, 8192, 128, True, True, False, "qknorm", 5000),
 }
+# The metric's sequence-length sweep ("TOPS ... at seqlen 1K-32K", BASELINE.json; SURVEY.md 8(d)
+# C4-sweep): N in {1K, ..., 32K}, B = 32768 / N, H = 32, d = 128, causal, QK-normed inputs.
+for _n in (1024, 2048, 4096, 8192, 16384, 32768):
+    _name = f"S{_n // 1024}K"
+    CONFIGS[_name] = Config(_name, 32768 // _n, 32, _n, 128, True, True, False, "qknorm", 6000 + _n // 1024)
 
 
 def _rmsnorm(x, gamma, eps=1e-6):
