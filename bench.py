@@ -222,6 +222,8 @@ def main():
     ap.add_argument("--impl", default="sage", choices=["sage", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-chunks", type=int, default=0,
+                    help="head chunks of the pipelined e2e step (0: about 16 MB of inputs per chunk, at most 16)")
     ap.add_argument("--qk-norm", action="store_true",
                     help="QK-norm fused in front of the path (sage_fwd_qknorm / sage_bwd_qknorm, C5's ablation)")
     ap.add_argument("--p-u8", action="store_true", help="unsigned P^ variant (SAGE_P_U8)")
@@ -305,7 +307,9 @@ def main():
     outs_h = [torch.empty_like(h).pin_memory() for h in host]
     e2e_ms = []
     BH = c.batch * c.heads
-    n_chunks = 1 if (args.qk_norm or args.e2e_steps == 0) else min(8, BH)
+    in_bytes = sum(h.numel() * h.element_size() for h in host)
+    auto_chunks = max(1, min(16, in_bytes // (16 << 20)))  # measured: 8 at C2, 16 at C3
+    n_chunks = 1 if (args.qk_norm or args.e2e_steps == 0) else min(args.e2e_chunks or auto_chunks, BH)
     bounds = [(BH * i // n_chunks, BH * (i + 1) // n_chunks) for i in range(n_chunks)]
     flat = lambda t: t.view(BH, c.seqlen, c.head_dim)
     chunk = lambda t, a, b: flat(t)[a:b].unsqueeze(0)  # [1, heads of the chunk, N, d], contiguous
