@@ -279,7 +279,10 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T)
 // registers, the group's mu_Q rows are broadcast from shared memory.
 constexpr int kBiasI = 32;
 template <typename TI, int D>
-__global__ void __launch_bounds__(128) qsmooth_bias_kernel(const TI* __restrict__ k,
+#ifndef SAGE_BIAS_MINB
+#define SAGE_BIAS_MINB 1
+#endif
+__global__ void __launch_bounds__(128, SAGE_BIAS_MINB) qsmooth_bias_kernel(const TI* __restrict__ k,
                                                            const float* __restrict__ mu_k,
                                                            const float* __restrict__ mu_q, float* __restrict__ bias,
                                                            int N, NormIn nrm) {
