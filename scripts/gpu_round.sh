@@ -10,7 +10,7 @@ TAG=$TAG CONFIGS="C3 C4 C5" bash scripts/gpu_bench_all.sh > /dev/null 2>&1
 for a in --qk-norm --p-u8 --fine-bwd --deterministic; do
   timeout 600 python bench.py --config C5 --steps 10 --warmup 3 --no-cpu-baseline $a > gpurun_out/bench_${TAG}_C5${a//-/_}.json 2> /dev/null
 done
-TAG=$TAG CONFIGS="${NCU_CONFIGS:-C2 C3 C4}" bash scripts/gpu_evidence.sh > /dev/null 2>&1
+TAG=$TAG CONFIGS="${NCU_CONFIGS:-C2 C3 C4}" EXTRA_K="${EXTRA_K}" bash scripts/gpu_evidence.sh > /dev/null 2>&1
 ls gpurun_out
 # summaries here (the .ncu-rep files are too large to bring back: gpurun_out is capped at 64 MiB)
 python scripts/ncu_summary.py json gpurun_out/ncu_summary_$TAG.json gpurun_out/prof_*.ncu-rep > /dev/null 2>&1
