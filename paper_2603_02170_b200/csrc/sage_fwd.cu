@@ -32,6 +32,10 @@ constexpr float kLog2_255 = 7.994353436858858f;
 // Groups of 4 (of the 8 per 32-column chunk) whose exponentials run on the FMA pipe (ex2_poly2), at
 // d=128 (measured: 1 group = 12.5% of the exponentials, C4 K2 4.52 -> 4.40 ms; 2 neutral, 3 slower;
 // none at d=64, where it does not help)
+// softmax warpgroup registers (setmaxnreg); the other warpgroup gets 256 - this (2 CTAs per SM)
+#ifndef SAGE_K2_REGS
+#define SAGE_K2_REGS 216  // measured: 184 -> 216 takes C3 K2 0.966 -> 0.893 ms, C4 4.39 -> 4.35 ms
+#endif
 #ifndef SAGE_K2_POLY
 #define SAGE_K2_POLY 1
 #endif
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   constexpr bool kPTmem = D == 64;
 
   if (warp >= 4) {
-    reg_dealloc<72>();
+    reg_dealloc<256 - SAGE_K2_REGS>();
     if (warp == 4) {
       // ---------------------------------------------------------- TMA producer
       if (elect_one()) {
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
   } else {
-    reg_alloc<184>();
+    reg_alloc<SAGE_K2_REGS>();
     // ------------------------------------------------------------ softmax / correction (128 threads)
     const int r = threadIdx.x;  // query row within the block == TMEM lane
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
