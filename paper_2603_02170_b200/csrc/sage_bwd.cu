@@ -91,6 +91,15 @@ struct BwdSmem {
 
 // Profiling hooks (timeline + ablation switches) exist only in the SAGE_TRACE=1 build
 // (libsage_trace.so); the production library compiles them out.
+#ifndef SAGE_K4_RP
+#define SAGE_K4_RP 56
+#endif
+#ifndef SAGE_K4_RC64
+#define SAGE_K4_RC64 144  // measured: 136 -> 144 takes C2 K4 0.521 -> 0.516 ms; 152 slower (0.543)
+#endif
+#ifndef SAGE_K4_RC128
+#define SAGE_K4_RC128 128
+#endif
 #ifndef SAGE_TRACE
 #define SAGE_TRACE 0
 #endif
@@ -151,7 +160,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kStages = L::kStages;
   constexpr bool kAlias = D == 128;
   // setmaxnreg budgets (x128 threads each; sum = 512 regs/thread-slot = the 64K register file)
-  constexpr uint32_t kRegProducer = 56, kRegCompute = D == 64 ? 136 : 128, kRegDrain = D == 64 ? 184 : 200;
+  // setmaxnreg budget per warpgroup (sums to 4 x 128): producer/MMA, 2 x compute, drain gets the rest
+  constexpr uint32_t kRegProducer = SAGE_K4_RP, kRegCompute = D == 64 ? SAGE_K4_RC64 : SAGE_K4_RC128,
+                     kRegDrain = 512 - kRegProducer - 2 * kRegCompute;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment (128B swizzle atoms) by offsetting the __shared__ array itself, so every
   // derived pointer stays in the shared window (LDS/STS, not generic LD/ST)
