@@ -36,6 +36,8 @@ def _load():
         I, D = ctypes.c_int, ctypes.c_double
         _lib.oracle_fwd.argtypes = [I, I, I, I, I, D] + [P] * 14
         _lib.oracle_bwd.argtypes = [I, I, I, I, I, D] + [P] * 17
+        _lib.oracle_fwd_sel.argtypes = [I, I, I, I, I, D] + [P] * 15
+        _lib.oracle_bwd_sel.argtypes = [I, I, I, I, I, D] + [P] * 19
         _lib.oracle_fpa.argtypes = [I, I, I, I, D] + [P] * 13
         _lib.oracle_psi_block.argtypes = [P, I, I, P, P]
         _lib.oracle_psi_token_row.argtypes = [P, I, D, I, P]
@@ -88,11 +90,24 @@ def _flags(causal, k_smooth, q_smooth, quant, p_u8, p_col=False, ds_fine=False):
         (0 if quant else QUANT_OFF) | (P_U8 if p_u8 else 0) | (P_COL if p_col else 0) | (DS_FINE if ds_fine else 0)
 
 
-def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk=128, tau=None, p_u8=False):
-    """Alg. 1 per head.  Returns dict with o, lse and the Tier-A intermediates."""
+def _sel(blocks, BH, T):
+    """None, or a [BH][T] uint8 selection from a list of block indices (the same for every head)."""
+    if blocks is None:
+        return None
+    m = np.zeros((BH, T), np.uint8)
+    m[:, list(blocks)] = 1
+    return m
+
+
+def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk=128, tau=None, p_u8=False,
+        q_blocks=None):
+    """Alg. 1 per head.  Returns dict with o, lse and the Tier-A intermediates.
+    q_blocks: compute O and L only for these query blocks (other rows stay zero), with the same
+    arithmetic as the full run (sampled checks at sizes the full oracle cannot finish)."""
     q, k, v = _f64(q), _f64(k), _f64(v)
     BH, N, d = q.shape
     T = N // blk
+    qsel = _sel(q_blocks, BH, T)
     flags = _flags(causal, k_smooth, q_smooth, quant, p_u8)
     out = dict(o=np.zeros((BH, N, d)), lse=np.zeros((BH, N)),
                mu_k=np.zeros((BH, d), np.float32), mu_q=np.zeros((BH, T, d), np.float32),
@@ -101,7 +116,7 @@ def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk
                v8=np.zeros((BH, N, d), np.int8),
                sq=np.zeros((BH, T), np.float32), sk=np.zeros((BH, T), np.float32),
                sv=np.zeros((BH, T), np.float32))
-    rc = _load().oracle_fwd(BH, N, d, blk, flags, _default_tau(d, tau), _p(q), _p(k), _p(v),
+    rc = _load().oracle_fwd_sel(BH, N, d, blk, flags, _default_tau(d, tau), _p(q), _p(k), _p(v), _p(qsel),
                             _p(out["o"]), _p(out["lse"]), _p(out["mu_k"]), _p(out["mu_q"]),
                             _p(out["bias"]), _p(out["q8"]), _p(out["k8"]), _p(out["v8"]),
                             _p(out["sq"]), _p(out["sk"]), _p(out["sv"]))
@@ -111,7 +126,7 @@ def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk
 
 
 def bwd(q, k, v, o_stored, do, lse, *, causal=False, k_smooth=True, q_smooth=False, quant=True,
-        blk=128, tau=None, tiles=False, p_u8=False, p_col=False, ds_fine=False):
+        blk=128, tau=None, tiles=False, p_u8=False, p_col=False, ds_fine=False, q_blocks=None, k_blocks=None):
     """Alg. 2 per head.  o_stored is the O the forward stored (A15).
 
     tiles=True also returns the per-tile quantised P^ / dS^ ([BH, N q, N kv] uint8 / int8, tile (i, j) at
@@ -119,10 +134,16 @@ def bwd(q, k, v, o_stored, do, lse, *, causal=False, k_smooth=True, q_smooth=Fal
     pre-psi dS ([BH, N, N] double); tiles a causal run skips stay zero.  p_col=True: psi(P) per key
     column of each tile (ORC_P_COL); the dumped s_P is then the tile's largest column scale.
     ds_fine=True: psi(dS) per query row for dQ and per key column for dK (ORC_DS_FINE); the dumped dS^
-    is then the dK operand."""
+    is then the dK operand.
+    q_blocks / k_blocks (either given): process only the tiles of these query / key blocks; dQ is
+    computed for q_blocks and dK, dV for k_blocks (other rows stay zero), bitwise as in the full run."""
     q, k, v, o_stored, do, lse = map(_f64, (q, k, v, o_stored, do, lse))
     BH, N, d = q.shape
     T = N // blk
+    if q_blocks is not None or k_blocks is not None:
+        qsel, ksel = _sel(q_blocks or [], BH, T), _sel(k_blocks or [], BH, T)
+    else:
+        qsel = ksel = None
     flags = _flags(causal, k_smooth, q_smooth, quant, p_u8, p_col, ds_fine)
     out = dict(dq=np.zeros((BH, N, d)), dk=np.zeros((BH, N, d)), dv=np.zeros((BH, N, d)),
                delta=np.zeros((BH, N)), do8=np.zeros((BH, N, d), np.int8),
@@ -131,8 +152,8 @@ def bwd(q, k, v, o_stored, do, lse, *, causal=False, k_smooth=True, q_smooth=Fal
         out.update(p8=np.zeros((BH, N, N), np.uint8), sp=np.zeros((BH, T, T), np.float32),
                    ds8=np.zeros((BH, N, N), np.int8), sds=np.zeros((BH, T, T), np.float32),
                    ds=np.zeros((BH, N, N)))
-    rc = _load().oracle_bwd(BH, N, d, blk, flags, _default_tau(d, tau), _p(q), _p(k), _p(v),
-                            _p(o_stored), _p(do), _p(lse), _p(out["dq"]), _p(out["dk"]),
+    rc = _load().oracle_bwd_sel(BH, N, d, blk, flags, _default_tau(d, tau), _p(q), _p(k), _p(v),
+                            _p(o_stored), _p(do), _p(lse), _p(qsel), _p(ksel), _p(out["dq"]), _p(out["dk"]),
                             _p(out["dv"]), _p(out["delta"]), _p(out["do8"]), _p(out["sdo"]),
                             _p(out.get("p8")), _p(out.get("sp")), _p(out.get("ds8")), _p(out.get("sds")),
                             _p(out.get("ds")))

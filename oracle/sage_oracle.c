@@ -238,8 +238,10 @@ static void s_tile(const head_prep *h, int i, int j, double tau, double *S) {
 /* Alg. 1: forward, per head, with the corrections of reading A7:
  *   m_0 = -inf (size B_q), l_ij = e^{m_{i,j-1}-m_ij} l_{i,j-1} + rowsum(P~_ij),
  *   O_ij = diag(e^{m_{i,j-1}-m_ij}) O_{i,j-1} + MM(P^_ij, V^_j) x s_P x s_V.   */
+/* qsel (may be NULL = every block): compute O and L only for the query blocks i with qsel[i] != 0 (the
+ * other rows of o / lse are left untouched).  The selected blocks run exactly the same arithmetic. */
 static void fwd_head(const double *q, const double *k, const double *v, int N, int d, int blk,
-                     int flags, double tau, double *o, double *lse,
+                     int flags, double tau, const uint8_t *qsel, double *o, double *lse,
                      float *mu_k, float *mu_q, double *bias,
                      int8_t *q8o, int8_t *k8o, int8_t *v8o, float *sqo, float *sko, float *svo) {
   head_prep h;
@@ -262,6 +264,7 @@ static void fwd_head(const double *q, const double *k, const double *v, int N, i
   double *m = malloc(blk * sizeof(double)), *l = malloc(blk * sizeof(double));
 
   for (int i = 0; i < T; ++i) {
+    if (qsel && !qsel[i]) continue;
     for (int r = 0; r < blk; ++r) { m[r] = -INFINITY; l[r] = 0.0; }
     memset(acc, 0, (size_t)blk * d * sizeof(double));
     int jmax = causal ? i : T - 1;
@@ -319,17 +322,19 @@ static void fwd_head(const double *q, const double *k, const double *v, int N, i
   prep_free(&h);
 }
 
-int oracle_fwd(int BH, int N, int d, int blk, int flags, double tau,
-               const double *q, const double *k, const double *v,
-               double *o, double *lse,
-               float *mu_k, float *mu_q, double *bias,
-               int8_t *q8, int8_t *k8, int8_t *v8, float *sq, float *sk, float *sv) {
+/* qsel: NULL, or [BH][T] query-block selection (see fwd_head). */
+int oracle_fwd_sel(int BH, int N, int d, int blk, int flags, double tau,
+                   const double *q, const double *k, const double *v, const uint8_t *qsel,
+                   double *o, double *lse,
+                   float *mu_k, float *mu_q, double *bias,
+                   int8_t *q8, int8_t *k8, int8_t *v8, float *sq, float *sk, float *sv) {
   if (BH <= 0 || N <= 0 || d <= 0 || blk <= 0 || N % blk) return -1;
   int T = N / blk;
   size_t nd = (size_t)N * d;
 #pragma omp parallel for schedule(dynamic, 1)
   for (int b = 0; b < BH; ++b) {
-    fwd_head(q + b * nd, k + b * nd, v + b * nd, N, d, blk, flags, tau, o + b * nd, lse + (size_t)b * N,
+    fwd_head(q + b * nd, k + b * nd, v + b * nd, N, d, blk, flags, tau, qsel ? qsel + (size_t)b * T : NULL,
+             o + b * nd, lse + (size_t)b * N,
              mu_k ? mu_k + (size_t)b * d : NULL, mu_q ? mu_q + (size_t)b * T * d : NULL,
              bias ? bias + (size_t)b * T * N : NULL,
              q8 ? q8 + b * nd : NULL, k8 ? k8 + b * nd : NULL, v8 ? v8 + b * nd : NULL,
@@ -338,12 +343,24 @@ int oracle_fwd(int BH, int N, int d, int blk, int flags, double tau,
   return 0;
 }
 
+int oracle_fwd(int BH, int N, int d, int blk, int flags, double tau,
+               const double *q, const double *k, const double *v,
+               double *o, double *lse,
+               float *mu_k, float *mu_q, double *bias,
+               int8_t *q8, int8_t *k8, int8_t *v8, float *sq, float *sk, float *sv) {
+  return oracle_fwd_sel(BH, N, d, blk, flags, tau, q, k, v, NULL, o, lse, mu_k, mu_q, bias, q8, k8, v8, sq, sk, sv);
+}
+
 /* ------------------------------------------------------------------------ */
 /* Alg. 2: backward, per head.  Outer loop over kv blocks j, inner over q
  * blocks i.  o_stored is the O the forward wrote (A15), lse its L.
  * dP = dO_i V_j^T (A8) is exact in double from the I/O values (A9).          */
+/* qsel / ksel (both NULL = every block): only tiles (i, j) with qsel[i] or ksel[j] are processed; dQ_i is
+ * accumulated for the selected query blocks and dK_j, dV_j for the selected key blocks (the other rows
+ * stay zero).  A selected output receives exactly the tiles, in exactly the order, of the full run. */
 static void bwd_head(const double *q, const double *k, const double *v, const double *o_stored,
-                     const double *dO, const double *lse, int N, int d, int blk, int flags, double tau,
+                     const double *dO, const double *lse, const uint8_t *qsel, const uint8_t *ksel,
+                     int N, int d, int blk, int flags, double tau,
                      double *dq, double *dk, double *dv, double *delta_out, int8_t *do8_out, float *sdo_out,
                      uint8_t *p8_out, float *sp_out, int8_t *ds8_out, float *sds_out, double *ds_out) {
   head_prep h;
@@ -379,8 +396,11 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
   memset(dk, 0, nd * sizeof(double));
   memset(dv, 0, nd * sizeof(double));
 
+  int all = !qsel && !ksel;
   for (int j = 0; j < T; ++j) {
     for (int i = causal ? j : 0; i < T; ++i) {
+      int want_q = all || (qsel && qsel[i]), want_k = all || (ksel && ksel[j]);
+      if (!want_q && !want_k) continue;
       /* line 5: S_ij recomputed from Q^, K^; P_ij = exp(S_ij - L_i). */
       s_tile(&h, i, j, tau, S);
       for (int r = 0; r < blk; ++r)
@@ -417,7 +437,7 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
               a += (int32_t)Px[(size_t)r * blk + n] * (int32_t)do8[(size_t)(i * blk + r) * d + c];
             val = (double)a * spcol[n] * sdo[i];
           }
-          dv[(size_t)(j * blk + n) * d + c] += val;
+          if (want_k) dv[(size_t)(j * blk + n) * d + c] += val;
         }
       /* line 8: dP_ij = MM(dO_i, V_j^T), kept unquantised (A8, A9).
        * line 9: dS_ij = P_ij o (dP_ij - D_i). */
@@ -467,7 +487,7 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
               a += (int32_t)dSq8[(size_t)r * blk + n] * (int32_t)h.k8[(size_t)(j * blk + n) * d + c];
             val = (double)a * sq_row[r] * h.sk[j] * tau;
           }
-          dq[(size_t)(i * blk + r) * d + c] += val;
+          if (want_q) dq[(size_t)(i * blk + r) * d + c] += val;
         }
       /* line 11: dK_j += MM(dS^_ij^T, Q^_i) x s_dS x s_Q  (x tau, A6);
        * with Q-smoothing also dK_bias = (dS^T 1) mu_Q^T  (A13). */
@@ -487,7 +507,7 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
             val = (double)a * sk_col[n] * h.sq[i] * tau;
           }
           if (flags & ORC_Q_SMOOTH) val += tau * (qo ? 1.0 : sk_col[n]) * colsum * h.mu_q[(size_t)i * d + c];
-          dk[(size_t)(j * blk + n) * d + c] += val;
+          if (want_k) dk[(size_t)(j * blk + n) * d + c] += val;
         }
       }
     }
@@ -500,18 +520,20 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
   prep_free(&h);
 }
 
-int oracle_bwd(int BH, int N, int d, int blk, int flags, double tau,
-               const double *q, const double *k, const double *v, const double *o_stored,
-               const double *dO, const double *lse,
-               double *dq, double *dk, double *dv,
-               double *delta, int8_t *do8, float *sdo,
-               uint8_t *p8, float *sp, int8_t *ds8, float *sds, double *ds) {
+/* qsel, ksel: NULL, or [BH][T] query / key block selections (see bwd_head). */
+int oracle_bwd_sel(int BH, int N, int d, int blk, int flags, double tau,
+                   const double *q, const double *k, const double *v, const double *o_stored,
+                   const double *dO, const double *lse, const uint8_t *qsel, const uint8_t *ksel,
+                   double *dq, double *dk, double *dv,
+                   double *delta, int8_t *do8, float *sdo,
+                   uint8_t *p8, float *sp, int8_t *ds8, float *sds, double *ds) {
   if (BH <= 0 || N <= 0 || d <= 0 || blk <= 0 || N % blk) return -1;
   int T = N / blk;
   size_t nd = (size_t)N * d;
 #pragma omp parallel for schedule(dynamic, 1)
   for (int b = 0; b < BH; ++b) {
     bwd_head(q + b * nd, k + b * nd, v + b * nd, o_stored + b * nd, dO + b * nd, lse + (size_t)b * N,
+             qsel ? qsel + (size_t)b * T : NULL, ksel ? ksel + (size_t)b * T : NULL,
              N, d, blk, flags, tau, dq + b * nd, dk + b * nd, dv + b * nd,
              delta ? delta + (size_t)b * N : NULL, do8 ? do8 + b * nd : NULL,
              sdo ? sdo + (size_t)b * T : NULL,
@@ -520,6 +542,16 @@ int oracle_bwd(int BH, int N, int d, int blk, int flags, double tau,
              ds ? ds + (size_t)b * N * N : NULL);
   }
   return 0;
+}
+
+int oracle_bwd(int BH, int N, int d, int blk, int flags, double tau,
+               const double *q, const double *k, const double *v, const double *o_stored,
+               const double *dO, const double *lse,
+               double *dq, double *dk, double *dv,
+               double *delta, int8_t *do8, float *sdo,
+               uint8_t *p8, float *sp, int8_t *ds8, float *sds, double *ds) {
+  return oracle_bwd_sel(BH, N, d, blk, flags, tau, q, k, v, o_stored, dO, lse, NULL, NULL, dq, dk, dv, delta, do8,
+                        sdo, p8, sp, ds8, sds, ds);
 }
 
 /* ------------------------------------------------------------------------ */
