@@ -36,7 +36,7 @@ def _load():
         I, D = ctypes.c_int, ctypes.c_double
         _lib.oracle_fwd.argtypes = [I, I, I, I, I, D] + [P] * 14
         _lib.oracle_bwd.argtypes = [I, I, I, I, I, D] + [P] * 17
-        _lib.oracle_fwd_sel.argtypes = [I, I, I, I, I, D] + [P] * 15
+        _lib.oracle_fwd_sel.argtypes = [I, I, I, I, I, D] + [P] * 17
         _lib.oracle_bwd_sel.argtypes = [I, I, I, I, I, D] + [P] * 19
         _lib.oracle_fpa.argtypes = [I, I, I, I, D] + [P] * 13
         _lib.oracle_psi_block.argtypes = [P, I, I, P, P]
@@ -100,10 +100,13 @@ def _sel(blocks, BH, T):
 
 
 def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk=128, tau=None, p_u8=False,
-        q_blocks=None):
+        q_blocks=None, tiles=False):
     """Alg. 1 per head.  Returns dict with o, lse and the Tier-A intermediates.
     q_blocks: compute O and L only for these query blocks (other rows stay zero), with the same
-    arithmetic as the full run (sampled checks at sizes the full oracle cannot finish)."""
+    arithmetic as the full run (sampled checks at sizes the full oracle cannot finish).
+    tiles=True also returns the per-token P^ of every processed tile (p8, [BH, N q, N kv] uint8; tile (i, j)
+    at rows i*blk.., columns j*blk..; masked or skipped entries 0) and its row scale s_P (sp, [BH, N q, T]
+    float64, Alg. 1 line 9)."""
     q, k, v = _f64(q), _f64(k), _f64(v)
     BH, N, d = q.shape
     T = N // blk
@@ -116,10 +119,12 @@ def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk
                v8=np.zeros((BH, N, d), np.int8),
                sq=np.zeros((BH, T), np.float32), sk=np.zeros((BH, T), np.float32),
                sv=np.zeros((BH, T), np.float32))
+    if tiles:
+        out.update(p8=np.zeros((BH, N, N), np.uint8), sp=np.zeros((BH, N, T)))
     rc = _load().oracle_fwd_sel(BH, N, d, blk, flags, _default_tau(d, tau), _p(q), _p(k), _p(v), _p(qsel),
                             _p(out["o"]), _p(out["lse"]), _p(out["mu_k"]), _p(out["mu_q"]),
                             _p(out["bias"]), _p(out["q8"]), _p(out["k8"]), _p(out["v8"]),
-                            _p(out["sq"]), _p(out["sk"]), _p(out["sv"]))
+                            _p(out["sq"]), _p(out["sk"]), _p(out["sv"]), _p(out.get("p8")), _p(out.get("sp")))
     if rc:
         raise ValueError("oracle_fwd: bad shape")
     return out

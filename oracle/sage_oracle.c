@@ -243,7 +243,8 @@ static void s_tile(const head_prep *h, int i, int j, double tau, double *S) {
 static void fwd_head(const double *q, const double *k, const double *v, int N, int d, int blk,
                      int flags, double tau, const uint8_t *qsel, double *o, double *lse,
                      float *mu_k, float *mu_q, double *bias,
-                     int8_t *q8o, int8_t *k8o, int8_t *v8o, float *sqo, float *sko, float *svo) {
+                     int8_t *q8o, int8_t *k8o, int8_t *v8o, float *sqo, float *sko, float *svo,
+                     uint8_t *p8o, double *spo) {
   head_prep h;
   prep_head(&h, q, k, N, d, blk, flags);
   int T = h.T, qo = (flags & ORC_QUANT_OFF) != 0, causal = (flags & ORC_CAUSAL) != 0;
@@ -291,6 +292,9 @@ static void fwd_head(const double *q, const double *k, const double *v, int N, i
         } else {
           int16_t *Phr = Ph + (size_t)r * blk;
           double sp = psi_token_row(Pr, blk, rm - mnew, pmax, Phr);   /* line 9 */
+          /* optional dumps (test infrastructure: Tier-C of the forward), P^ [N q][N kv], s_P [N q][T] */
+          if (p8o) for (int n = 0; n < blk; ++n) p8o[(size_t)(i * blk + r) * N + (size_t)j * blk + n] = (uint8_t)Phr[n];
+          if (spo) spo[(size_t)(i * blk + r) * T + j] = sp;
           for (int c = 0; c < d; ++c) {                            /* line 10 */
             int32_t pv = 0;
             for (int n = 0; n < blk; ++n)
@@ -327,7 +331,8 @@ int oracle_fwd_sel(int BH, int N, int d, int blk, int flags, double tau,
                    const double *q, const double *k, const double *v, const uint8_t *qsel,
                    double *o, double *lse,
                    float *mu_k, float *mu_q, double *bias,
-                   int8_t *q8, int8_t *k8, int8_t *v8, float *sq, float *sk, float *sv) {
+                   int8_t *q8, int8_t *k8, int8_t *v8, float *sq, float *sk, float *sv,
+                   uint8_t *p8, double *sp) {
   if (BH <= 0 || N <= 0 || d <= 0 || blk <= 0 || N % blk) return -1;
   int T = N / blk;
   size_t nd = (size_t)N * d;
@@ -338,7 +343,8 @@ int oracle_fwd_sel(int BH, int N, int d, int blk, int flags, double tau,
              mu_k ? mu_k + (size_t)b * d : NULL, mu_q ? mu_q + (size_t)b * T * d : NULL,
              bias ? bias + (size_t)b * T * N : NULL,
              q8 ? q8 + b * nd : NULL, k8 ? k8 + b * nd : NULL, v8 ? v8 + b * nd : NULL,
-             sq ? sq + (size_t)b * T : NULL, sk ? sk + (size_t)b * T : NULL, sv ? sv + (size_t)b * T : NULL);
+             sq ? sq + (size_t)b * T : NULL, sk ? sk + (size_t)b * T : NULL, sv ? sv + (size_t)b * T : NULL,
+             p8 ? p8 + (size_t)b * N * N : NULL, sp ? sp + (size_t)b * N * T : NULL);
   }
   return 0;
 }
@@ -348,7 +354,8 @@ int oracle_fwd(int BH, int N, int d, int blk, int flags, double tau,
                double *o, double *lse,
                float *mu_k, float *mu_q, double *bias,
                int8_t *q8, int8_t *k8, int8_t *v8, float *sq, float *sk, float *sv) {
-  return oracle_fwd_sel(BH, N, d, blk, flags, tau, q, k, v, NULL, o, lse, mu_k, mu_q, bias, q8, k8, v8, sq, sk, sv);
+  return oracle_fwd_sel(BH, N, d, blk, flags, tau, q, k, v, NULL, o, lse, mu_k, mu_q, bias, q8, k8, v8, sq, sk, sv,
+                        NULL, NULL);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -491,3 +491,25 @@ def test_block_selection_is_the_full_run(orc):
                 np.testing.assert_array_equal(bs[name][:, rows], b[name][:, rows])
         assert not bs["dq"][:, :128].any() and not bs["dk"][:, 128:256].any()
         np.testing.assert_array_equal(bs["delta"], b["delta"])
+
+
+def test_forward_tile_dump(orc):
+    """The forward dump (Tier C of K2) is Alg. 1 line 9's per-token P^: every processed row of a
+    tile has P^ in [0, 127] with 127 attained at the row's max, s_P = e^{rowmax - m_ij} / 127 <= 1/127
+    (m_ij >= rowmax); causal tiles above the diagonal stay empty; the dump does not change O."""
+    q, k, v, _ = (f64(t).reshape(1, 384, 64) for t in make_inputs(1, 1, 384, 64, "gauss", seed=23, sigma=1.5))
+    f = orc.fwd(q, k, v, causal=True, tiles=True)
+    f0 = orc.fwd(q, k, v, causal=True)
+    np.testing.assert_array_equal(f["o"], f0["o"])
+    p8, sp = f["p8"][0], f["sp"][0]
+    assert p8.max() <= 127
+    for i in range(3):
+        for j in range(3):
+            tile = p8[i * 128:(i + 1) * 128, j * 128:(j + 1) * 128]
+            if j > i:
+                assert not tile.any()
+                continue
+            rows_max = tile.max(axis=1)
+            assert (rows_max == 127).all()
+            assert (sp[i * 128:(i + 1) * 128, j] <= 1.0 / 127.0 + 1e-15).all()
+    assert (sp[:, 0] > 0).all()
