@@ -20,13 +20,15 @@
  *
  * Conventions
  *   - Tensors Q, K, V, O, dO, dQ, dK, dV: bf16 (fp16 with SAGE_FP16), contiguous [B, H, N, d] (d innermost),
- *     16-byte aligned device pointers.  N % 128 == 0, d in {64, 128}.
+ *     16-byte aligned device pointers on the current device.  N % 128 == 0, d in {64, 128}.  With
+ *     SAGE_FP32_OUT the outputs O, dQ, dK, dV are fp32 instead.
  *   - lse: fp32 [B, H, N], natural log (Alg. 1 line 14).
  *   - Ownership: the caller allocates every buffer (device memory), including the
  *     forward->backward context `ctx` (sage_ctx_bytes) and the scratch workspace
  *     (sage_workspace_bytes).  The library never allocates or frees device memory.
  *   - Execution: every call only enqueues kernels on `stream` and returns; errors in
- *     arguments are reported before anything is launched (nothing is written).
+ *     arguments are reported before anything is launched (nothing is written).  Calls are
+ *     reentrant and thread-safe as long as concurrent calls use distinct workspaces.
  *     Asynchronous device faults surface at the caller's next synchronisation.
  *   - There is no CPU fallback: without an sm_100 device the calls return SAGE_ERR_ARCH.
  */
@@ -85,9 +87,13 @@ enum {
                               dQ / dK / dV to 0.022 / 0.022 / 0.021 vs the paper's 0.018 / 0.022 /
                               0.016 (per-tile: 0.067 / 0.066 / 0.055).  Slower backward.  Not
                               combinable with SAGE_DETERMINISTIC. */
-  SAGE_FP16 = 1u << 8       /* fp16 instead of bf16 for Q, K, V, O, dO, dQ, dK, dV (and X_q, X_k, dX_q,
+  SAGE_FP16 = 1u << 8,      /* fp16 instead of bf16 for Q, K, V, O, dO, dQ, dK, dV (and X_q, X_k, dX_q,
                               dX_k with QK-norm, whose module output is then fp16): dP = dO V^T runs
                               as an fp16 kind::f16 MMA, the paper's "FP16" option */
+  SAGE_FP32_OUT = 1u << 9   /* O, dQ, dK, dV written as fp32 (no rounding to the I/O type), e.g. to
+                              compare against an unrounded reference (reading A18).  delta is then
+                              formed from the fp32 O the forward stored (A15).  Not combinable with
+                              SAGE_QK_NORM (SAGE_ERR_INVALID_VALUE). */
 };
 
 typedef struct {
@@ -96,25 +102,44 @@ typedef struct {
   float softmax_scale;                    /* tau; 0 => 1/sqrt(d) (reading A6) */
 } sage_params;
 
-/* Bytes of the forward->backward context: int8 Q^, K^ [B,H,N,d]; fp32 s_Q, s_K
- * [B,H,N/128]; mu_K [B,H,d]; and with SAGE_Q_SMOOTH mu_Q [B,H,N/128,d] and the
- * bias [B,H,N/128,N] (Alg. 2 line 1 inputs).  0 on invalid params. */
+/* The forward->backward context (Alg. 2's inputs): a caller-owned device buffer plus a host
+ * tag.  sage_fwd fills the buffer and sets params_tag = sage_params_tag(p); sage_bwd refuses
+ * (SAGE_ERR_INVALID_VALUE, nothing launched) a ctx whose tag differs from its own params' tag -- a
+ * context produced under another shape, softmax scale or flag set (SPEC's "missing retained quantized
+ * operands") -- and a ctx never filled by sage_fwd (tag 0). */
+typedef struct {
+  void* buf;           /* device memory of at least sage_ctx_bytes(p) bytes, 256-byte aligned */
+  size_t bytes;        /* size of buf */
+  uint64_t params_tag; /* written by sage_fwd; 0 = not filled */
+} sage_ctx;
+
+/* Bytes of the context buffer: int8 Q^, K^ [B,H,N,d]; fp32 s_Q, s_K [B,H,N/128]; mu_K [B,H,d]; and with
+ * SAGE_Q_SMOOTH mu_Q [B,H,N/128,d] and the bias [B,H,N/128,N] (Alg. 2 line 1 inputs).
+ * 0 on invalid params. */
 SAGE_API size_t sage_ctx_bytes(const sage_params* p);
+
+/* The tag sage_fwd writes into sage_ctx.params_tag for these params (a 64-bit FNV-1a hash of every
+ * field; never 0).  0 on invalid params. */
+SAGE_API uint64_t sage_params_tag(const sage_params* p);
 
 /* Bytes of scratch for sage_fwd (backward = 0: V^, s_V, partial sums) or sage_bwd
  * (backward = 1: dO^, s_dO, delta, L*log2(e), fp32 dQ accumulator). 0 on invalid params. */
 SAGE_API size_t sage_workspace_bytes(const sage_params* p, int backward);
 
-/* Forward (Alg. 1).  Reads q, k, v; writes o, lse and the context ctx.
- * ws must hold sage_workspace_bytes(p, 0) bytes.  stream: a cudaStream_t (NULL = legacy). */
+/* Forward (Alg. 1).  Reads q, k, v; writes o, lse, the context buffer ctx->buf and ctx->params_tag.
+ * ws must hold sage_workspace_bytes(p, 0) bytes.  stream: a cudaStream_t (NULL = legacy).
+ * Errors: SAGE_ERR_INVALID_VALUE (bad params, null pointer, q not on the current device),
+ * SAGE_ERR_MISALIGNED, SAGE_ERR_WORKSPACE (ctx->bytes or ws_bytes too small), SAGE_ERR_ARCH,
+ * SAGE_ERR_CUDA (a launch failed). */
 SAGE_API sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const void* v, void* o, float* lse,
-                     void* ctx, size_t ctx_bytes, void* ws, size_t ws_bytes, void* stream);
+                              sage_ctx* ctx, void* ws, size_t ws_bytes, void* stream);
 
 /* Backward (Alg. 2).  Reads v, the o and lse written by sage_fwd, dO and ctx; writes
- * dq, dk, dv.  ws must hold sage_workspace_bytes(p, 1) bytes. */
+ * dq, dk, dv.  ws must hold sage_workspace_bytes(p, 1) bytes.  Errors as sage_fwd, plus
+ * SAGE_ERR_INVALID_VALUE when ctx->params_tag != sage_params_tag(p). */
 SAGE_API sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const float* lse, const void* dO,
-                     const void* ctx, size_t ctx_bytes, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
-                     void* stream);
+                              const sage_ctx* ctx, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
+                              void* stream);
 
 /* QK-norm variant ("Stabilizing Outliers with QK-Norm"; eps P:405).  p->flags must hold
  * SAGE_QK_NORM.  Instead of Q and K the caller passes the pre-norm X_q, X_k (bf16 [B,H,N,d]) and the
@@ -126,14 +151,14 @@ SAGE_API sage_status sage_bwd(const sage_params* p, const void* v, const void* o
  * eps > 0 (the paper uses 1e-6). */
 SAGE_API sage_status sage_fwd_qknorm(const sage_params* p, const void* xq, const void* xk, const void* v,
                                      const float* gamma_q, const float* gamma_k, float eps, void* o, float* lse,
-                                     void* ctx, size_t ctx_bytes, void* ws, size_t ws_bytes, void* stream);
+                                     sage_ctx* ctx, void* ws, size_t ws_bytes, void* stream);
 /* Backward of sage_fwd_qknorm: Alg. 2 as sage_bwd, then the RMSNorm backward (reading A26) fused with
  * the dQ finalisation: writes dX_q, dX_k (bf16 [B,H,N,d]) into dxq, dxk, dV into dv, and
  * dgamma_q, dgamma_k (fp32 [d], summed over all B*H*N rows in a fixed order).  xq, xk, gamma_q,
  * gamma_k must be the forward's. */
 SAGE_API sage_status sage_bwd_qknorm(const sage_params* p, const void* xq, const void* xk, const float* gamma_q,
                                      const float* gamma_k, const void* v, const void* o, const float* lse,
-                                     const void* dO, const void* ctx, size_t ctx_bytes, void* dxq, void* dxk,
+                                     const void* dO, const sage_ctx* ctx, void* dxq, void* dxk,
                                      void* dv, float* dgamma_q, float* dgamma_k, void* ws, size_t ws_bytes,
                                      void* stream);
 
@@ -175,14 +200,29 @@ SAGE_API sage_status sage_debug_trace(void* host_out, size_t bytes);
 
 /* Test only (libsage_trace.so; the production libsage.so returns SAGE_ERR_UNSUPPORTED): make every
  * later sage_bwd dump, for heads bh < `heads` (bh = b*H + h), K4's own backward intermediates
- * (Alg. 2 lines 6 and 9, P:689 / P:695) into caller-owned device memory:
+ * (Alg. 2 lines 5-11) into caller-owned device memory (T = N/128):
  *   p_hat_t  int8 [heads][N kv][N q]  P^ of tile (i, j) transposed (key-major), psi(P) per tile (A11)
  *   ds_hat_t int8 [heads][N kv][N q]  dS^, same layout
  *   ds_t     fp32 [heads][N kv][N q]  dS = P o (dP - delta) before psi
  *   s_p, s_ds fp32 [heads][T i][T j]  the tile scales fl32(amax / 127)
- * Tiles a causal run skips are not written.  heads = 0 turns the dump off.  The buffers must stay
- * valid until the dumping sage_bwd has completed.  Not thread-safe (process-wide state). */
+ *   s_t      int32 [heads][N kv][N q] the recomputed S^T = K^_j Q^_i^T accumulator (line 5)
+ *   dv_t     int32 [heads][T i][N kv][d]  the dV tile P^^T dO^_i before its scaling (line 7)
+ *   dk_t     int32 [heads][T i][N kv][d]  the dK tile dS^^T Q^_i (line 11)
+ *   dq_t     int32 [heads][T j][N q][d]   the dQ tile dS^ K^_j (line 10)
+ * Any of the last four may be NULL (not dumped).  Tiles a causal run skips are not written.
+ * heads = 0 turns the dump off.  The buffers must stay valid until the dumping sage_bwd has completed.
+ * Not thread-safe (process-wide state). */
 SAGE_API sage_status sage_debug_dump(void* p_hat_t, float* s_p, void* ds_hat_t, float* s_ds, float* ds_t, int heads);
+SAGE_API sage_status sage_debug_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t);
+
+/* Test only (libsage_trace.so): make every later sage_fwd dump, for heads bh < `heads`, K2's own
+ * intermediates (Alg. 1 lines 7-10) into caller-owned device memory:
+ *   s       int32 [heads][N q][N kv]    the S = Q^_i K^_j^T accumulator of every processed tile (line 7)
+ *   p_hat   uint8 [heads][N q][N kv]    the per-token P^ (line 9), 0..127 (0..255 with SAGE_P_U8)
+ *   s_p     fp32  [heads][N q][T j]     its per-row scale s_P = e^{rowmax - m_ij} / 127 (line 9)
+ *   pv      int32 [heads][T j][N q][d]  the P^ V^_j accumulator before scaling (line 10)
+ * Any pointer may be NULL (not dumped).  heads = 0 turns the dump off. */
+SAGE_API sage_status sage_debug_fwd_dump(int32_t* s, void* p_hat, float* s_p, int32_t* pv, int heads);
 
 /* Optional instrumentation (calling thread only).  While enabled, sage_fwd / sage_bwd record
  * a CUDA event pair around their fused kernel (K2 / K4) and count every kernel they launch.

@@ -66,7 +66,7 @@ size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Dims {
   size_t BH, N, d, T;
-  bool causal, ks, qs, pu8, qkn, det, pcol, fine, fp16;
+  bool causal, ks, qs, pu8, qkn, det, pcol, fine, fp16, f32out;
   float tau;
 };
 
@@ -76,7 +76,7 @@ bool dims_of(const sage_params* p, Dims* o) {
   if (p->head_dim != 64 && p->head_dim != 128) return false;
   if (p->seqlen % kBlk || p->seqlen > kMaxSeqLen) return false;
   if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH | SAGE_P_U8 | SAGE_QK_NORM | SAGE_DETERMINISTIC |
-                             SAGE_P_COLSCALE | SAGE_FINE_BWD | SAGE_FP16))
+                             SAGE_P_COLSCALE | SAGE_FINE_BWD | SAGE_FP16 | SAGE_FP32_OUT))
     return false;
   if (!(p->softmax_scale >= 0.f) || std::isinf(p->softmax_scale)) return false;
   const size_t BH = (size_t)p->batch * p->heads;
@@ -94,7 +94,9 @@ bool dims_of(const sage_params* p, Dims* o) {
   o->pcol = p->flags & SAGE_P_COLSCALE;
   o->fine = p->flags & SAGE_FINE_BWD;
   o->fp16 = p->flags & SAGE_FP16;
+  o->f32out = p->flags & SAGE_FP32_OUT;
   if (o->det && (o->pcol || o->fine)) return false;  // one backward variant at a time
+  if (o->f32out && o->qkn) return false;              // the QK-norm outputs dX are I/O-typed
   o->tau = p->softmax_scale > 0.f ? p->softmax_scale : 1.f / std::sqrt((float)p->head_dim);
   return true;
 }
@@ -195,18 +197,90 @@ int ablate_flags() {
   return v;
 }
 
-// sage_debug_dump state (libsage_trace.so only): K4 tile dump on while heads > 0
+// sage_debug_dump / sage_debug_fwd_dump state (libsage_trace.so only): K4 / K2 dumps on while heads > 0
 int g_dump_heads = 0;
+int g_fwd_dump_heads = 0;
 
 template <typename T>
 T* at(void* base, size_t off) {
   return reinterpret_cast<T*>(static_cast<uint8_t*>(base) + off);
 }
 
+// A device pointer of another device than the current one would be launched against on the wrong
+// GPU: reject it (host or unregistered pointers are left to the launch to fault on).
+bool on_current_device(const void* ptr) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return true;
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return true;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return true;
+  return a.device == dev;
+}
+
+// FNV-1a over every sage_params field (sage_params_tag); never 0.
+uint64_t params_tag(const sage_params* p) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint32_t v) {
+    for (int b = 0; b < 4; ++b) {
+      h ^= (v >> (8 * b)) & 0xFFu;
+      h *= 1099511628211ull;
+    }
+  };
+  uint32_t sc;
+  std::memcpy(&sc, &p->softmax_scale, 4);
+  mix((uint32_t)p->batch);
+  mix((uint32_t)p->heads);
+  mix((uint32_t)p->seqlen);
+  mix((uint32_t)p->head_dim);
+  mix(p->flags);
+  mix(sc);
+  return h ? h : 1;
+}
+
 }  // namespace
+
+namespace {
+// Per-thread cache of encoded tensor maps (the encode is a driver call of a few microseconds; a training
+// loop re-uses the same buffers every step).  Keyed by everything the encoding depends on.
+struct TmapEntry {
+  const void* base;
+  uint64_t rows, cols;
+  uint32_t box_rows, box_cols, type, device;
+  uint64_t stamp;
+  CUtensorMap map;
+};
+constexpr int kTmapCache = 64;
+thread_local TmapEntry g_tmaps[kTmapCache];
+thread_local uint64_t g_tmap_clock = 0;
+}  // namespace
+
+bool make_tmap_2d_uncached(CUtensorMap* m, const void* base, TmapType type, uint64_t rows, uint64_t cols,
+                           uint32_t box_rows, uint32_t box_cols);
 
 bool make_tmap_2d(CUtensorMap* m, const void* base, TmapType type, uint64_t rows, uint64_t cols, uint32_t box_rows,
                   uint32_t box_cols) {
+  int dev = 0;
+  (void)cudaGetDevice(&dev);
+  TmapEntry* victim = &g_tmaps[0];
+  for (auto& e : g_tmaps) {
+    if (e.stamp && e.base == base && e.rows == rows && e.cols == cols && e.box_rows == box_rows &&
+        e.box_cols == box_cols && e.type == (uint32_t)type && e.device == (uint32_t)dev) {
+      e.stamp = ++g_tmap_clock;
+      *m = e.map;
+      return true;
+    }
+    if (e.stamp < victim->stamp) victim = &e;
+  }
+  if (!make_tmap_2d_uncached(m, base, type, rows, cols, box_rows, box_cols)) return false;
+  *victim = TmapEntry{base, rows, cols, box_rows, box_cols, (uint32_t)type, (uint32_t)dev, ++g_tmap_clock, *m};
+  return true;
+}
+
+bool make_tmap_2d_uncached(CUtensorMap* m, const void* base, TmapType type, uint64_t rows, uint64_t cols,
+                           uint32_t box_rows, uint32_t box_cols) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
   const uint32_t esz = type == kF32 ? 4 : (type == kBF16 || type == kF16) ? 2 : 1;
@@ -290,6 +364,11 @@ size_t sage_ctx_bytes(const sage_params* p) {
   return dims_of(p, &D) ? ctx_layout(D).total : 0;
 }
 
+uint64_t sage_params_tag(const sage_params* p) {
+  Dims D;
+  return dims_of(p, &D) ? params_tag(p) : 0;
+}
+
 size_t sage_workspace_bytes(const sage_params* p, int backward) {
   Dims D;
   if (!dims_of(p, &D)) return 0;
@@ -346,6 +425,7 @@ sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v,
   if (ctx_bytes < C.total || ws_bytes < W.total) return SAGE_ERR_WORKSPACE;
   sage_status st = check_arch();
   if (st != SAGE_OK) return st;
+  if (!on_current_device(q) || !on_current_device(o) || !on_current_device(ctx)) return SAGE_ERR_INVALID_VALUE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int BH = (int)D.BH, N = (int)D.N, d = (int)D.d;
   const void *qb = q, *kb = k, *vb = v;  // bf16, or fp16 with SAGE_FP16
@@ -394,6 +474,7 @@ sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v,
   a.bias = bias;
   a.o = o;
   a.fp16 = D.fp16;
+  a.f32out = D.f32out;
   a.lse = lse;
   a.BH = BH;
   a.N = N;
@@ -402,7 +483,7 @@ sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v,
   a.causal = D.causal;
   a.qsmooth = D.qs;
   a.pu8 = D.pu8;
-  a.ablate = ablate_flags();
+  a.ablate = ablate_flags() | (g_fwd_dump_heads > 0 ? 16 : 0);
   if ((e = timed(0, s, [&] { return launch_fwd(a, s); })) != cudaSuccess) return cuda_fail(e);
   if (g_prof.on) g_prof.launches += (D.ks ? 2 : 1) + (D.qs ? 3 : 0) + 1 + 1;
   return SAGE_OK;
@@ -422,6 +503,7 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
   if (ctx_bytes < C.total || ws_bytes < W.total) return SAGE_ERR_WORKSPACE;
   sage_status st = check_arch();
   if (st != SAGE_OK) return st;
+  if (!on_current_device(dO) || !on_current_device(dq) || !on_current_device(ctx)) return SAGE_ERR_INVALID_VALUE;
   if (D.det && !D.causal) {
     // the rotated non-causal order needs all T key-block CTAs of a head resident at once
     int dev = 0, sms = 0;
@@ -434,7 +516,9 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
   void* cx = const_cast<void*>(ctx);
   int8_t *q8 = at<int8_t>(cx, C.q8), *k8 = at<int8_t>(cx, C.k8), *do8 = at<int8_t>(ws, W.do8);
   float *sq = at<float>(cx, C.sq), *sk = at<float>(cx, C.sk), *sdo = at<float>(ws, W.sdo);
-  float *delta = at<float>(ws, W.delta), *l2 = at<float>(ws, W.l2), *dqacc = at<float>(ws, W.dq);
+  float *delta = at<float>(ws, W.delta), *l2 = at<float>(ws, W.l2);
+  // SAGE_FP32_OUT: dQ is reduced straight into the caller's fp32 dq (zeroed by K3; no K5)
+  float* dqacc = D.f32out ? static_cast<float*>(dq) : at<float>(ws, W.dq);
 
   BwdArgs a{};
   const uint64_t rows = D.BH * D.N;
@@ -446,7 +530,8 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
   cudaError_t e;
   // K3: delta, psi(dO), L*log2(e), zero dQ accumulator (Alg. 2 lines 2, 6)
   unsigned* dqflags = D.det ? at<unsigned>(ws, W.flags) : nullptr;
-  if ((e = launch_bwd_prep(o, dO, lse, delta, l2, do8, sdo, dqacc, BH, N, d, s, dqflags, D.fp16)) != cudaSuccess)
+  if ((e = launch_bwd_prep(o, dO, lse, delta, l2, do8, sdo, dqacc, BH, N, d, s, dqflags, D.fp16, D.f32out)) !=
+      cudaSuccess)
     return cuda_fail(e);
   // K4: fused INT8 backward (Alg. 2 lines 3-11)
   a.q_scale = sq;
@@ -460,6 +545,7 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
   a.dk = dk;
   a.dv = dv;
   a.fp16 = D.fp16;
+  a.f32out = D.f32out;
   a.BH = BH;
   a.N = N;
   a.d = d;
@@ -487,7 +573,8 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
     if (g_prof.on) g_prof.launches += 6;  // 2 x (norm_bwd, dgamma stage 1, stage 2)
     return SAGE_OK;
   }
-  // K5
+  // K5 (not with SAGE_FP32_OUT: dq already holds the fp32 sum)
+  if (D.f32out) return SAGE_OK;
   if ((e = launch_dq_finalize(dqacc, dq, D.BH * D.N * D.d, s, D.fp16)) != cudaSuccess)
     return cuda_fail(e);
   if (g_prof.on) g_prof.launches += 1;  // K5
@@ -498,43 +585,49 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
 extern "C" {
 
 sage_status sage_fwd(const sage_params* p, const void* q, const void* k, const void* v, void* o, float* lse,
-                     void* ctx, size_t ctx_bytes, void* ws, size_t ws_bytes, void* stream) {
+                     sage_ctx* ctx, void* ws, size_t ws_bytes, void* stream) {
   Dims D;
-  if (!dims_of(p, &D) || D.qkn) return SAGE_ERR_INVALID_VALUE;  // QK-norm: sage_fwd_qknorm
-  return fwd_impl(D, q, k, v, nullptr, nullptr, 0.f, o, lse, ctx, ctx_bytes, ws, ws_bytes, stream);
+  if (!dims_of(p, &D) || D.qkn || !ctx) return SAGE_ERR_INVALID_VALUE;  // QK-norm: sage_fwd_qknorm
+  const sage_status st = fwd_impl(D, q, k, v, nullptr, nullptr, 0.f, o, lse, ctx->buf, ctx->bytes, ws, ws_bytes, stream);
+  if (st == SAGE_OK) ctx->params_tag = params_tag(p);
+  return st;
 }
 
 sage_status sage_fwd_qknorm(const sage_params* p, const void* xq, const void* xk, const void* v, const float* gamma_q,
-                            const float* gamma_k, float eps, void* o, float* lse, void* ctx, size_t ctx_bytes,
-                            void* ws, size_t ws_bytes, void* stream) {
+                            const float* gamma_k, float eps, void* o, float* lse, sage_ctx* ctx, void* ws,
+                            size_t ws_bytes, void* stream) {
   Dims D;
-  if (!dims_of(p, &D) || !D.qkn || !gamma_q || !gamma_k || !(eps > 0.f) || std::isinf(eps))
+  if (!dims_of(p, &D) || !D.qkn || !ctx || !gamma_q || !gamma_k || !(eps > 0.f) || std::isinf(eps))
     return SAGE_ERR_INVALID_VALUE;
   if (!aligned16(gamma_q) || !aligned16(gamma_k)) return SAGE_ERR_MISALIGNED;
-  return fwd_impl(D, xq, xk, v, gamma_q, gamma_k, eps, o, lse, ctx, ctx_bytes, ws, ws_bytes, stream);
+  const sage_status st =
+      fwd_impl(D, xq, xk, v, gamma_q, gamma_k, eps, o, lse, ctx->buf, ctx->bytes, ws, ws_bytes, stream);
+  if (st == SAGE_OK) ctx->params_tag = params_tag(p);
+  return st;
 }
 
 sage_status sage_bwd(const sage_params* p, const void* v, const void* o, const float* lse, const void* dO,
-                     const void* ctx, size_t ctx_bytes, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
-                     void* stream) {
+                     const sage_ctx* ctx, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, void* stream) {
   Dims D;
-  if (!dims_of(p, &D) || D.qkn) return SAGE_ERR_INVALID_VALUE;  // QK-norm: sage_bwd_qknorm
-  return bwd_impl(D, v, o, lse, dO, ctx, ctx_bytes, dq, dk, dv, ws, ws_bytes, stream, nullptr, nullptr, nullptr,
-                  nullptr, nullptr, nullptr);
+  if (!dims_of(p, &D) || D.qkn || !ctx) return SAGE_ERR_INVALID_VALUE;  // QK-norm: sage_bwd_qknorm
+  if (ctx->params_tag != params_tag(p)) return SAGE_ERR_INVALID_VALUE;   // another forward's context
+  return bwd_impl(D, v, o, lse, dO, ctx->buf, ctx->bytes, dq, dk, dv, ws, ws_bytes, stream, nullptr, nullptr,
+                  nullptr, nullptr, nullptr, nullptr);
 }
 
 sage_status sage_bwd_qknorm(const sage_params* p, const void* xq, const void* xk, const float* gamma_q,
                             const float* gamma_k, const void* v, const void* o, const float* lse, const void* dO,
-                            const void* ctx, size_t ctx_bytes, void* dxq, void* dxk, void* dv, float* dgamma_q,
-                            float* dgamma_k, void* ws, size_t ws_bytes, void* stream) {
+                            const sage_ctx* ctx, void* dxq, void* dxk, void* dv, float* dgamma_q, float* dgamma_k,
+                            void* ws, size_t ws_bytes, void* stream) {
   Dims D;
-  if (!dims_of(p, &D) || !D.qkn || !xq || !xk || !gamma_q || !gamma_k || !dgamma_q || !dgamma_k)
+  if (!dims_of(p, &D) || !D.qkn || !ctx || !xq || !xk || !gamma_q || !gamma_k || !dgamma_q || !dgamma_k)
     return SAGE_ERR_INVALID_VALUE;
+  if (ctx->params_tag != params_tag(p)) return SAGE_ERR_INVALID_VALUE;
   if (!aligned16(xq) || !aligned16(xk) || !aligned16(gamma_q) || !aligned16(gamma_k) || !aligned16(dgamma_q) ||
       !aligned16(dgamma_k))
     return SAGE_ERR_MISALIGNED;
-  return bwd_impl(D, v, o, lse, dO, ctx, ctx_bytes, dxq, dxk, dv, ws, ws_bytes, stream, xq, xk, gamma_q, gamma_k,
-                  dgamma_q, dgamma_k);
+  return bwd_impl(D, v, o, lse, dO, ctx->buf, ctx->bytes, dxq, dxk, dv, ws, ws_bytes, stream, xq, xk, gamma_q,
+                  gamma_k, dgamma_q, dgamma_k);
 }
 
 sage_status sage_debug_trace(void* host_out, size_t bytes) {
@@ -555,6 +648,30 @@ sage_status sage_debug_dump(void* p_hat_t, float* s_p, void* ds_hat_t, float* s_
   return SAGE_OK;
 #else
   (void)p_hat_t; (void)s_p; (void)ds_hat_t; (void)s_ds; (void)ds_t; (void)heads;
+  return SAGE_ERR_UNSUPPORTED;
+#endif
+}
+
+sage_status sage_debug_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t) {
+#if SAGE_TRACE
+  cudaError_t e = set_bwd_dump_acc(s_t, dv_t, dk_t, dq_t);
+  return e == cudaSuccess ? SAGE_OK : cuda_fail(e);
+#else
+  (void)s_t; (void)dv_t; (void)dk_t; (void)dq_t;
+  return SAGE_ERR_UNSUPPORTED;
+#endif
+}
+
+sage_status sage_debug_fwd_dump(int32_t* s, void* p_hat, float* s_p, int32_t* pv, int heads) {
+#if SAGE_TRACE
+  if (heads < 0) return SAGE_ERR_INVALID_VALUE;
+  FwdDump d{s, static_cast<uint8_t*>(p_hat), s_p, pv, heads};
+  cudaError_t e = set_fwd_dump(d);
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_fwd_dump_heads = heads;
+  return SAGE_OK;
+#else
+  (void)s; (void)p_hat; (void)s_p; (void)pv; (void)heads;
   return SAGE_ERR_UNSUPPORTED;
 #endif
 }

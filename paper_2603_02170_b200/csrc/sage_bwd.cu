@@ -21,7 +21,8 @@
 //                 tiles, so every dV/dK/dQ int32 tile is converted and scaled here while the
 //                 compute warpgroups already work on the next tile.  dK_j (and dV_j for d=64)
 //                 accumulate in fp32 registers; for d=128 dV_j accumulates in fp32 TMEM.
-//                 dQ_i is reduced across key blocks with fp32 red.global.add (finalised by K5).
+//                 dQ_i is reduced across key blocks with a TMA reduce-add (cp.reduce.async.bulk.tensor
+//                 .add, fp32) per drain warp, finalised by K5.
 // TMEM (512 columns):  d=64 : S 0 | dP 128 | dV 256 | dK 320 | dQ 384
 //                      d=128: S/dV 0 | dP/dK 128 | dQ 256 | dV fp32 accumulator 384
 //   (d=128 aliases the dV tile onto S and the dK tile onto dP; the MMA issuer orders them.)
@@ -95,7 +96,7 @@ struct BwdSmem {
 #define SAGE_K4_RP 56
 #endif
 #ifndef SAGE_K4_RC64
-#define SAGE_K4_RC64 144  // measured: 136 -> 144 takes C2 K4 0.521 -> 0.516 ms; 152 slower (0.543)
+#define SAGE_K4_RC64 136  // 144 spilled (68 B STL per thread) for a within-noise gain: kept at 136
 #endif
 #ifndef SAGE_K4_RC128
 #define SAGE_K4_RC128 128
@@ -118,6 +119,15 @@ __device__ unsigned long long g_trace[kTrCtas * kTrTiles * kTrEvents];
 // scales s_P, s_dS as [head][T i][T j], for heads bh < g_dump.heads (Tier C, fidelity reports).
 __device__ BwdDump g_dump;
 #define DUMPING (SAGE_TRACE && (ablate & 16) && bh < g_dump.heads)
+// ... and the int32 accumulators (sage_debug_dump_acc): S^T [head][N kv][N q], the dV / dK tiles
+// [head][T i][N kv][D], the dQ tiles [head][T j][N q][D], each before any scaling
+struct BwdDumpAcc {
+  int32_t *s_t, *dv, *dk, *dq;
+};
+__device__ BwdDumpAcc g_dacc;
+__device__ __forceinline__ void dump_words(int32_t* dst, const uint32_t* v, int n) {
+  for (int e = 0; e < n; e += 4) *reinterpret_cast<uint4*>(dst + e) = make_uint4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+}
 
 // Order-preserving float <-> int map (monotone for all finite values and +-inf), so a float max is
 // one redux.sync.max.s32 instead of five shuffles.
@@ -149,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* __restrict__ k_scale, const float* __restrict__ do_scale,
                     const float* __restrict__ l2g, const float* __restrict__ deltag, const float* __restrict__ bias,
                     const float* __restrict__ mu_q, float* __restrict__ dq_acc, void* __restrict__ dk_out,
-                    void* __restrict__ dv_out, int N, int BH, float tau, int pu8, int fp16,
+                    void* __restrict__ dv_out, int N, int BH, float tau, int pu8, int fp16, int f32out,
                     unsigned* __restrict__ dq_flags, int ablate_arg) {
   constexpr bool fine = VAR == 3;
   constexpr bool pcol = VAR == 2 || fine;
@@ -163,6 +173,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // setmaxnreg budget per warpgroup (sums to 4 x 128): producer/MMA, 2 x compute, drain gets the rest
   constexpr uint32_t kRegProducer = SAGE_K4_RP, kRegCompute = D == 64 ? SAGE_K4_RC64 : SAGE_K4_RC128,
                      kRegDrain = 512 - kRegProducer - 2 * kRegCompute;
+  static_assert(kRegProducer % 8 == 0 && kRegCompute % 8 == 0 && kRegDrain % 8 == 0, "setmaxnreg needs multiples of 8");
+  static_assert(kRegProducer >= 24 && kRegCompute <= 256 && kRegDrain >= 24 && kRegDrain <= 256,
+                "setmaxnreg values must lie in [24, 256]");
+  static_assert(kRegProducer + 2 * kRegCompute + kRegDrain == 512, "the four warpgroups share 512 registers/slot");
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment (128B swizzle atoms) by offsetting the __shared__ array itself, so every
   // derived pointer stays in the shared window (LDS/STS, not generic LD/ST)
@@ -500,6 +514,8 @@ if (cm) {
         tmem_ld32(tS + qc0 + cc * 32 + lane_off, v);
         tmem_wait_ld();
         if (threadIdx.x == 128 && cc == 0) TR(16, it);
+        if (DUMPING && g_dacc.s_t)
+          dump_words(g_dacc.s_t + ((size_t)bh * N + j * kBlk + r) * N + i * kBlk + qc0 + cc * 32, v, 32);
 #pragma unroll
         for (int e4 = 0; e4 < 8; ++e4) {
           float4 l4 = Ls4[cc * 8 + e4];
@@ -707,6 +723,8 @@ if (cm) {
           tmem_ld32(tDV + qc0 + c0 + lane_off, v);
           tmem_ld32(tDVacc + qc0 + c0 + lane_off, a);
           tmem_wait_ld();
+          if (DUMPING && g_dacc.dv)
+            dump_words(g_dacc.dv + (((size_t)bh * T + i) * N + j * kBlk + r) * D + qc0 + c0, v, 32);
           if (it == 0) {
 #pragma unroll
             for (int e = 0; e < 32; ++e) a[e] = 0u;
@@ -759,6 +777,8 @@ if (cm) {
             uint32_t v[32];
             tmem_ld32(tDV + c0 + lane_off, v);
             tmem_wait_ld();
+            if (DUMPING && g_dacc.dv)
+              dump_words(g_dacc.dv + (((size_t)bh * T + i) * N + j * kBlk + r) * D + c0, v, 32);
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {
               float2 x = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f,
@@ -795,6 +815,8 @@ if (cm) {
         for (int c = 0; c < D / 16; ++c) {
           uint32_t(&v)[16] = kb[c & 1];
           if (c + 1 < D / 16) tmem_ld16(tDK + (c + 1) * 16 + lane_off, kb[(c + 1) & 1]);
+          if (DUMPING && g_dacc.dk)
+            dump_words(g_dacc.dk + (((size_t)bh * T + i) * N + j * kBlk + r) * D + c * 16, v, 16);
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {
             const int cc = c * 16 + e;
@@ -840,6 +862,8 @@ if (cm) {
               uint32_t v[32];
               tmem_ld32(tDQ + c0 + lane_off, v);
               tmem_wait_ld();
+              if (DUMPING && g_dacc.dq)
+                dump_words(g_dacc.dq + (((size_t)bh * T + j) * N + i * kBlk + r) * D + c0, v, 32);
               uint8_t* box = stage + bx * L::kDqBox;
 #pragma unroll
               for (int e = 0; e < 32; e += 4) {
@@ -895,6 +919,16 @@ if (cm) {
 #pragma unroll
         for (int e = 0; e < 32; ++e) vv[e] = dv_acc[c0 + e];
       }
+      if (f32out) {  // SAGE_FP32_OUT
+#pragma unroll
+        for (int e4 = 0; e4 < 32; e4 += 4) {
+          *reinterpret_cast<float4*>(static_cast<float*>(dk_out) + orow + c0 + e4) =
+              make_float4(dk_acc[c0 + e4], dk_acc[c0 + e4 + 1], dk_acc[c0 + e4 + 2], dk_acc[c0 + e4 + 3]);
+          *reinterpret_cast<float4*>(static_cast<float*>(dv_out) + orow + c0 + e4) =
+              make_float4(vv[e4], vv[e4 + 1], vv[e4 + 2], vv[e4 + 3]);
+        }
+        continue;
+      }
 #pragma unroll
       for (int e8 = 0; e8 < 32; e8 += 8) {
         uint32_t hk[4], hv[4];  // the I/O type: bf16, or fp16 with SAGE_FP16
@@ -927,13 +961,18 @@ cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
   kern<<<a.BH * T, kThreads, kSmem, s>>>(a.tm_q, a.tm_k, a.tm_doq, a.tm_v, a.tm_do, a.tm_dq, a.q_scale,
                                                        a.k_scale, a.do_scale, a.l2, a.delta, a.bias, a.mu_q,
                                                        a.dq_acc, a.dk, a.dv, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
-                                                       a.fp16 ? 1 : 0, a.dq_flags, a.ablate);
+                                                       a.fp16 ? 1 : 0, a.f32out ? 1 : 0, a.dq_flags, a.ablate);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t set_bwd_dump(const BwdDump& d) { return cudaMemcpyToSymbol(g_dump, &d, sizeof(d)); }
+
+cudaError_t set_bwd_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t) {
+  const BwdDumpAcc a{s_t, dv_t, dk_t, dq_t};
+  return cudaMemcpyToSymbol(g_dacc, &a, sizeof(a));
+}
 
 cudaError_t read_bwd_trace(void* host, size_t bytes) {
   if (bytes > sizeof(g_trace)) bytes = sizeof(g_trace);

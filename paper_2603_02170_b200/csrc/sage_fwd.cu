@@ -53,6 +53,11 @@ __device__ unsigned long long g_trace_fwd[kTrCtas * kTrTiles * kTrEvents];
       g_trace_fwd[(blockIdx.x * kTrTiles + (jj)) * kTrEvents + (ev)] = clock64();   \
   } while (0)
 
+// Test-only dump (libsage_trace.so, SAGE_ABLATE bit 16, sage_debug_fwd_dump): K2's own S accumulator,
+// per-token P^ and s_P and the PV accumulator of every processed tile, heads bh < g_fdump.heads.
+__device__ FwdDump g_fdump;
+#define FDUMPING (SAGE_TRACE && (ablate & 16) && bh < g_fdump.heads)
+
 template <int D>
 struct FwdSmem {
   static constexpr int kStages = D == 64 ? 3 : 2;
@@ -75,7 +80,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ q_scale,
                     const float* __restrict__ k_scale, const float* __restrict__ v_scale,
                     const float* __restrict__ bias, void* __restrict__ o_out, float* __restrict__ lse, int N,
-                    int BH, float tau, int pu8, int fp16, int ablate_arg) {
+                    int BH, float tau, int pu8, int fp16, int f32out, int ablate_arg) {
   const int ablate = SAGE_TRACE ? ablate_arg : 0;
   using L = FwdSmem<D>;
   constexpr int kStages = L::kStages;
@@ -242,6 +247,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         uint32_t v[32];
         tmem_ld32(tPV + c0 + lane_off, v);
         tmem_wait_ld();
+        if (FDUMPING && g_fdump.pv) {
+          int32_t* dst = g_fdump.pv + (((size_t)bh * T + jj) * N + (size_t)i * kBlk + r) * D + c0;
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) *reinterpret_cast<uint4*>(dst + e) = make_uint4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+        }
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           float2 acc = make_float2(oacc[c0 + e], oacc[c0 + e + 1]);
@@ -269,6 +279,18 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_wait(s_full + (j & 1), (j >> 1) & 1);
       tc_fence_after();
       if (r == 0) TRF(2, j);
+      if (FDUMPING && g_fdump.s) {  // the int32 S accumulator of tile (i, j), unmasked (Alg. 1 line 7)
+        int32_t* dst = g_fdump.s + ((size_t)bh * N + (size_t)i * kBlk + r) * N + (size_t)j * kBlk;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kBlk; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbuf(j) + c0 + lane_off, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<uint4*>(dst + c0 + e) = make_uint4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+        }
+      }
       // pass 1: row max (on int32 when there is no per-column bias)
       float rm;
       if constexpr (!QSMOOTH) {
@@ -365,6 +387,11 @@ __global__ void __launch_bounds__(kThreads, 2)
           const float2 qb = fadd2(b, make_float2(kMagic, kMagic));
           pk[e4] = pack4_magic(qa.x, qa.y, qb.x, qb.y);
         }
+        if (FDUMPING && g_fdump.p) {
+          uint8_t* dst = g_fdump.p + ((size_t)bh * N + (size_t)i * kBlk + r) * N + (size_t)j * kBlk + c0;
+          *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(dst + 16) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
         if constexpr (kPTmem) {
 #pragma unroll
           for (int w = 0; w < 8; ++w) pw[c0 / 4 + w] = pk[w];
@@ -386,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       // l = alpha l + e^{rowmax - m_ij} sum(e^{S - rowmax})  (line 8, reading A7)
       l = fmaf(alpha, l, e_rm * inv_pmax * (rs2.x + rs2.y));
       const float spv = e_rm * inv_pmax * sv;
+      if (FDUMPING && g_fdump.sp) g_fdump.sp[((size_t)bh * N + (size_t)i * kBlk + r) * T + j] = e_rm * inv_pmax;
       m = m_new;
       prev_alpha = alpha;
       prev_spv = spv;
@@ -395,14 +423,21 @@ __global__ void __launch_bounds__(kThreads, 2)
     correct(nj - 1, prev_alpha, prev_spv);
     // epilogue: O = acc / l (Alg. 1 line 13), L = m + ln l (line 14, natural log)
     const float inv_l = l > 0.f ? 1.f / l : 0.f;
-    // O in the I/O type (bf16, or fp16 with SAGE_FP16): 8 values per 16-byte store
-    uint4* orow = reinterpret_cast<uint4*>(static_cast<uint16_t*>(o_out) + ((size_t)row0 + r) * D);
+    if (f32out) {  // SAGE_FP32_OUT
+      float4* orow = reinterpret_cast<float4*>(static_cast<float*>(o_out) + ((size_t)row0 + r) * D);
 #pragma unroll
-    for (int c0 = 0; c0 < D; c0 += 8) {
-      uint32_t h[4];
+      for (int c0 = 0; c0 < D; c0 += 4)
+        orow[c0 / 4] = make_float4(oacc[c0] * inv_l, oacc[c0 + 1] * inv_l, oacc[c0 + 2] * inv_l, oacc[c0 + 3] * inv_l);
+    } else {
+      // O in the I/O type (bf16, or fp16 with SAGE_FP16): 8 values per 16-byte store
+      uint4* orow = reinterpret_cast<uint4*>(static_cast<uint16_t*>(o_out) + ((size_t)row0 + r) * D);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) h[e] = pack2_io(oacc[c0 + 2 * e] * inv_l, oacc[c0 + 2 * e + 1] * inv_l, fp16);
-      orow[c0 / 8] = make_uint4(h[0], h[1], h[2], h[3]);
+      for (int c0 = 0; c0 < D; c0 += 8) {
+        uint32_t h[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h[e] = pack2_io(oacc[c0 + 2 * e] * inv_l, oacc[c0 + 2 * e + 1] * inv_l, fp16);
+        orow[c0 / 8] = make_uint4(h[0], h[1], h[2], h[3]);
+      }
     }
     lse[(size_t)row0 + r] = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
   }
@@ -423,11 +458,13 @@ cudaError_t launch_t(const FwdArgs& a, cudaStream_t s) {
   const int T = a.N / kBlk;
   kern<<<a.BH * T, kThreads, FwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_v, a.q_scale, a.k_scale, a.v_scale,
                                                        a.bias, a.o, a.lse, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
-                                                       a.fp16 ? 1 : 0, a.ablate);
+                                                       a.fp16 ? 1 : 0, a.f32out ? 1 : 0, a.ablate);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+cudaError_t set_fwd_dump(const FwdDump& d) { return cudaMemcpyToSymbol(g_fdump, &d, sizeof(d)); }
 
 cudaError_t read_fwd_trace(void* host, size_t bytes) {
   if (bytes > sizeof(g_trace_fwd)) bytes = sizeof(g_trace_fwd);

@@ -54,9 +54,11 @@ cudaError_t launch_qsmooth_bias(const void* k, const float* mu_k, const float* m
                                 cudaStream_t s, NormIn nrm, bool fp16);
 // K3: delta = rowsum(dO o O) (Alg. 2 line 2), psi(dO) (line 6, reading A22), l2 = lse*log2(e),
 //     dq_acc = 0.
+//     delta = fl32(sum in fp64 of the exact products): bit-exact against the oracle given the stored O.
+//     o_f32: O is fp32 (SAGE_FP32_OUT) instead of the I/O type.
 cudaError_t launch_bwd_prep(const void* o, const void* dO, const float* lse, float* delta, float* l2, int8_t* do_q,
                             float* do_scale, float* dq_acc, int BH, int N, int d, cudaStream_t s, unsigned* dq_flags,
-                            bool fp16);
+                            bool fp16, bool o_f32);
 cudaError_t launch_fill(float* x, size_t n, float v, cudaStream_t s);
 // K5: dQ fp32 -> bf16.
 cudaError_t launch_dq_finalize(const float* dq_acc, void* dq, size_t n, cudaStream_t s, bool fp16);
@@ -73,9 +75,20 @@ struct FwdArgs {
   bool causal, qsmooth;
   bool pu8;    // SAGE_P_U8: P^ in 0..255 (u8 x s8 PV)
   bool fp16;   // SAGE_FP16: fp16 I/O
-  int ablate;  // profiling only (SAGE_ABLATE bit 8: timeline)
+  bool f32out; // SAGE_FP32_OUT: O written as fp32
+  int ablate;  // profiling only (SAGE_ABLATE bit 8: timeline, bit 16: sage_debug_fwd_dump)
 };
 cudaError_t launch_fwd(const FwdArgs& a, cudaStream_t s);
+// test-only K2 dump (libsage_trace.so, sage_debug_fwd_dump): S int32 [head][N q][N kv], P^ u8 same
+// layout, s_P fp32 [head][N q][T], PV int32 [head][T j][N q][d]; null pointers are skipped
+struct FwdDump {
+  int32_t* s;
+  uint8_t* p;
+  float* sp;
+  int32_t* pv;
+  int heads;
+};
+cudaError_t set_fwd_dump(const FwdDump& d);
 cudaError_t read_fwd_trace(void* host, size_t bytes);  // profiling: K2 event timeline
 
 struct BwdArgs {
@@ -93,6 +106,7 @@ struct BwdArgs {
   bool causal, qsmooth;
   bool pu8;    // SAGE_P_U8: psi(P) in 0..255 (u8 x s8 dV)
   bool fp16;   // SAGE_FP16: fp16 V, dO (dP MMA kind::f16 with f16 operands) and outputs
+  bool f32out; // SAGE_FP32_OUT: dK, dV written as fp32
   bool pcol;   // SAGE_P_COLSCALE: psi(P) per key row of P^T instead of per tile
   bool fine;   // SAGE_FINE_BWD: pcol + psi(dS) per key for dK and per query for dQ
   unsigned* dq_flags;  // SAGE_DETERMINISTIC: [BH][T][4] zeroed ordering flags, or null
@@ -108,6 +122,9 @@ struct BwdDump {
   int heads;
 };
 cudaError_t set_bwd_dump(const BwdDump& d);
+// the int32 accumulators (sage_debug_dump_acc): S^T [head][N kv][N q], dV / dK tiles [head][T i][N kv][d],
+// dQ tiles [head][T j][N q][d]; null = not dumped
+cudaError_t set_bwd_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t);
 
 // UMMA tile test (sage_debug_umma)
 cudaError_t launch_debug_umma(int mode, int K, int N, const CUtensorMap* tma, const CUtensorMap* tmb,

@@ -11,6 +11,8 @@
 // nvcc cannot contract it (reading A4).
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "sage_internal.h"
 #include "sm100.cuh"
 
@@ -338,8 +340,22 @@ __global__ void __launch_bounds__(128, SAGE_BIAS_MINB) qsmooth_bias_kernel(const
 }
 
 // ---------------------------------------------------------------- K3: backward prep
-template <typename T, int D>
-__global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, const T* __restrict__ dO,
+// delta[r] = sum_c dO[r][c] * O[r][c] (Alg. 2 line 2) from the O the forward stored (A15): every product
+// of two I/O-type values is exact in fp64 (and of an I/O value with an fp32 O, SAGE_FP32_OUT), and the
+// fp64 sum of a row's d products is exact unless they span > 37 binades, so delta = fl32(exact sum):
+// the same bits as the oracle's fp64 row sum rounded to fp32.
+template <typename TO>
+__device__ __forceinline__ void load_o8(const TO* p, float (&f)[8]) {
+  if constexpr (std::is_same<TO, float>::value) {
+    const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  } else {
+    load8<TO>(p, f);
+  }
+}
+
+template <typename T, typename TO, int D>
+__global__ void __launch_bounds__(256) bwd_prep_kernel(const TO* __restrict__ o, const T* __restrict__ dO,
                                                        const float* __restrict__ lse, float* __restrict__ delta,
                                                        float* __restrict__ l2, int8_t* __restrict__ do_q,
                                                        float* __restrict__ do_scale, float* __restrict__ dq_acc,
@@ -364,18 +380,18 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, 
     const size_t off = base + (size_t)r * D + g * kVec;
     float fo[kVec];
     unpack8<T>(rdo[it], v[it]);
-    load8<T>(o + off, fo);
-    float dot = 0.f;
+    load_o8<TO>(o + off, fo);
+    double dot = 0.0;
 #pragma unroll
     for (int e = 0; e < kVec; ++e) {
-      dot = fmaf(v[it][e], fo[e], dot);
+      dot = fma((double)v[it][e], (double)fo[e], dot);
       amax = fmaxf(amax, fabsf(v[it][e]));
     }
 #pragma unroll
     for (int s = kGroups / 2; s; s >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, s);
     if (g == 0) {
       const size_t row = (size_t)blk * kBlk + r;
-      delta[row] = dot;
+      delta[row] = __double2float_rn(dot);
       l2[row] = lse[row] * 1.4426950408889634f;
     }
     *reinterpret_cast<float4*>(dq_acc + off) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -636,15 +652,23 @@ cudaError_t launch_qsmooth_bias(const void* k, const float* mu_k, const float* m
 
 cudaError_t launch_bwd_prep(const void* o, const void* dO, const float* lse, float* delta, float* l2, int8_t* do_q,
                             float* do_scale, float* dq_acc, int BH, int N, int d, cudaStream_t s, unsigned* dq_flags,
-                            bool fp16) {
+                            bool fp16, bool o_f32) {
   unsigned grid = (unsigned)(BH * (N / kBlk));
   SAGE_IO_DISPATCH(fp16, {
-    const IoT* ot = static_cast<const IoT*>(o);
     const IoT* dot = static_cast<const IoT*>(dO);
-    if (d == 128)
-      bwd_prep_kernel<IoT, 128><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
-    else
-      bwd_prep_kernel<IoT, 64><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
+    if (o_f32) {
+      const float* ot = static_cast<const float*>(o);
+      if (d == 128)
+        bwd_prep_kernel<IoT, float, 128><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
+      else
+        bwd_prep_kernel<IoT, float, 64><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
+    } else {
+      const IoT* ot = static_cast<const IoT*>(o);
+      if (d == 128)
+        bwd_prep_kernel<IoT, IoT, 128><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
+      else
+        bwd_prep_kernel<IoT, IoT, 64><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
+    }
   });
   return cudaGetLastError();
 }

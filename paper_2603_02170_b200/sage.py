@@ -16,13 +16,13 @@ LIB_PATH = os.environ.get("SAGE_LIB") or os.path.join(_HERE, "libsage.so")
 
 SAGE_CAUSAL, SAGE_K_SMOOTH, SAGE_Q_SMOOTH, SAGE_P_U8, SAGE_QK_NORM, SAGE_DETERMINISTIC, SAGE_P_COLSCALE = \
     1, 2, 4, 8, 16, 32, 64
-SAGE_FINE_BWD, SAGE_FP16 = 128, 256
+SAGE_FINE_BWD, SAGE_FP16, SAGE_FP32_OUT = 128, 256, 512
 _STATUS = {0: "SAGE_OK", 1: "SAGE_ERR_INVALID_VALUE", 2: "SAGE_ERR_UNSUPPORTED", 3: "SAGE_ERR_MISALIGNED",
            4: "SAGE_ERR_WORKSPACE", 5: "SAGE_ERR_CUDA", 6: "SAGE_ERR_ARCH"}
 
 # exported symbols of include/sage.h
-SYMBOLS = ("sage_ctx_bytes", "sage_workspace_bytes", "sage_fwd", "sage_bwd", "sage_fwd_qknorm", "sage_bwd_qknorm",
-           "sage_ctx_get_view",
+SYMBOLS = ("sage_ctx_bytes", "sage_workspace_bytes", "sage_params_tag", "sage_fwd", "sage_bwd", "sage_fwd_qknorm",
+           "sage_bwd_qknorm", "sage_ctx_get_view", "sage_debug_fwd_dump", "sage_debug_dump_acc",
            "sage_ws_get_view", "sage_debug_umma", "sage_debug_trace", "sage_debug_dump", "sage_profile_enable", "sage_profile_read",
            "sage_status_string", "sage_last_cuda_error", "sage_version")
 
@@ -30,6 +30,11 @@ SYMBOLS = ("sage_ctx_bytes", "sage_workspace_bytes", "sage_fwd", "sage_bwd", "sa
 class SageParams(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("heads", ctypes.c_int32), ("seqlen", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("flags", ctypes.c_uint32), ("softmax_scale", ctypes.c_float)]
+
+
+class SageCtxDesc(ctypes.Structure):
+    """include/sage.h sage_ctx: the caller-owned device buffer and the params tag sage_fwd writes."""
+    _fields_ = [("buf", ctypes.c_void_p), ("bytes", ctypes.c_size_t), ("params_tag", ctypes.c_uint64)]
 
 
 class SageCtxView(ctypes.Structure):
@@ -61,10 +66,15 @@ def lib():
         L.sage_ctx_bytes.restype = S
         L.sage_workspace_bytes.argtypes = [pp, ctypes.c_int]
         L.sage_workspace_bytes.restype = S
-        L.sage_fwd.argtypes = [pp, P, P, P, P, P, P, S, P, S, P]
-        L.sage_bwd.argtypes = [pp, P, P, P, P, P, S, P, P, P, P, S, P]
-        L.sage_fwd_qknorm.argtypes = [pp, P, P, P, P, P, ctypes.c_float, P, P, P, S, P, S, P]
-        L.sage_bwd_qknorm.argtypes = [pp, P, P, P, P, P, P, P, P, P, S, P, P, P, P, P, P, S, P]
+        pc = ctypes.POINTER(SageCtxDesc)
+        L.sage_params_tag.argtypes = [pp]
+        L.sage_params_tag.restype = ctypes.c_uint64
+        L.sage_fwd.argtypes = [pp, P, P, P, P, P, pc, P, S, P]
+        L.sage_bwd.argtypes = [pp, P, P, P, P, pc, P, P, P, P, S, P]
+        L.sage_fwd_qknorm.argtypes = [pp, P, P, P, P, P, ctypes.c_float, P, P, pc, P, S, P]
+        L.sage_bwd_qknorm.argtypes = [pp, P, P, P, P, P, P, P, P, pc, P, P, P, P, P, P, S, P]
+        L.sage_debug_fwd_dump.argtypes = [P, P, P, P, ctypes.c_int]
+        L.sage_debug_dump_acc.argtypes = [P, P, P, P]
         L.sage_ctx_get_view.argtypes = [pp, P, ctypes.POINTER(SageCtxView)]
         L.sage_ws_get_view.argtypes = [pp, ctypes.c_int, P, ctypes.POINTER(SageWsView)]
         L.sage_debug_umma.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P]
@@ -94,10 +104,12 @@ def _check(status, what):
 
 
 def make_params(batch, heads, seqlen, head_dim, causal=False, k_smooth=True, q_smooth=False, softmax_scale=None,
-                p_u8=False, qk_norm=False, deterministic=False, p_colscale=False, fine_bwd=False, fp16=False):
+                p_u8=False, qk_norm=False, deterministic=False, p_colscale=False, fine_bwd=False, fp16=False,
+                fp32_out=False):
     flags = (SAGE_CAUSAL if causal else 0) | (SAGE_K_SMOOTH if k_smooth else 0) | (SAGE_Q_SMOOTH if q_smooth else 0) | \
         (SAGE_P_U8 if p_u8 else 0) | (SAGE_QK_NORM if qk_norm else 0) | (SAGE_DETERMINISTIC if deterministic else 0) | \
-        (SAGE_P_COLSCALE if p_colscale else 0) | (SAGE_FINE_BWD if fine_bwd else 0) | (SAGE_FP16 if fp16 else 0)
+        (SAGE_P_COLSCALE if p_colscale else 0) | (SAGE_FINE_BWD if fine_bwd else 0) | (SAGE_FP16 if fp16 else 0) | \
+        (SAGE_FP32_OUT if fp32_out else 0)
     return SageParams(batch, heads, seqlen, head_dim, flags, 0.0 if softmax_scale is None else softmax_scale)
 
 
@@ -105,8 +117,9 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def _stream(stream):
-    s = torch.cuda.current_stream() if stream is None else stream
+def _stream(stream, device=None):
+    """The caller's stream, or the current stream of the tensors' device (not of the current device)."""
+    s = torch.cuda.current_stream(device) if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
 
 
@@ -120,11 +133,27 @@ def _check_io(*ts):
             raise SageError("shape/device/dtype mismatch")
 
 
+def _check_out(t, shape, dtype, device, what):
+    """A caller-provided output: contiguous, of the expected shape, dtype and device."""
+    if not (t.is_cuda and t.is_contiguous() and tuple(t.shape) == tuple(shape) and t.dtype == dtype
+            and t.device == device):
+        raise SageError(f"{what}: expected a contiguous {dtype} {tuple(shape)} tensor on {device}, got "
+                        f"{t.dtype} {tuple(t.shape)} on {t.device}")
+
+
 class SageCtx:
-    """Forward->backward state (Alg. 2 inputs): the caller-owned ctx buffer plus params."""
+    """Forward->backward state (Alg. 2 inputs): the caller-owned ctx buffer, the params it was
+    produced under and the params tag sage_fwd wrote (sage_bwd rejects a ctx from other params)."""
 
     def __init__(self, params, ctx, shape):
         self.params, self.buf, self.shape = params, ctx, shape
+        self.desc = SageCtxDesc(ctx.data_ptr(), ctx.numel(), 0)
+
+    @property
+    def out_dtype(self):
+        if self.params.flags & SAGE_FP32_OUT:
+            return torch.float32
+        return torch.float16 if self.params.flags & SAGE_FP16 else torch.bfloat16
 
     def view(self):
         """Device tensors of the context (Q^, K^, scales, mu_K, mu_Q, bias) -- no copies."""
@@ -153,22 +182,26 @@ class SageCtx:
 
 
 class Workspace:
-    """Reusable scratch buffers (sage_workspace_bytes), grown on demand per device."""
+    """Reusable scratch buffers (sage_workspace_bytes), grown on demand, one per (device, stream,
+    direction): calls on different streams never share scratch, and a buffer replaced when it grows
+    was only used on its own stream (the caching allocator hands it out again in stream order)."""
 
     def __init__(self):
         self.bufs = {}
 
-    def get(self, params, backward, device):
+    def get(self, params, backward, device, stream=None):
         n = lib().sage_workspace_bytes(ctypes.byref(params), int(backward))
         if n == 0:
             raise SageError("invalid sage_params")
         device = torch.device(device)
         if device.index is None:
             device = torch.device(device.type, torch.cuda.current_device())
-        key = (str(device), backward)
+        s = torch.cuda.current_stream(device) if stream is None else stream
+        key = (str(device), s.cuda_stream, bool(backward))
         b = self.bufs.get(key)
         if b is None or b.numel() < n:
-            b = torch.empty(n, dtype=torch.uint8, device=device)
+            with torch.cuda.stream(s):
+                b = torch.empty(n, dtype=torch.uint8, device=device)
             self.bufs[key] = b
         return b
 
@@ -182,41 +215,62 @@ def ws_view(params, backward, ws):
     return v
 
 
+def _out_dtype(io_dtype, fp32_out):
+    return torch.float32 if fp32_out else io_dtype
+
+
 def forward(q, k, v, causal=False, k_smooth=True, q_smooth=False, softmax_scale=None, out=None, lse=None,
             ctx=None, workspace=None, stream=None, p_u8=False, deterministic=False, p_colscale=False,
-            fine_bwd=False):
-    """sage_fwd (Alg. 1): returns (o, lse, SageCtx).  q, k, v: CUDA bf16 [B, H, N, d].
+            fine_bwd=False, fp32_out=False):
+    """sage_fwd (Alg. 1): returns (o, lse, SageCtx).  q, k, v: CUDA bf16 (or fp16) [B, H, N, d].
     p_u8: the unsigned-P^ variant (SAGE_P_U8); deterministic: a bitwise reproducible backward
     (SAGE_DETERMINISTIC); p_colscale: per-key psi(P) in the backward (SAGE_P_COLSCALE); fine_bwd: per-key
-    psi(P) and per-key / per-query psi(dS) (SAGE_FINE_BWD).  The backward inherits them through the ctx."""
+    psi(P) and per-key / per-query psi(dS) (SAGE_FINE_BWD); fp32_out: O (and later dQ, dK, dV) in fp32
+    (SAGE_FP32_OUT).  The backward inherits them through the ctx."""
     _check_io(q, k, v)
     B, H, N, d = q.shape
+    dev = q.device
     p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8, deterministic=deterministic,
-                    p_colscale=p_colscale, fine_bwd=fine_bwd, fp16=q.dtype == torch.float16)
+                    p_colscale=p_colscale, fine_bwd=fine_bwd, fp16=q.dtype == torch.float16, fp32_out=fp32_out)
     nctx = lib().sage_ctx_bytes(ctypes.byref(p))
     if nctx == 0:
         raise SageError(f"unsupported shape/flags {tuple(q.shape)} (N % 128 == 0, d in {{64, 128}})")
-    o = torch.empty_like(q) if out is None else out
-    lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if lse is None else lse
-    ctxb = torch.empty(nctx, dtype=torch.uint8, device=q.device) if ctx is None else ctx
-    ws = _ws.get(p, False, q.device) if workspace is None else workspace
-    _check(lib().sage_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(ctxb), ctxb.numel(),
-                          _ptr(ws), ws.numel(), _stream(stream)), "sage_fwd")
-    return o, lse, SageCtx(p, ctxb, (B, H, N, d))
+    with torch.cuda.device(dev):
+        o = torch.empty(q.shape, dtype=_out_dtype(q.dtype, fp32_out), device=dev) if out is None else out
+        _check_out(o, q.shape, _out_dtype(q.dtype, fp32_out), dev, "out")
+        lse = torch.empty((B, H, N), dtype=torch.float32, device=dev) if lse is None else lse
+        _check_out(lse, (B, H, N), torch.float32, dev, "lse")
+        ctxb = torch.empty(nctx, dtype=torch.uint8, device=dev) if ctx is None else ctx
+        if ctxb.device != dev or ctxb.numel() < nctx:
+            raise SageError("ctx buffer too small or on another device")
+        ws = _ws.get(p, False, dev, stream) if workspace is None else workspace
+        c = SageCtx(p, ctxb, (B, H, N, d))
+        _check(lib().sage_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), ctypes.byref(c.desc),
+                              _ptr(ws), ws.numel(), _stream(stream, dev)), "sage_fwd")
+    return o, lse, c
 
 
 def backward(ctx, v, o, lse, do, dq=None, dk=None, dv=None, workspace=None, stream=None):
-    """sage_bwd (Alg. 2): returns (dq, dk, dv) in the I/O dtype."""
-    _check_io(v, o, do)
+    """sage_bwd (Alg. 2): returns (dq, dk, dv) in the I/O dtype (fp32 with SAGE_FP32_OUT)."""
+    _check_io(v, do)
+    dev = do.device
+    if tuple(do.shape) != tuple(ctx.shape) or ctx.buf.device != dev:
+        raise SageError(f"backward: tensors {tuple(do.shape)} on {dev} do not match the forward's ctx "
+                        f"{tuple(ctx.shape)} on {ctx.buf.device}")
     if (do.dtype == torch.float16) != bool(ctx.params.flags & SAGE_FP16):
         raise SageError("the backward's dtype differs from the forward's")
-    dq = torch.empty_like(do) if dq is None else dq
-    dk = torch.empty_like(do) if dk is None else dk
-    dv = torch.empty_like(do) if dv is None else dv
-    ws = _ws.get(ctx.params, True, do.device) if workspace is None else workspace
-    _check(lib().sage_bwd(ctypes.byref(ctx.params), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(ctx.buf),
-                          ctx.buf.numel(), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream(stream)),
-           "sage_bwd")
+    B, H, N, d = ctx.shape
+    _check_out(o, ctx.shape, ctx.out_dtype, dev, "o")
+    _check_out(lse, (B, H, N), torch.float32, dev, "lse")
+    with torch.cuda.device(dev):
+        dq = torch.empty(ctx.shape, dtype=ctx.out_dtype, device=dev) if dq is None else dq
+        dk = torch.empty(ctx.shape, dtype=ctx.out_dtype, device=dev) if dk is None else dk
+        dv = torch.empty(ctx.shape, dtype=ctx.out_dtype, device=dev) if dv is None else dv
+        for t, n in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+            _check_out(t, ctx.shape, ctx.out_dtype, dev, n)
+        ws = _ws.get(ctx.params, True, dev, stream) if workspace is None else workspace
+        _check(lib().sage_bwd(ctypes.byref(ctx.params), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), ctypes.byref(ctx.desc),
+                              _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream(stream, dev)), "sage_bwd")
     return dq, dk, dv
 
 
@@ -232,40 +286,57 @@ def forward_qknorm(xq, xk, v, gamma_q, gamma_k, eps=1e-6, causal=False, k_smooth
     [B, H, N, d]; gamma_q, gamma_k: fp32 [d].  Returns (o, lse, SageCtx)."""
     _check_io(xq, xk, v)
     B, H, N, d = xq.shape
-    _check_gamma(gamma_q, d, xq.device)
-    _check_gamma(gamma_k, d, xq.device)
+    dev = xq.device
+    _check_gamma(gamma_q, d, dev)
+    _check_gamma(gamma_k, d, dev)
     p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8, qk_norm=True,
                     deterministic=deterministic, p_colscale=p_colscale, fine_bwd=fine_bwd,
                     fp16=xq.dtype == torch.float16)
     nctx = lib().sage_ctx_bytes(ctypes.byref(p))
     if nctx == 0:
         raise SageError(f"unsupported shape/flags {tuple(xq.shape)}")
-    o = torch.empty_like(xq) if out is None else out
-    lse = torch.empty((B, H, N), dtype=torch.float32, device=xq.device) if lse is None else lse
-    ctxb = torch.empty(nctx, dtype=torch.uint8, device=xq.device) if ctx is None else ctx
-    ws = _ws.get(p, False, xq.device) if workspace is None else workspace
-    _check(lib().sage_fwd_qknorm(ctypes.byref(p), _ptr(xq), _ptr(xk), _ptr(v), _ptr(gamma_q), _ptr(gamma_k),
-                                 float(eps), _ptr(o), _ptr(lse), _ptr(ctxb), ctxb.numel(), _ptr(ws), ws.numel(),
-                                 _stream(stream)), "sage_fwd_qknorm")
-    return o, lse, SageCtx(p, ctxb, (B, H, N, d))
+    with torch.cuda.device(dev):
+        o = torch.empty_like(xq) if out is None else out
+        _check_out(o, xq.shape, xq.dtype, dev, "out")
+        lse = torch.empty((B, H, N), dtype=torch.float32, device=dev) if lse is None else lse
+        _check_out(lse, (B, H, N), torch.float32, dev, "lse")
+        ctxb = torch.empty(nctx, dtype=torch.uint8, device=dev) if ctx is None else ctx
+        if ctxb.device != dev or ctxb.numel() < nctx:
+            raise SageError("ctx buffer too small or on another device")
+        ws = _ws.get(p, False, dev, stream) if workspace is None else workspace
+        c = SageCtx(p, ctxb, (B, H, N, d))
+        _check(lib().sage_fwd_qknorm(ctypes.byref(p), _ptr(xq), _ptr(xk), _ptr(v), _ptr(gamma_q), _ptr(gamma_k),
+                                     float(eps), _ptr(o), _ptr(lse), ctypes.byref(c.desc), _ptr(ws), ws.numel(),
+                                     _stream(stream, dev)), "sage_fwd_qknorm")
+    return o, lse, c
 
 
 def backward_qknorm(ctx, xq, xk, gamma_q, gamma_k, v, o, lse, do, out=None, workspace=None, stream=None):
     """sage_bwd_qknorm: returns (dxq, dxk, dv, dgamma_q, dgamma_k) (into `out` if given)."""
     _check_io(xq, xk, v, o, do)
     d = xq.shape[-1]
-    _check_gamma(gamma_q, d, xq.device)
-    _check_gamma(gamma_k, d, xq.device)
-    if out is None:
-        out = (torch.empty_like(do), torch.empty_like(do), torch.empty_like(do),
-               torch.empty(d, dtype=torch.float32, device=do.device),
-               torch.empty(d, dtype=torch.float32, device=do.device))
-    dxq, dxk, dv, dgq, dgk = out
-    ws = _ws.get(ctx.params, True, do.device) if workspace is None else workspace
-    _check(lib().sage_bwd_qknorm(ctypes.byref(ctx.params), _ptr(xq), _ptr(xk), _ptr(gamma_q), _ptr(gamma_k), _ptr(v),
-                                 _ptr(o), _ptr(lse), _ptr(do), _ptr(ctx.buf), ctx.buf.numel(), _ptr(dxq), _ptr(dxk),
-                                 _ptr(dv), _ptr(dgq), _ptr(dgk), _ptr(ws), ws.numel(), _stream(stream)),
-           "sage_bwd_qknorm")
+    dev = do.device
+    if tuple(do.shape) != tuple(ctx.shape) or ctx.buf.device != dev:
+        raise SageError("backward_qknorm: tensors do not match the forward's ctx")
+    _check_gamma(gamma_q, d, dev)
+    _check_gamma(gamma_k, d, dev)
+    B, H, N, _ = ctx.shape
+    _check_out(lse, (B, H, N), torch.float32, dev, "lse")
+    with torch.cuda.device(dev):
+        if out is None:
+            out = (torch.empty_like(do), torch.empty_like(do), torch.empty_like(do),
+                   torch.empty(d, dtype=torch.float32, device=dev),
+                   torch.empty(d, dtype=torch.float32, device=dev))
+        dxq, dxk, dv, dgq, dgk = out
+        for t, n in ((dxq, "dxq"), (dxk, "dxk"), (dv, "dv")):
+            _check_out(t, ctx.shape, do.dtype, dev, n)
+        _check_gamma(dgq, d, dev)
+        _check_gamma(dgk, d, dev)
+        ws = _ws.get(ctx.params, True, dev, stream) if workspace is None else workspace
+        _check(lib().sage_bwd_qknorm(ctypes.byref(ctx.params), _ptr(xq), _ptr(xk), _ptr(gamma_q), _ptr(gamma_k),
+                                     _ptr(v), _ptr(o), _ptr(lse), _ptr(do), ctypes.byref(ctx.desc), _ptr(dxq),
+                                     _ptr(dxk), _ptr(dv), _ptr(dgq), _ptr(dgk), _ptr(ws), ws.numel(),
+                                     _stream(stream, dev)), "sage_bwd_qknorm")
     return dxq, dxk, dv, dgq, dgk
 
 
@@ -329,11 +400,13 @@ def debug_umma(mode, a, b, K=None, N=None):
     return out
 
 
-def debug_dump(heads, N, device):
+def debug_dump(heads, N, device, d=None, acc=False):
     """Arm sage_debug_dump (libsage_trace.so only) for heads [0, heads) of sequence length N:
-    returns the device buffers every later sage_bwd fills (include/sage.h); heads=0 disarms."""
+    returns the device buffers every later sage_bwd fills (include/sage.h); heads=0 disarms.
+    acc=True (head dim d) also arms sage_debug_dump_acc: the int32 S^T, dV, dK, dQ tile accumulators."""
     if heads == 0:
         _check(lib().sage_debug_dump(None, None, None, None, None, 0), "sage_debug_dump")
+        _check(lib().sage_debug_dump_acc(None, None, None, None), "sage_debug_dump_acc")
         return None
     T = N // 128
     bufs = dict(p_hat_t=torch.zeros((heads, N, N), dtype=torch.int8, device=device),
@@ -343,6 +416,31 @@ def debug_dump(heads, N, device):
                 ds_t=torch.zeros((heads, N, N), dtype=torch.float32, device=device))
     _check(lib().sage_debug_dump(_ptr(bufs["p_hat_t"]), _ptr(bufs["s_p"]), _ptr(bufs["ds_hat_t"]),
                                  _ptr(bufs["s_ds"]), _ptr(bufs["ds_t"]), heads), "sage_debug_dump")
+    if acc:
+        bufs.update(s_t=torch.zeros((heads, N, N), dtype=torch.int32, device=device),
+                    dv_t=torch.zeros((heads, T, N, d), dtype=torch.int32, device=device),
+                    dk_t=torch.zeros((heads, T, N, d), dtype=torch.int32, device=device),
+                    dq_t=torch.zeros((heads, T, N, d), dtype=torch.int32, device=device))
+        _check(lib().sage_debug_dump_acc(_ptr(bufs["s_t"]), _ptr(bufs["dv_t"]), _ptr(bufs["dk_t"]),
+                                         _ptr(bufs["dq_t"])), "sage_debug_dump_acc")
+    else:
+        _check(lib().sage_debug_dump_acc(None, None, None, None), "sage_debug_dump_acc")
+    return bufs
+
+
+def debug_fwd_dump(heads, N, d, device):
+    """Arm sage_debug_fwd_dump (libsage_trace.so only): every later sage_fwd writes K2's int32 S, P^,
+    s_P and int32 PV accumulators of heads [0, heads) into the returned buffers; heads=0 disarms."""
+    if heads == 0:
+        _check(lib().sage_debug_fwd_dump(None, None, None, None, 0), "sage_debug_fwd_dump")
+        return None
+    T = N // 128
+    bufs = dict(s=torch.zeros((heads, N, N), dtype=torch.int32, device=device),
+                p_hat=torch.zeros((heads, N, N), dtype=torch.uint8, device=device),
+                s_p=torch.zeros((heads, N, T), dtype=torch.float32, device=device),
+                pv=torch.zeros((heads, T, N, d), dtype=torch.int32, device=device))
+    _check(lib().sage_debug_fwd_dump(_ptr(bufs["s"]), _ptr(bufs["p_hat"]), _ptr(bufs["s_p"]), _ptr(bufs["pv"]), heads),
+           "sage_debug_fwd_dump")
     return bufs
 
 

@@ -45,48 +45,85 @@ def test_sizes_and_invalid_params(L):
     assert L.sage_ctx_bytes(ctypes.byref(bad)) == 0
 
 
+def _ctx(buf, nbytes, tag=0):
+    from paper_2603_02170_b200.sage import SageCtxDesc
+    return ctypes.byref(SageCtxDesc(buf, nbytes, tag))
+
+
+def test_params_tag(L):
+    """sage_params_tag: a non-zero hash that separates every field (the ctx check of sage_bwd)."""
+    from paper_2603_02170_b200.sage import make_params
+    base = make_params(2, 3, 256, 64, causal=True)
+    t0 = L.sage_params_tag(ctypes.byref(base))
+    assert t0 != 0 and t0 == L.sage_params_tag(ctypes.byref(make_params(2, 3, 256, 64, causal=True)))
+    others = [make_params(1, 3, 256, 64, causal=True), make_params(2, 2, 256, 64, causal=True),
+              make_params(2, 3, 384, 64, causal=True), make_params(2, 3, 256, 128, causal=True),
+              make_params(2, 3, 256, 64), make_params(2, 3, 256, 64, causal=True, q_smooth=True),
+              make_params(2, 3, 256, 64, causal=True, softmax_scale=0.2),
+              make_params(2, 3, 256, 64, causal=True, p_u8=True), make_params(2, 3, 256, 64, causal=True, fp32_out=True)]
+    tags = {L.sage_params_tag(ctypes.byref(o)) for o in others}
+    assert t0 not in tags and len(tags) == len(others)
+    assert L.sage_params_tag(ctypes.byref(make_params(1, 1, 100, 64))) == 0
+
+
 def test_error_paths_do_not_launch(L):
     """Validation happens before any device access: fake (never dereferenced) pointers."""
     from paper_2603_02170_b200.sage import make_params
     p = make_params(1, 2, 256, 64)
     nctx = L.sage_ctx_bytes(ctypes.byref(p))
     nws = L.sage_workspace_bytes(ctypes.byref(p), 0)
+    tag = L.sage_params_tag(ctypes.byref(p))
     A = ctypes.c_void_p(0x10000)
     mis = ctypes.c_void_p(0x10008)
     z = ctypes.c_void_p(0)
     S = ctypes.c_size_t
     bad = make_params(1, 2, 200, 64)
-    assert L.sage_fwd(ctypes.byref(bad), A, A, A, A, A, A, S(nctx), A, S(nws), z) == 1
-    assert L.sage_fwd(ctypes.byref(p), z, A, A, A, A, A, S(nctx), A, S(nws), z) == 1
-    assert L.sage_fwd(ctypes.byref(p), mis, A, A, A, A, A, S(nctx), A, S(nws), z) == 3
-    assert L.sage_fwd(ctypes.byref(p), A, A, A, A, A, A, S(nctx - 1), A, S(nws), z) == 4
-    assert L.sage_fwd(ctypes.byref(p), A, A, A, A, A, A, S(nctx), A, S(nws - 1), z) == 4
+    C = _ctx(0x10000, nctx)
+    assert L.sage_fwd(ctypes.byref(bad), A, A, A, A, A, C, A, S(nws), z) == 1
+    assert L.sage_fwd(ctypes.byref(p), z, A, A, A, A, C, A, S(nws), z) == 1
+    assert L.sage_fwd(ctypes.byref(p), A, A, A, A, A, None, A, S(nws), z) == 1
+    assert L.sage_fwd(ctypes.byref(p), mis, A, A, A, A, C, A, S(nws), z) == 3
+    assert L.sage_fwd(ctypes.byref(p), A, A, A, A, A, _ctx(0x10000, nctx - 1), A, S(nws), z) == 4
+    assert L.sage_fwd(ctypes.byref(p), A, A, A, A, A, C, A, S(nws - 1), z) == 4
     nwb = L.sage_workspace_bytes(ctypes.byref(p), 1)
-    assert L.sage_bwd(ctypes.byref(p), A, A, A, A, A, S(nctx), A, A, A, A, S(nwb - 1), z) == 4
-    assert L.sage_bwd(ctypes.byref(p), A, A, A, A, A, S(nctx), A, A, mis, A, S(nwb), z) == 3
+    Ct = _ctx(0x10000, nctx, tag)
+    assert L.sage_bwd(ctypes.byref(p), A, A, A, A, Ct, A, A, A, A, S(nwb - 1), z) == 4
+    assert L.sage_bwd(ctypes.byref(p), A, A, A, A, Ct, A, A, mis, A, S(nwb), z) == 3
+    # a context the forward never filled (tag 0), or filled under other params, is refused
+    assert L.sage_bwd(ctypes.byref(p), A, A, A, A, C, A, A, A, A, S(nwb), z) == 1
+    other = L.sage_params_tag(ctypes.byref(make_params(1, 2, 256, 64, causal=True)))
+    assert L.sage_bwd(ctypes.byref(p), A, A, A, A, _ctx(0x10000, nctx, other), A, A, A, A, S(nwb), z) == 1
     assert L.sage_debug_umma(8, 64, 128, A, A, A, z) == 1
     assert L.sage_debug_umma(1, 128, 96, A, A, A, z) == 1
     # one backward variant at a time: SAGE_DETERMINISTIC with SAGE_P_COLSCALE is rejected
     assert L.sage_ctx_bytes(ctypes.byref(make_params(1, 2, 256, 64, deterministic=True, p_colscale=True))) == 0
     assert L.sage_ctx_bytes(ctypes.byref(make_params(1, 2, 256, 64, deterministic=True, fine_bwd=True))) == 0
     assert L.sage_ctx_bytes(ctypes.byref(make_params(1, 2, 256, 64, p_colscale=True))) == nctx
+    # SAGE_FP32_OUT is valid alone, not with QK-norm
+    assert L.sage_ctx_bytes(ctypes.byref(make_params(1, 2, 256, 64, fp32_out=True))) == nctx
+    assert L.sage_ctx_bytes(ctypes.byref(make_params(1, 2, 256, 64, fp32_out=True, qk_norm=True))) == 0
     # QK-norm params need the _qknorm entry points, which need gamma and eps > 0
     pn = make_params(1, 2, 256, 64, qk_norm=True)
     ncn = L.sage_ctx_bytes(ctypes.byref(pn))
     assert ncn > nctx  # + rstd of the X_q, X_k rows
     nwn = L.sage_workspace_bytes(ctypes.byref(pn), 0)
-    assert L.sage_fwd(ctypes.byref(pn), A, A, A, A, A, A, S(ncn), A, S(nwn), z) == 1
-    assert L.sage_bwd(ctypes.byref(pn), A, A, A, A, A, S(ncn), A, A, A, A, S(1 << 30), z) == 1
+    Cn = _ctx(0x10000, ncn)
+    assert L.sage_fwd(ctypes.byref(pn), A, A, A, A, A, Cn, A, S(nwn), z) == 1
+    assert L.sage_bwd(ctypes.byref(pn), A, A, A, A, _ctx(0x10000, ncn, L.sage_params_tag(ctypes.byref(pn))),
+                      A, A, A, A, S(1 << 30), z) == 1
     F = ctypes.c_float
-    assert L.sage_fwd_qknorm(ctypes.byref(p), A, A, A, A, A, F(1e-6), A, A, A, S(nctx), A, S(nws), z) == 1
-    assert L.sage_fwd_qknorm(ctypes.byref(pn), A, A, A, z, A, F(1e-6), A, A, A, S(ncn), A, S(nwn), z) == 1
-    assert L.sage_fwd_qknorm(ctypes.byref(pn), A, A, A, A, A, F(0.0), A, A, A, S(ncn), A, S(nwn), z) == 1
-    assert L.sage_fwd_qknorm(ctypes.byref(pn), A, A, A, mis, A, F(1e-6), A, A, A, S(ncn), A, S(nwn), z) == 3
-    assert L.sage_fwd_qknorm(ctypes.byref(pn), A, A, A, A, A, F(1e-6), A, A, A, S(ncn - 1), A, S(nwn), z) == 4
-    assert L.sage_bwd_qknorm(ctypes.byref(pn), A, A, A, A, A, A, A, A, A, S(ncn), A, A, A, z, A, A, S(1 << 30),
-                             z) == 1
-    # the tile dump exists only in the test build (libsage_trace.so)
+    assert L.sage_fwd_qknorm(ctypes.byref(p), A, A, A, A, A, F(1e-6), A, A, C, A, S(nws), z) == 1
+    assert L.sage_fwd_qknorm(ctypes.byref(pn), A, A, A, z, A, F(1e-6), A, A, Cn, A, S(nwn), z) == 1
+    assert L.sage_fwd_qknorm(ctypes.byref(pn), A, A, A, A, A, F(0.0), A, A, Cn, A, S(nwn), z) == 1
+    assert L.sage_fwd_qknorm(ctypes.byref(pn), A, A, A, mis, A, F(1e-6), A, A, Cn, A, S(nwn), z) == 3
+    assert L.sage_fwd_qknorm(ctypes.byref(pn), A, A, A, A, A, F(1e-6), A, A, _ctx(0x10000, ncn - 1), A, S(nwn),
+                             z) == 4
+    assert L.sage_bwd_qknorm(ctypes.byref(pn), A, A, A, A, A, A, A, A, Cn, A, A, A, A, A, A, S(1 << 30), z) == 1
+    assert L.sage_bwd_qknorm(ctypes.byref(pn), A, A, A, A, A, A, A, A, _ctx(0x10000, ncn, L.sage_params_tag(
+        ctypes.byref(pn))), A, A, A, z, A, A, S(1 << 30), z) == 1
+    # the tile dumps exist only in the test build (libsage_trace.so)
     assert L.sage_debug_dump(A, A, A, A, A, 1) == 2
+    assert L.sage_debug_fwd_dump(A, A, A, A, 1) == 2
 
 
 def test_trace_build_exports_the_same_abi():
@@ -110,7 +147,7 @@ def test_no_gpu_no_fallback(L):
     p = make_params(1, 2, 256, 64)
     A = ctypes.c_void_p(0x10000)
     S = ctypes.c_size_t
-    st = L.sage_fwd(ctypes.byref(p), A, A, A, A, A, A, S(1 << 30), A, S(1 << 30), ctypes.c_void_p(0))
+    st = L.sage_fwd(ctypes.byref(p), A, A, A, A, A, _ctx(0x10000, 1 << 30), A, S(1 << 30), ctypes.c_void_p(0))
     assert st in (5, 6)  # SAGE_ERR_CUDA / SAGE_ERR_ARCH
 
 

@@ -28,45 +28,51 @@ def _gpu():
 
 
 def _run(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, deterministic=False, p_colscale=False,
-         fine_bwd=False):
+         fine_bwd=False, softmax_scale=None, fp32_out=False):
     dev = "cuda"
     qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
     o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8,
-                               deterministic=deterministic, p_colscale=p_colscale, fine_bwd=fine_bwd)
+                               deterministic=deterministic, p_colscale=p_colscale, fine_bwd=fine_bwd,
+                               softmax_scale=softmax_scale, fp32_out=fp32_out)
     dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
     torch.cuda.synchronize()
     return dict(o=o, lse=lse, dq=dq, dk=dk, dv=dv, ctx=ctx)
 
 
-def _oracle(q, k, v, do, heads, causal, k_smooth, q_smooth, p_u8=False, p_col=False, ds_fine=False):
+def _oracle(q, k, v, do, heads, causal, k_smooth, q_smooth, p_u8=False, p_col=False, ds_fine=False, tau=None,
+            o_round=round_bf16):
     """Oracle on the selected flattened heads; O is stored as bf16 before the backward (A15)."""
     B, H, N, d = q.shape
     sel = lambda t: f64(t).reshape(B * H, N, d)[heads]
     qn, kn, vn, don = map(sel, (q, k, v, do))
-    kw = dict(causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8)
+    kw = dict(causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8, tau=tau)
     f = oracle.fwd(qn, kn, vn, **kw)
-    o_st = round_bf16(f["o"])
+    o_st = o_round(f["o"])
     b = oracle.bwd(qn, kn, vn, o_st, don, f["lse"], p_col=p_col, ds_fine=ds_fine, **kw)
     return f, b
 
 
-def _compare(gpu, f, b, heads, B, H, N, d):
+def _compare(gpu, f, b, heads, B, H, N, d, out_round=round_bf16):
+    """rel-L2 / cos over all compared heads (global flatten, A21) and the worst single head; max |dL|."""
     flat = lambda t: f64(t).reshape(B * H, N, d)[heads]
     res = {}
     for name, ref in (("o", f["o"]), ("dq", b["dq"]), ("dk", b["dk"]), ("dv", b["dv"])):
         got = flat(gpu[name])
-        ref = round_bf16(ref)
-        res[name] = (rel_l2(ref, got), cos_sim(ref, got))
+        ref = out_round(ref)
+        worst = max(rel_l2(ref[h], got[h]) for h in range(len(heads)))
+        res[name] = (rel_l2(ref, got), cos_sim(ref, got), worst)
     lse = f64(gpu["lse"]).reshape(B * H, N)[heads]
     res["lse"] = float(np.abs(lse - f["lse"]).max())
     return res
 
 
 def _assert_ok(res, what):
+    """North-star tolerance: rel-L2 <= 2e-3 and cos >= 0.9999 globally and for every head; L within 1e-5
+    absolute."""
     for name in ("o", "dq", "dk", "dv"):
-        rl, cs = res[name]
-        assert rl <= REL_TOL and cs >= COS_TOL, (what, name, rl, cs, res)
-    assert res["lse"] <= 1e-4, (what, res)
+        rl, cs, worst = res[name]
+        assert rl <= REL_TOL and cs >= COS_TOL and worst <= REL_TOL, (what, name, rl, cs, worst, res)
+    assert res["lse"] <= 1e-5, (what, res)
 
 
 # ------------------------------------------------------------------ Tier B: UMMA tiles
@@ -146,8 +152,12 @@ def test_tier_a_bit_exact(d, q_smooth):
     np.testing.assert_array_equal(do8.reshape(B * H, N, d), b["do8"])
     np.testing.assert_array_equal(sdo.reshape(B * H, T), b["sdo"])
     delta = wsb[wb.delta - base: wb.delta - base + B * H * N * 4].view(torch.float32).cpu().numpy()
-    # delta from the GPU's own bf16 O; the oracle's from its own O: compare loosely
-    assert rel_l2(b["delta"], delta.reshape(B * H, N)) < 1e-2
+    # delta = rowsum(dO o O) from the O the forward stored (A15): the oracle given the GPU's stored O
+    # (exact fp64 sum of exact products) rounded once to fp32 -- bit-exact
+    flat = lambda t: f64(t).reshape(B * H, N, d)
+    b_st = oracle.bwd(flat(q), flat(k), flat(v), flat(gpu["o"]), flat(do), f["lse"], causal=True, k_smooth=True,
+                      q_smooth=q_smooth)
+    np.testing.assert_array_equal(delta.reshape(B * H, N), b_st["delta"].astype(np.float32))
 
 
 # ------------------------------------------------------------------ fused fwd + bwd parity
@@ -458,3 +468,107 @@ def test_max_seqlen_properties():
     assert (o - 1.0).abs().max().item() < 0.02
     for name in ("dq", "dk", "dv"):
         assert torch.count_nonzero(gpu[name]).item() == 0, name
+
+
+# ------------------------------------------------------------------ softmax scale, fp32 outputs, binding checks
+@pytest.mark.parametrize("d,tau", [(64, 0.05), (128, 0.2)])
+def test_non_default_softmax_scale(d, tau):
+    """sage_params.softmax_scale (reading A6): S, dQ and dK carry the caller's tau."""
+    B, H, N = 1, 2, 384
+    q, k, v, do = make_inputs(B, H, N, d, "gauss", seed=70 + d, sigma=2.0)
+    gpu = _run(q, k, v, do, True, True, False, softmax_scale=tau)
+    heads = list(range(B * H))
+    f, b = _oracle(q, k, v, do, heads, True, True, False, tau=tau)
+    _assert_ok(_compare(gpu, f, b, heads, B, H, N, d), ("tau", d, tau))
+    # and it differs from the default scale's result
+    g0 = _run(q, k, v, do, True, True, False)
+    assert rel_l2(f64(g0["o"]), f64(gpu["o"])) > 1e-2
+
+
+FP32_CASES = [
+    (1, 2, 384, 64, True, True, False, "qknorm"),
+    (1, 2, 256, 128, False, True, True, "outlier_kq"),
+]
+
+
+@pytest.mark.parametrize("B,H,N,d,causal,ks,qs,recipe", FP32_CASES)
+def test_fp32_out_against_unrounded_oracle(B, H, N, d, causal, ks, qs, recipe):
+    """SAGE_FP32_OUT (reading A18): O, dQ, dK, dV in fp32, compared against the oracle's unrounded double
+    results (O stored as fp32 for delta, A15) -- without the bf16 rounding that takes 1.66e-3 of the budget
+    the GPU is within 5e-4 of the quantised oracle."""
+    q, k, v, do = make_inputs(B, H, N, d, recipe, seed=1300 + N + d)
+    gpu = _run(q, k, v, do, causal, ks, qs, fp32_out=True)
+    for n in ("o", "dq", "dk", "dv"):
+        assert gpu[n].dtype == torch.float32, n
+    heads = list(range(B * H))
+    f32 = lambda x: np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+    f, b = _oracle(q, k, v, do, heads, causal, ks, qs, o_round=f32)
+    res = _compare(gpu, f, b, heads, B, H, N, d, out_round=lambda x: x)
+    for name in ("o", "dq", "dk", "dv"):
+        assert res[name][0] <= 5e-4 and res[name][1] >= 0.99999, (name, res)
+    assert res["lse"] <= 1e-5, res
+
+
+def test_binding_rejects_mismatched_tensors():
+    """The binding checks shapes, dtypes and devices against the forward's context before calling the C
+    ABI, and the C ABI refuses a context produced under other params (sage_ctx.params_tag)."""
+    q, k, v, do = (t.cuda() for t in make_inputs(1, 2, 256, 64, "gauss", seed=3))
+    o, lse, ctx = sage.forward(q, k, v, causal=True)
+    with pytest.raises(sage.SageError):
+        sage.backward(ctx, v[:, :1].contiguous(), o, lse, do[:, :1].contiguous())
+    with pytest.raises(sage.SageError):
+        sage.backward(ctx, v, o, lse[:, :1].contiguous(), do)
+    with pytest.raises(sage.SageError):
+        sage.forward(q, k, v, out=torch.empty(1, 2, 256, 64, dtype=torch.float32, device="cuda"))
+    # a ctx from a non-causal forward presented with causal params: refused by the library
+    o2, lse2, ctx2 = sage.forward(q, k, v, causal=False)
+    ctx2.params = ctx.params
+    with pytest.raises(sage.SageError, match="INVALID_VALUE"):
+        sage.backward(ctx2, v, o2, lse2, do)
+    # a context never filled by sage_fwd (tag 0)
+    ctx3 = sage.SageCtx(ctx.params, torch.empty_like(ctx.buf), ctx.shape)
+    with pytest.raises(sage.SageError, match="INVALID_VALUE"):
+        sage.backward(ctx3, v, o, lse, do)
+
+
+def test_streams_and_devices():
+    """Calls on a side stream use that stream's own workspace and agree with the default stream's."""
+    q, k, v, do = (t.cuda() for t in make_inputs(1, 2, 256, 128, "qknorm", seed=4))
+    o, lse, ctx = sage.forward(q, k, v, causal=True)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        o2, lse2, ctx2 = sage.forward(q, k, v, causal=True)
+        dq2, dk2, dv2 = sage.backward(ctx2, v, o2, lse2, do)
+    torch.cuda.current_stream().wait_stream(s)
+    dq, dk, dv = sage.backward(ctx, v, o, lse, do)
+    torch.cuda.synchronize()
+    assert torch.equal(o, o2) and torch.equal(lse, lse2) and torch.equal(dv, dv2) and torch.equal(dk, dk2)
+    assert rel_l2(f64(dq), f64(dq2)) < 1e-3  # dQ's fp32 reduction order varies run to run
+    keys = [key for key in sage._ws.bufs if key[1] == s.cuda_stream]
+    assert keys, "the side stream got its own workspace"
+
+
+@pytest.mark.slow
+def test_max_seqlen_sampled_oracle_head():
+    """N = 32768 (kMaxSeqLen, the top of the metric's 1K-32K) against the oracle on sampled blocks of one
+    head: query blocks {0, 100, 255} (O, L, dQ) and key blocks {200, 255} (dK, dV); the oracle runs the
+    same tiles as a full run for those rows (oracle.fwd / bwd q_blocks / k_blocks, pinned bitwise)."""
+    B, H, N, d = 1, 1, 32768, 128
+    q, k, v, do = make_inputs(B, H, N, d, "qknorm", seed=32)
+    gpu = _run(q, k, v, do, True, True, False)
+    qb, kb = [0, 100, 255], [200, 255]
+    need = sorted(set(qb) | set(range(200, 256)))
+    flat = lambda t: f64(t).reshape(1, N, d)
+    oracle.set_threads(8)
+    f = oracle.fwd(flat(q), flat(k), flat(v), causal=True, q_blocks=need)
+    b = oracle.bwd(flat(q), flat(k), flat(v), round_bf16(f["o"]), flat(do), f["lse"], causal=True,
+                   q_blocks=qb, k_blocks=kb)
+    rows = lambda bl: np.concatenate([np.arange(i * 128, (i + 1) * 128) for i in bl])
+    for name, ref, r in (("o", f["o"], rows(qb)), ("dq", b["dq"], rows(qb)), ("dk", b["dk"], rows(kb)),
+                         ("dv", b["dv"], rows(kb))):
+        got = flat(gpu[name])[0][r]
+        want = round_bf16(ref[0][r])
+        assert rel_l2(want, got) <= REL_TOL and cos_sim(want, got) >= COS_TOL, (name, rel_l2(want, got))
+    lse = f64(gpu["lse"]).reshape(N)[rows(qb)]
+    assert np.abs(lse - f["lse"][0][rows(qb)]).max() <= 1e-5
