@@ -310,7 +310,7 @@ def _parity_rows(c, lo, outs):
     oracle.build()
     T, N, d = c.seqlen // 128, c.seqlen, c.head_dim
     qb = sorted({0, T // 2, T - 1})
-    kb = [T - 1] if c.causal else [0]
+    kb = [T - 4, T - 1] if c.causal else [0]  # causal: key block T-4 sees 4 query blocks
     q, k, v, do = _np_heads([t[0, :1] for t in rank_inputs(c, lo, lo + 1)], 1, c)
     f, b, dt = oracle_sampled(c, q, k, v, do, qb, kb)
     g = {n: outs[n][0, 0].float().cpu().numpy().astype(np.float64) for n in ("o", "dq", "dk", "dv")}
