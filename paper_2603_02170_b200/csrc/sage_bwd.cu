@@ -81,7 +81,7 @@ struct BwdSmem {
   static constexpr int kScDO = kScQ + (FINE ? 0 : kMaxT * 4);
   static constexpr int kDq = FINE ? kDSq + kBlk * kBlk : (kScDO + kMaxT * 4 + 1023) / 1024 * 1024;
   static constexpr int kBar = FINE ? kScDO : kDq + 4 * kDqWarp;
-  static constexpr int kNumBars = 1 + 2 * kStages + 13;
+  static constexpr int kNumBars = 1 + 2 * kStages + 14;
   static constexpr int kTmemSlot = kBar + kNumBars * 8;
   static constexpr int kBytes = kTmemSlot + 16;
   static constexpr int kAlloc = kBytes + 1024;
@@ -99,7 +99,10 @@ struct BwdSmem {
 #define SAGE_K4_RC64 136  // 144 spilled (68 B STL per thread) for a within-noise gain: kept at 136
 #endif
 #ifndef SAGE_K4_RC128
-#define SAGE_K4_RC128 128
+#define SAGE_K4_RC128 120  // ptxas spills at 128 (20 B / 124 B per thread), none at 120
+#endif
+#ifndef SAGE_K4_DKQ128
+#define SAGE_K4_DKQ128 1  // d=128: dK shares the dQ region (1) or dP's (0, round 1)
 #endif
 #ifndef SAGE_TRACE
 #define SAGE_TRACE 0
@@ -202,6 +205,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* dq_drained = b0 + 10;  // drain -> MMA (4 warps): dQ tile read (dkq_drained: dK tile read)
   uint64_t* v_tmem = b0 + 11;      // compute -> MMA (8 warps): V_j copied into TMEM (d=64)
   uint64_t* s_free = b0 + 12;      // compute -> MMA (8 warps): S^T read into registers (d=64)
+  uint64_t* dk_full = b0 + 13;     // d=128: MMA -> drain, the dK tile (dkq_full then marks the dQ tile,
+                                   // issued after it: both have read dS^^T)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
   int* red = reinterpret_cast<int*>(smem + L::kRed);
   float* scl = reinterpret_cast<float*>(smem + L::kScl);
@@ -243,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(q_empty + s, kEmptyCount);
     }
     for (int b = 0; b < 4; ++b) mbar_init(b0 + b, 1);
+    mbar_init(dk_full, 1);
     for (int b = 4; b < 6; ++b) mbar_init(b0 + b, kComputeWarps);
     // d=128: the compute warps drain the dV tile (it aliases S, so draining it gates S_{i+1})
     mbar_init(dv_drained, kAlias ? kComputeWarps : kDrainWarps);
@@ -269,7 +275,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tS = tmem;
   const uint32_t tDP = tmem + 128;
   const uint32_t tDV = kAlias ? tmem : tmem + 256;
-  const uint32_t tDK = kAlias ? tmem + 128 : tmem + 256 + D;
+  // d=128: dK_i and then dQ_i take turns in the third region, so dP_{i+1} never waits for the dK drain
+  constexpr bool kDkQ = kAlias && SAGE_K4_DKQ128;
+  const uint32_t tDK = kAlias ? (kDkQ ? tmem + 256 : tmem + 128) : tmem + 256 + D;
   const uint32_t tDQ = kAlias ? tmem + 256 : tmem + 256 + 2 * D;
   const uint32_t tDVacc = tmem + 384;  // d=128 only
   // d=64: the A operands of dP^T (V_j, bf16) and dV (P^^T, int8) live in TMEM ("TS" MMAs), which
@@ -279,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tPa = tmem + 480;  // P^^T int8 [128 kv][128 q]: 32 columns
 
   if (warp < 4) {
-    reg_dealloc<kRegProducer>();
+    reg_set<kRegProducer, 65536 / kThreads>();
     if (warp == 0) {
       // ---------------------------------------------------------- TMA producer (one elected lane)
       if (elect_one()) {
@@ -404,6 +412,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       };
+      // d=128: dK_i and then (once drained) dQ_i in the same TMEM region
+      auto issue_dk = [&](int it) {
+        if (elect_one()) {
+          const uint32_t q_addr = st0 + soff(it) + L::kSQ;
+#pragma unroll
+          for (int kk = 0; kk < kBlk / 32; ++kk)
+            mma_i8(tDK, desc_kmajor(dst_addr, 128, kk * 32), desc_mnmajor(q_addr, D, kk * 32), kIdDV, kk > 0);
+          mma_commit(dk_full);
+          mma_commit(q_empty + it % kStages);  // Q^_i was the stage's last MMA operand
+          TR(3, it);
+        }
+        __syncwarp();
+      };
+      auto issue_dq = [&](int it) {
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < kBlk / 32; ++kk)
+            mma_i8(tDQ, desc_mnmajor(dsq_addr, 128, kk * 32), desc_mnmajor(k_addr, D, kk * 32), kIdDQ, kk > 0);
+          mma_commit(dkq_full);  // dQ_i ready; with dK_i before it, dS^^T has been read
+          TR(4, it);
+        }
+        __syncwarp();
+      };
       mbar_wait(kv_full, 0);
       issue_s(0);
       if constexpr (kTS) mbar_wait(v_tmem, 0);
@@ -434,31 +465,50 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) TR(20, it);
           tc_fence_after();
           issue_dkdq(it);
-        } else {
-          // d=128: dV_i lands on S's columns, dK_i on dP's (both read by p_ready); S_{i+1} /
-          // dP_{i+1} wait until those tiles are drained.
+        } else if constexpr (!kDkQ) {
+          // d=128 (round 1): dV_i lands on S's columns, dK_i on dP's (both read by p_ready)
           mbar_wait(p_ready, ph);
           tc_fence_after();
           issue_dv(it);
-          // the compute warps finish a tile (ds_ready) before the drain finishes its dV tile, so
-          // dK_i/dQ_i go first, then S_{i+1} into the drained S columns, then dP_{i+1}
           mbar_wait(ds_ready, ph);
-          if (it > 0) mbar_wait(dq_drained, pph);  // dQ slot; the dK slot (dP's) was freed at p_ready
+          if (it > 0) mbar_wait(dq_drained, pph);
           tc_fence_after();
           issue_dkdq(it);
           if (more) {
             mbar_wait(dv_drained, ph);
             tc_fence_after();
             issue_s(it + 1);
-            mbar_wait(dkq_drained, ph);  // dK_i read out of dP's columns
+            mbar_wait(dkq_drained, ph);
             tc_fence_after();
             issue_dp(it + 1);
           }
+        } else {
+          // d=128: dV_i lands on S's columns (read by p_ready), so S_{i+1} waits until the compute
+          // warps have drained dV_i; dP_{i+1} goes out right behind dV_i (dP_i was read by p_ready).
+          // dK_i and then dQ_i take turns in the third region.
+          mbar_wait(p_ready, ph);
+          if (lane == 0) TR(17, it);
+          tc_fence_after();
+          issue_dv(it);
+          if (more) issue_dp(it + 1);
+          mbar_wait(ds_ready, ph);
+          if (it > 0) mbar_wait(dq_drained, pph);  // dQ_{i-1} drained out of the third region
+          if (lane == 0) TR(20, it);
+          tc_fence_after();
+          issue_dk(it);
+          if (more) {
+            mbar_wait(dv_drained, ph);
+            tc_fence_after();
+            issue_s(it + 1);
+          }
+          mbar_wait(dkq_drained, ph);  // dK_i drained
+          tc_fence_after();
+          issue_dq(it);
         }
       }
     }
   } else if (warp < 4 + kComputeWarps) {
-    reg_alloc<kRegCompute>();
+    reg_set<kRegCompute, 65536 / kThreads>();
     // ------------------------------------------------------------ compute warpgroups (256 threads)
     const int cw = warp - 4;                 // compute warp 0..7
     const int wg = cw / 4;
@@ -744,7 +794,7 @@ if (cm) {
       }
     }
   } else {
-    reg_alloc<kRegDrain>();
+    reg_set<kRegDrain, 65536 / kThreads>();
     // ------------------------------------------------------------ drain warpgroup (128 threads)
     const int r = (warp % 4) * 32 + lane;  // TMEM lane: key row (dV, dK) or query row (dQ)
     const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
@@ -793,7 +843,7 @@ if (cm) {
       }
 
       // dK_j += tile * s_dS * s_Q * tau (+ Q-smoothing bias branch)  (line 11)
-      mbar_wait(dkq_full, ph);
+      mbar_wait(kDkQ ? dk_full : dkq_full, ph);
       tc_fence_after();
       if (threadIdx.x == 384) TR(11, it);
       if (!(ablate & 1)) {
@@ -833,10 +883,14 @@ if (cm) {
         }
       }
       tc_fence_before();
-      warp_arrive(dkq_drained);  // dK tile read (d=128: dP's columns may take dP_{i+1})
+      warp_arrive(dkq_drained);  // dK tile read (d=128: the region may take dQ_i)
       if constexpr (L::kSplitDO && QSMOOTH) warp_arrive(q_empty + it % kStages);  // mu_Qi read
 
       // dQ_i += tile * s_dS * s_K * tau, fp32 reduction across key blocks (line 10)
+      if constexpr (kDkQ) {
+        mbar_wait(dkq_full, ph);  // d=128: the dQ tile, issued once dK_i was drained
+        tc_fence_after();
+      }
       if (threadIdx.x == 384) TR(12, it);
       {
         // scaled rows -> this warp's swizzled smem staging (2 buffers) -> TMA reduce-add per box

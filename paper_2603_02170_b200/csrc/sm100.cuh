@@ -442,6 +442,13 @@ template <uint32_t N>
 __device__ __forceinline__ void reg_dealloc() {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
 }
+// Set this warpgroup's register budget to N from the launch allocation kLaunch: .inc may only raise the
+// count and .dec only lower it (the wrong direction is an illegal instruction).
+template <uint32_t N, uint32_t kLaunch>
+__device__ __forceinline__ void reg_set() {
+  if constexpr (N > kLaunch) reg_alloc<N>();
+  else if constexpr (N < kLaunch) reg_dealloc<N>();
+}
 
 // One lane of a converged warp returns true (elect.sync): the single-thread issue of
 // tcgen05.mma / TMA inside warp-uniform control flow, so descriptors stay in uniform registers.
