@@ -209,11 +209,12 @@ SAGE_API sage_status sage_debug_trace(void* host_out, size_t bytes);
  *   dv_t     int32 [heads][T i][N kv][d]  the dV tile P^^T dO^_i before its scaling (line 7)
  *   dk_t     int32 [heads][T i][N kv][d]  the dK tile dS^^T Q^_i (line 11)
  *   dq_t     int32 [heads][T j][N q][d]   the dQ tile dS^ K^_j (line 10)
- * Any of the last four may be NULL (not dumped).  Tiles a causal run skips are not written.
+ *   dp_t     fp32  [heads][N kv][N q] dP^T = V_j dO_i^T as the BF16 MMA accumulated it (line 8)
+ * Any of the last five may be NULL (not dumped).  Tiles a causal run skips are not written.
  * heads = 0 turns the dump off.  The buffers must stay valid until the dumping sage_bwd has completed.
  * Not thread-safe (process-wide state). */
 SAGE_API sage_status sage_debug_dump(void* p_hat_t, float* s_p, void* ds_hat_t, float* s_ds, float* ds_t, int heads);
-SAGE_API sage_status sage_debug_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t);
+SAGE_API sage_status sage_debug_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t, float* dp_t);
 
 /* Test only (libsage_trace.so): make every later sage_fwd dump, for heads bh < `heads`, K2's own
  * intermediates (Alg. 1 lines 7-10) into caller-owned device memory:

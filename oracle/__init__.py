@@ -10,10 +10,13 @@ Parity status per function:
   * ``fwd`` / ``bwd`` with ``quant=True``        pinned (Table 1 trend/values, smoothing identities, grid fixed points)
   * ``fpa``                                     pinned (finite differences, closed forms, App. B bound)
   * ``qknorm.forward`` / ``qknorm.backward``    pinned (closed forms, unit RMS, finite differences)
+  * ``e4m3``, ``psi_block_e4m3``, ``fwd(pv_fp8)`` pinned (torch float8_e4m3fn, exact-P limit, FPA closeness)
+  * ``policy.attention`` (per-MatMul precision)  pinned (exact policy == fpa, per-site dependency pattern,
+                                                 SageBwd policy tracks the tiled quantised oracle)
 """
-from . import qknorm
-from .oracle import (CAUSAL, K_SMOOTH, Q_SMOOTH, QUANT_OFF, build, fpa, fwd, bwd,
-                     psi_block, psi_token_row, set_threads, max_threads)
+from . import policy, qknorm
+from .oracle import (CAUSAL, K_SMOOTH, Q_SMOOTH, QUANT_OFF, build, fpa, fwd, bwd, e4m3,
+                     psi_block, psi_block_e4m3, psi_token_row, set_threads, max_threads)
 
-__all__ = ["qknorm", "CAUSAL", "K_SMOOTH", "Q_SMOOTH", "QUANT_OFF", "build", "fpa", "fwd", "bwd",
-           "psi_block", "psi_token_row", "set_threads", "max_threads"]
+__all__ = ["policy", "qknorm", "CAUSAL", "K_SMOOTH", "Q_SMOOTH", "QUANT_OFF", "build", "fpa", "fwd", "bwd",
+           "psi_block", "psi_token_row", "set_threads", "max_threads", "e4m3", "psi_block_e4m3"]

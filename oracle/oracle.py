@@ -9,7 +9,7 @@ import subprocess
 
 import numpy as np
 
-CAUSAL, K_SMOOTH, Q_SMOOTH, QUANT_OFF, P_U8, P_COL, DS_FINE = 1, 2, 4, 8, 16, 32, 64
+CAUSAL, K_SMOOTH, Q_SMOOTH, QUANT_OFF, P_U8, P_COL, DS_FINE, PV_FP8 = 1, 2, 4, 8, 16, 32, 64, 128
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sage_oracle.c")
@@ -43,6 +43,9 @@ def _load():
         _lib.oracle_psi_token_row.argtypes = [P, I, D, I, P]
         _lib.oracle_psi_token_row.restype = D
         _lib.oracle_set_threads.argtypes = [I]
+        _lib.oracle_e4m3.argtypes = [D]
+        _lib.oracle_e4m3.restype = D
+        _lib.oracle_psi_block_e4m3.argtypes = [P, I, P, P]
         _lib.oracle_max_threads.restype = I
     return _lib
 
@@ -81,13 +84,28 @@ def psi_token_row(pt, rm_minus_m, pmax=127):
     return q, sp
 
 
+def e4m3(x):
+    """FP8 E4M3 round-to-nearest-even with saturation at 448 (the PTX cvt.rn.satfinite conversion)."""
+    return _load().oracle_e4m3(float(x))
+
+
+def psi_block_e4m3(x):
+    """psi into E4M3 over one block (the ORC_PV_FP8 V^): (e4m3 values, fp32 scale amax/448)."""
+    x = _f64(x)
+    q = np.zeros(x.shape, dtype=np.float64)
+    s = np.zeros(1, dtype=np.float64)
+    _load().oracle_psi_block_e4m3(_p(x), x.size, _p(q), _p(s))
+    return q, float(s[0])
+
+
 def _default_tau(d, tau):
     return 1.0 / np.sqrt(d) if tau is None else float(tau)
 
 
-def _flags(causal, k_smooth, q_smooth, quant, p_u8, p_col=False, ds_fine=False):
+def _flags(causal, k_smooth, q_smooth, quant, p_u8, p_col=False, ds_fine=False, pv_fp8=False):
     return (CAUSAL if causal else 0) | (K_SMOOTH if k_smooth else 0) | (Q_SMOOTH if q_smooth else 0) | \
-        (0 if quant else QUANT_OFF) | (P_U8 if p_u8 else 0) | (P_COL if p_col else 0) | (DS_FINE if ds_fine else 0)
+        (0 if quant else QUANT_OFF) | (P_U8 if p_u8 else 0) | (P_COL if p_col else 0) | (DS_FINE if ds_fine else 0) | \
+        (PV_FP8 if pv_fp8 else 0)
 
 
 def _sel(blocks, BH, T):
@@ -100,18 +118,20 @@ def _sel(blocks, BH, T):
 
 
 def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk=128, tau=None, p_u8=False,
-        q_blocks=None, tiles=False):
+        q_blocks=None, tiles=False, pv_fp8=False):
     """Alg. 1 per head.  Returns dict with o, lse and the Tier-A intermediates.
     q_blocks: compute O and L only for these query blocks (other rows stay zero), with the same
     arithmetic as the full run (sampled checks at sizes the full oracle cannot finish).
     tiles=True also returns the per-token P^ of every processed tile (p8, [BH, N q, N kv] uint8; tile (i, j)
     at rows i*blk.., columns j*blk..; masked or skipped entries 0) and its row scale s_P (sp, [BH, N q, T]
-    float64, Alg. 1 line 9)."""
+    float64, Alg. 1 line 9).
+    pv_fp8=True: P^ and V^ in FP8 E4M3 (ORC_PV_FP8); v8 is then left zero and the
+    dumped p8 is zero (the E4M3 P^ is not an integer); sv holds the E4M3 block scales amax/448."""
     q, k, v = _f64(q), _f64(k), _f64(v)
     BH, N, d = q.shape
     T = N // blk
     qsel = _sel(q_blocks, BH, T)
-    flags = _flags(causal, k_smooth, q_smooth, quant, p_u8)
+    flags = _flags(causal, k_smooth, q_smooth, quant, p_u8, pv_fp8=pv_fp8)
     out = dict(o=np.zeros((BH, N, d)), lse=np.zeros((BH, N)),
                mu_k=np.zeros((BH, d), np.float32), mu_q=np.zeros((BH, T, d), np.float32),
                bias=np.zeros((BH, T, N)),

@@ -42,6 +42,9 @@
                              of SURVEY.md 8(f) NEXT-2): dV_j += (P^^T dO^_i) with one scale per key */
 #define ORC_DS_FINE  64   /* backward psi(dS) per query row for dQ and per key column for dK, two int8
                              copies of the tile (the dS half of SURVEY.md 8(f) NEXT-2) */
+#define ORC_PV_FP8  128   /* forward P^ V^ in FP8 E4M3: per-token P^ = e4m3(P~ / s_P)
+                             with s_P = e^{rowmax - m}/448, V^ = e4m3(fl32(V * fl32(448/amax))) per block with
+                             s_V = fl32(amax/448); the products are summed exactly.  The backward is unchanged. */
 
 void oracle_set_threads(int n) {
 #ifdef _OPENMP
@@ -98,6 +101,36 @@ static void psi_block(const double *x, int n, int fp32_product, int quant_off, d
   }
   *scale_out = (double)scale;
 }
+
+/* FP8 E4M3 (1 sign, 4 exponent bits with bias 7, 3 mantissa bits; largest finite 448, smallest subnormal
+ * 2^-9): round to nearest, ties to even, saturating at +-448 (PTX cvt.rn.satfinite.e4m3x2.f32). */
+static double e4m3_rne(double x) {
+  double a = fabs(x);
+  if (a == 0.0) return 0.0;
+  if (a >= 448.0) return x < 0 ? -448.0 : 448.0;
+  int E;
+  frexp(a, &E);                       /* a = f 2^E, f in [0.5, 1): binade 2^(E-1) */
+  int e = E - 1;
+  if (e < -6) e = -6;                 /* subnormals share the quantum 2^-9 */
+  double quantum = ldexp(1.0, e - 3); /* 3 mantissa bits */
+  double r = nearbyint(a / quantum) * quantum;
+  if (r > 448.0) r = 448.0;
+  return x < 0 ? -r : r;
+}
+double oracle_e4m3(double x) { return e4m3_rne(x); }
+
+/* psi into E4M3 over one block (ORC_PV_FP8): scale = fl32(amax/448), q = e4m3(fl32(x * fl32(448/amax))). */
+static void psi_block_e4m3(const double *x, int n, double *xq_out, double *scale_out) {
+  double amax = 0.0;
+  for (int e = 0; e < n; ++e) if (fabs(x[e]) > amax) amax = fabs(x[e]);
+  float famax = (float)amax;
+  float scale = famax / 448.0f;
+  float inv = famax > 0.0f ? 448.0f / famax : 0.0f;
+  for (int e = 0; e < n; ++e) xq_out[e] = e4m3_rne((double)((float)x[e] * inv));
+  *scale_out = (double)scale;
+}
+
+void oracle_psi_block_e4m3(const double *x, int n, double *q, double *scale) { psi_block_e4m3(x, n, q, scale); }
 
 /* Exported for the worked-example pins. */
 void oracle_psi_block(const double *x, int n, int fp32_product, int8_t *q, double *scale) {
@@ -253,15 +286,20 @@ static void fwd_head(const double *q, const double *k, const double *v, int N, i
   double *vx = malloc(nd * sizeof(double));
   int8_t *v8 = calloc(nd, 1);
   double *sv = malloc(T * sizeof(double));
+  int pv8 = (flags & ORC_PV_FP8) && !qo;
   for (int t = 0; t < T; ++t) {
     size_t off = (size_t)t * blk * d;
-    psi_block(v + off, blk * d, 1, qo, 127.0, v8 + off, &sv[t], vx + off);
+    if (pv8)
+      psi_block_e4m3(v + off, blk * d, vx + off, &sv[t]);   /* v8 (int8) stays zero in this mode */
+    else
+      psi_block(v + off, blk * d, 1, qo, 127.0, v8 + off, &sv[t], vx + off);
   }
   double *S = malloc((size_t)blk * blk * sizeof(double));
   double *Pt = malloc((size_t)blk * blk * sizeof(double));
   int16_t *Ph = malloc((size_t)blk * blk * sizeof(int16_t));
   double pmax = (flags & ORC_P_U8) ? 255.0 : 127.0;
   double *acc = malloc((size_t)blk * d * sizeof(double));
+  double *Pq = malloc(blk * sizeof(double));
   double *m = malloc(blk * sizeof(double)), *l = malloc(blk * sizeof(double));
 
   for (int i = 0; i < T; ++i) {
@@ -288,6 +326,17 @@ static void fwd_head(const double *q, const double *k, const double *v, int N, i
             double pv = 0.0;
             for (int n = 0; n < blk; ++n) pv += Pr[n] * vx[(size_t)(j * blk + n) * d + c];
             ar[c] = alpha * ar[c] + pv;
+          }
+        } else if (pv8) {
+          /* line 9 in FP8: s_P = e^{rowmax - m}/448, P^ = e4m3(P~ / s_P); line 10: exact sum of E4M3 products */
+          double sp = exp(rm - mnew) / 448.0;
+          for (int n = 0; n < blk; ++n) Pq[n] = e4m3_rne(Pr[n] / sp);
+          if (p8o) for (int n = 0; n < blk; ++n) p8o[(size_t)(i * blk + r) * N + (size_t)j * blk + n] = 0;
+          if (spo) spo[(size_t)(i * blk + r) * T + j] = sp;
+          for (int c = 0; c < d; ++c) {
+            double pv = 0.0;
+            for (int n = 0; n < blk; ++n) pv += Pq[n] * vx[(size_t)(j * blk + n) * d + c];
+            ar[c] = alpha * ar[c] + pv * sp * sv[j];
           }
         } else {
           int16_t *Phr = Ph + (size_t)r * blk;
@@ -322,7 +371,7 @@ static void fwd_head(const double *q, const double *k, const double *v, int N, i
     if (sko) sko[t] = (float)h.sk[t];
     if (svo) svo[t] = (float)sv[t];
   }
-  free(vx); free(v8); free(sv); free(S); free(Pt); free(Ph); free(acc); free(m); free(l);
+  free(vx); free(v8); free(sv); free(S); free(Pt); free(Ph); free(acc); free(m); free(l); free(Pq);
   prep_free(&h);
 }
 

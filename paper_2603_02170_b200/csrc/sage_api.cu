@@ -652,12 +652,12 @@ sage_status sage_debug_dump(void* p_hat_t, float* s_p, void* ds_hat_t, float* s_
 #endif
 }
 
-sage_status sage_debug_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t) {
+sage_status sage_debug_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t, float* dp_t) {
 #if SAGE_TRACE
-  cudaError_t e = set_bwd_dump_acc(s_t, dv_t, dk_t, dq_t);
+  cudaError_t e = set_bwd_dump_acc(s_t, dv_t, dk_t, dq_t, dp_t);
   return e == cudaSuccess ? SAGE_OK : cuda_fail(e);
 #else
-  (void)s_t; (void)dv_t; (void)dk_t; (void)dq_t;
+  (void)s_t; (void)dv_t; (void)dk_t; (void)dq_t; (void)dp_t;
   return SAGE_ERR_UNSUPPORTED;
 #endif
 }

@@ -126,6 +126,7 @@ __device__ BwdDump g_dump;
 // [head][T i][N kv][D], the dQ tiles [head][T j][N q][D], each before any scaling
 struct BwdDumpAcc {
   int32_t *s_t, *dv, *dk, *dq;
+  float* dp;  // dP^T = V_j dO_i^T as the kind::f16 MMA left it (fp32), [head][N kv][N q]
 };
 __device__ BwdDumpAcc g_dacc;
 __device__ __forceinline__ void dump_words(int32_t* dst, const uint32_t* v, int n) {
@@ -635,6 +636,9 @@ if (cm) {
 #pragma unroll
         for (int u = 0; u < 32; ++u) t[cc * 32 + u] = ex2(t[cc * 32 + u]);
         tmem_wait_ld();
+        if (DUMPING && g_dacc.dp)
+          dump_words(reinterpret_cast<int32_t*>(g_dacc.dp) + ((size_t)bh * N + j * kBlk + r) * N + i * kBlk + qc0 + cc * 32,
+                     v, 32);
 #pragma unroll
         for (int c16 = 0; c16 < 2; ++c16) {
           uint32_t w[4];
@@ -1023,8 +1027,8 @@ cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
 
 cudaError_t set_bwd_dump(const BwdDump& d) { return cudaMemcpyToSymbol(g_dump, &d, sizeof(d)); }
 
-cudaError_t set_bwd_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t) {
-  const BwdDumpAcc a{s_t, dv_t, dk_t, dq_t};
+cudaError_t set_bwd_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t, float* dp_t) {
+  const BwdDumpAcc a{s_t, dv_t, dk_t, dq_t, dp_t};
   return cudaMemcpyToSymbol(g_dacc, &a, sizeof(a));
 }
 

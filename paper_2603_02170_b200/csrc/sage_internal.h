@@ -124,7 +124,7 @@ struct BwdDump {
 cudaError_t set_bwd_dump(const BwdDump& d);
 // the int32 accumulators (sage_debug_dump_acc): S^T [head][N kv][N q], dV / dK tiles [head][T i][N kv][d],
 // dQ tiles [head][T j][N q][d]; null = not dumped
-cudaError_t set_bwd_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t);
+cudaError_t set_bwd_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t, float* dp_t);
 
 // UMMA tile test (sage_debug_umma)
 cudaError_t launch_debug_umma(int mode, int K, int N, const CUtensorMap* tma, const CUtensorMap* tmb,

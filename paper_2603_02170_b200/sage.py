@@ -74,7 +74,7 @@ def lib():
         L.sage_fwd_qknorm.argtypes = [pp, P, P, P, P, P, ctypes.c_float, P, P, pc, P, S, P]
         L.sage_bwd_qknorm.argtypes = [pp, P, P, P, P, P, P, P, P, pc, P, P, P, P, P, P, S, P]
         L.sage_debug_fwd_dump.argtypes = [P, P, P, P, ctypes.c_int]
-        L.sage_debug_dump_acc.argtypes = [P, P, P, P]
+        L.sage_debug_dump_acc.argtypes = [P, P, P, P, P]
         L.sage_ctx_get_view.argtypes = [pp, P, ctypes.POINTER(SageCtxView)]
         L.sage_ws_get_view.argtypes = [pp, ctypes.c_int, P, ctypes.POINTER(SageWsView)]
         L.sage_debug_umma.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P]
@@ -403,10 +403,11 @@ def debug_umma(mode, a, b, K=None, N=None):
 def debug_dump(heads, N, device, d=None, acc=False):
     """Arm sage_debug_dump (libsage_trace.so only) for heads [0, heads) of sequence length N:
     returns the device buffers every later sage_bwd fills (include/sage.h); heads=0 disarms.
-    acc=True (head dim d) also arms sage_debug_dump_acc: the int32 S^T, dV, dK, dQ tile accumulators."""
+    acc=True (head dim d) also arms sage_debug_dump_acc: the int32 S^T, dV, dK, dQ tile accumulators and the
+    fp32 dP^T."""
     if heads == 0:
         _check(lib().sage_debug_dump(None, None, None, None, None, 0), "sage_debug_dump")
-        _check(lib().sage_debug_dump_acc(None, None, None, None), "sage_debug_dump_acc")
+        _check(lib().sage_debug_dump_acc(None, None, None, None, None), "sage_debug_dump_acc")
         return None
     T = N // 128
     bufs = dict(p_hat_t=torch.zeros((heads, N, N), dtype=torch.int8, device=device),
@@ -420,11 +421,12 @@ def debug_dump(heads, N, device, d=None, acc=False):
         bufs.update(s_t=torch.zeros((heads, N, N), dtype=torch.int32, device=device),
                     dv_t=torch.zeros((heads, T, N, d), dtype=torch.int32, device=device),
                     dk_t=torch.zeros((heads, T, N, d), dtype=torch.int32, device=device),
-                    dq_t=torch.zeros((heads, T, N, d), dtype=torch.int32, device=device))
+                    dq_t=torch.zeros((heads, T, N, d), dtype=torch.int32, device=device),
+                    dp_t=torch.zeros((heads, N, N), dtype=torch.float32, device=device))
         _check(lib().sage_debug_dump_acc(_ptr(bufs["s_t"]), _ptr(bufs["dv_t"]), _ptr(bufs["dk_t"]),
-                                         _ptr(bufs["dq_t"])), "sage_debug_dump_acc")
+                                         _ptr(bufs["dq_t"]), _ptr(bufs["dp_t"])), "sage_debug_dump_acc")
     else:
-        _check(lib().sage_debug_dump_acc(None, None, None, None), "sage_debug_dump_acc")
+        _check(lib().sage_debug_dump_acc(None, None, None, None, None), "sage_debug_dump_acc")
     return bufs
 
 

@@ -47,7 +47,7 @@ def _gpu_with_dump(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, p_col=Fa
     B, H, N, d = q.shape
     dev = torch.device("cuda")
     qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
-    bufs = sage.debug_dump(B * H, N, dev)
+    bufs = sage.debug_dump(B * H, N, dev, d=d, acc=True)
     o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=k_smooth, q_smooth=q_smooth, p_u8=p_u8,
                                p_colscale=p_col, fine_bwd=fine)
     dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
@@ -56,7 +56,8 @@ def _gpu_with_dump(q, k, v, do, causal, k_smooth, q_smooth, p_u8=False, p_col=Fa
     # back to the oracle's [head][N q][N kv] layout
     tiles = dict(p8=bufs["p_hat_t"].transpose(1, 2).cpu().numpy().view(np.uint8), sp=bufs["s_p"].cpu().numpy(),
                  ds8=bufs["ds_hat_t"].transpose(1, 2).cpu().numpy(), sds=bufs["s_ds"].cpu().numpy(),
-                 ds=bufs["ds_t"].transpose(1, 2).cpu().numpy().astype(np.float64))
+                 ds=bufs["ds_t"].transpose(1, 2).cpu().numpy().astype(np.float64),
+                 dp=bufs["dp_t"].transpose(1, 2).cpu().numpy().astype(np.float64))
     wsb = sage._ws.get(ctx.params, True, dev)
     wb = sage.ws_view(ctx.params, True, wsb)
     off = wb.delta - wsb.data_ptr()
@@ -142,6 +143,15 @@ def _fidelity_row(g, b, f, ref, N, causal):
         row[name] = dict(gpu_rel_l2=rel_l2(ref[fpa_key], g[name]), gpu_cos=cos_sim(ref[fpa_key], g[name]),
                          oracle_rel_l2=rel_l2(ref[fpa_key], qo))
     row["delta"] = dict(gpu_rel_l2=rel_l2(ref["delta"], g["delta"]), oracle_rel_l2=rel_l2(ref["delta"], b["delta"]))
+    # dP = dO V^T (Alg. 2 line 8), the one unquantised MatMul: the GPU's BF16 MMA over the processed tiles
+    # against FPA's (the oracle computes it exactly, reading A9); the paper reports 0.0000
+    T = N // 128
+    mask = np.zeros((N, N), bool)
+    for i in range(T):
+        for j in range(T):
+            if not causal or j <= i:
+                mask[i * 128:(i + 1) * 128, j * 128:(j + 1) * 128] = True
+    row["dP"] = dict(gpu_rel_l2=rel_l2(ref["dP"][:, mask], g["dp"][:, mask]), oracle_rel_l2=0.0)
     row["P"] = dict(gpu_rel_l2=rel_l2(ref["P"], deq(g["p8"], g["sp"])),
                     oracle_rel_l2=rel_l2(ref["P"], deq(b["p8"], b["sp"])))
     row["dS_pre_psi"] = dict(gpu_rel_l2=rel_l2(ref["dS"], g["ds"]), oracle_rel_l2=rel_l2(ref["dS"], b["ds"]))
@@ -168,6 +178,7 @@ def _assert_gpu_tracks_oracle(row, what):
     for name in ("o", "dq", "dk", "dv", "P", "dS"):
         gr, orr = row[name]["gpu_rel_l2"], row[name]["oracle_rel_l2"]
         assert abs(gr - orr) <= 0.05 * orr + 1e-4, (what, name, gr, orr)
+    assert row["dP"]["gpu_rel_l2"] <= 1e-5, (what, row["dP"])  # fp32 accumulation of exact BF16 products
 
 
 TABLE1 = {1.0: (0.0160, 0.0184, 0.0220, 0.0159), 3.0: (0.0389, 0.0758, 0.0777, 0.0387),
@@ -211,6 +222,12 @@ def test_fidelity_qknorm_ablation(dump_lib):
         row = _fidelity_row(g, b, f, _fpa(q, k, v, do, True), N, True)
         _assert_gpu_tracks_oracle(row, recipe)
         rows[recipe] = row
+    # the per-MatMul precision policy (oracle.policy): each site quantised alone on head 0, the
+    # paper's Table 2 analysis -- which MatMul's quantisation the component errors come from
+    for recipe in ("qknorm", "noqknorm"):
+        q, k, v, do = make_inputs(B, H, N, d, recipe, seed=5000)
+        h0 = lambda t: f64(t).reshape(B * H, N, d)[0]
+        rows[recipe]["site_ablation_head0"] = oracle.policy.site_ablation(h0(q), h0(k), h0(v), h0(do), causal=True)
     _write_report("qknorm_ablation", dict(setting=f"B={B} H={H} N={N} d={d} causal K-smooth", rows=rows))
     for name in ("dq", "dk", "dS"):
         assert rows["qknorm"][name]["gpu_rel_l2"] < rows["noqknorm"][name]["gpu_rel_l2"], (name, rows)

@@ -9,7 +9,8 @@ write, with the production kernel code, the int32 tile accumulators and int8 ope
 - Tier B (bit-exact given the dumped int8 operands): K2's P^ V^_j (Alg. 1 line 10), K4's P^^T dO^_i
   (dV, line 7), dS^^T Q^_i (dK, line 11) and dS^ K^_j (dQ, line 10) accumulators equal the dumped operands
   re-multiplied in int64 -- this checks the fused kernels' descriptors, swizzles, stage offsets and TMEM
-  column placements, not a stand-alone test kernel's.
+  column placements, not a stand-alone test kernel's.  K4's BF16 dP^T (line 8) equals dO_i V_j^T within
+  fp32 accumulation (1e-6 of the sum of |products|).
 - Tier C (statistical, exp-bit dependent): K2's per-token P^ and s_P (Alg. 1 line 9) against the
   oracle's: >= 99.99% of P^ identical, none more than 1 LSB apart, s_P within 64 fp32 ulp.
 """
@@ -86,6 +87,7 @@ def test_fused_tiles(trace_lib, B, H, N, d, causal, ks, qs, recipe, u8):
     np.testing.assert_array_equal(v8, f["v8"])
 
     pdt = np.uint8 if u8 else np.int8
+    dof, vf = (f64(t).reshape(BH, N, d) for t in (do, v))
     blk = lambda t: slice(t * 128, (t + 1) * 128)
     tiles = [(i, j) for i in range(T) for j in range(T) if not causal or j <= i]
     n_p = n_same = 0
@@ -107,6 +109,10 @@ def test_fused_tiles(trace_lib, B, H, N, d, causal, ks, qs, recipe, u8):
             np.testing.assert_array_equal(bb["dv_t"][h, i, J], p_t[J, I] @ do8[h][I], err_msg=f"K4 dV h{h} ({i},{j})")
             np.testing.assert_array_equal(bb["dk_t"][h, i, J], ds_t[J, I] @ q8[h][I], err_msg=f"K4 dK h{h} ({i},{j})")
             np.testing.assert_array_equal(bb["dq_t"][h, j, I], ds_t[J, I].T @ k8[h][J], err_msg=f"K4 dQ h{h} ({i},{j})")
+            # the BF16 dP MMA (line 8): exact products of the I/O values, fp32 accumulation of d terms
+            dp_ref = dof[h][I] @ vf[h][J].T
+            bound = 1e-6 * (np.abs(dof[h][I]) @ np.abs(vf[h][J]).T) + 1e-30
+            assert (np.abs(bb["dp_t"][h][J, I].T - dp_ref) <= bound).all(), f"K4 dP h{h} ({i},{j})"
             # Tier C: the forward's per-token P^ and s_P against the oracle's
             ref_p = f["p8"][h][I, J].astype(np.int64)
             diff = np.abs(p_fwd - ref_p)
