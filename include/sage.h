@@ -90,10 +90,16 @@ enum {
   SAGE_FP16 = 1u << 8,      /* fp16 instead of bf16 for Q, K, V, O, dO, dQ, dK, dV (and X_q, X_k, dX_q,
                               dX_k with QK-norm, whose module output is then fp16): dP = dO V^T runs
                               as an fp16 kind::f16 MMA, the paper's "FP16" option */
-  SAGE_FP32_OUT = 1u << 9   /* O, dQ, dK, dV written as fp32 (no rounding to the I/O type), e.g. to
+  SAGE_FP32_OUT = 1u << 9,  /* O, dQ, dK, dV written as fp32 (no rounding to the I/O type), e.g. to
                               compare against an unrounded reference (reading A18).  delta is then
                               formed from the fp32 O the forward stored (A15).  Not combinable with
                               SAGE_QK_NORM (SAGE_ERR_INVALID_VALUE). */
+  SAGE_PV_FP8 = 1u << 10    /* variant: the forward's P^ V^ (Alg. 1 lines 9-10)
+                              in FP8 E4M3 -- per-token P^ = e4m3(P~ / s_P) with s_P = e^{rowmax - m}/448,
+                              V^ = e4m3(V / s_V) per block with s_V = amax/448 -- as a kind::f8f6f4 MMA
+                              accumulating in fp32 (no int32 -> fp32 conversions in the O update).  E4M3's
+                              3-bit mantissa makes O 2-4x less accurate than the INT8 path.  The backward is
+                              unchanged.  Not combinable with SAGE_P_U8. */
 };
 
 typedef struct {

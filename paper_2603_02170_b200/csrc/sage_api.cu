@@ -66,7 +66,7 @@ size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Dims {
   size_t BH, N, d, T;
-  bool causal, ks, qs, pu8, qkn, det, pcol, fine, fp16, f32out;
+  bool causal, ks, qs, pu8, qkn, det, pcol, fine, fp16, f32out, pvfp8;
   float tau;
 };
 
@@ -76,7 +76,7 @@ bool dims_of(const sage_params* p, Dims* o) {
   if (p->head_dim != 64 && p->head_dim != 128) return false;
   if (p->seqlen % kBlk || p->seqlen > kMaxSeqLen) return false;
   if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH | SAGE_P_U8 | SAGE_QK_NORM | SAGE_DETERMINISTIC |
-                             SAGE_P_COLSCALE | SAGE_FINE_BWD | SAGE_FP16 | SAGE_FP32_OUT))
+                             SAGE_P_COLSCALE | SAGE_FINE_BWD | SAGE_FP16 | SAGE_FP32_OUT | SAGE_PV_FP8))
     return false;
   if (!(p->softmax_scale >= 0.f) || std::isinf(p->softmax_scale)) return false;
   const size_t BH = (size_t)p->batch * p->heads;
@@ -95,6 +95,8 @@ bool dims_of(const sage_params* p, Dims* o) {
   o->fine = p->flags & SAGE_FINE_BWD;
   o->fp16 = p->flags & SAGE_FP16;
   o->f32out = p->flags & SAGE_FP32_OUT;
+  o->pvfp8 = p->flags & SAGE_PV_FP8;
+  if (o->pvfp8 && o->pu8) return false;  // one forward P^ variant at a time
   if (o->det && (o->pcol || o->fine)) return false;  // one backward variant at a time
   if (o->f32out && o->qkn) return false;              // the QK-norm outputs dX are I/O-typed
   o->tau = p->softmax_scale > 0.f ? p->softmax_scale : 1.f / std::sqrt((float)p->head_dim);
@@ -462,7 +464,8 @@ sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v,
   QuantJobs qj{};
   qj.j[0] = QuantJob{qb, muq, D.qs ? 2 : 0, q8, sq, rq, gq, eps};
   qj.j[1] = QuantJob{kb, muk, D.ks ? 1 : 0, k8, sk, rk, gk, eps};
-  qj.j[2] = QuantJob{vb, nullptr, 0, v8, sv, nullptr, nullptr, 0.f};
+  qj.j[0].fp8 = qj.j[1].fp8 = 0;
+  qj.j[2] = QuantJob{vb, nullptr, 0, v8, sv, nullptr, nullptr, 0.f, D.pvfp8 ? 1 : 0};
   if ((e = launch_quantize(qj, 3, BH, N, d, s, h)) != cudaSuccess) return cuda_fail(e);
   // mu_K is all-zero when K-smoothing is off (ctx is caller memory: make it so)
   if (!D.ks && (e = launch_fill(muk, D.BH * D.d, 0.f, s)) != cudaSuccess) return cuda_fail(e);
@@ -475,6 +478,7 @@ sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v,
   a.o = o;
   a.fp16 = D.fp16;
   a.f32out = D.f32out;
+  a.pvfp8 = D.pvfp8;
   a.lse = lse;
   a.BH = BH;
   a.N = N;

@@ -30,6 +30,7 @@ constexpr int kThreads = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLog2_127 = 6.988684686772166f;
 constexpr float kLog2_255 = 7.994353436858858f;
+constexpr float kLog2_448 = 8.807354922057604f;
 // Groups of 4 (of the 8 per 32-column chunk) whose exponentials run on the FMA pipe (ex2_poly2), at
 // d=128 (measured: 1 group = 12.5% of the exponentials, C4 K2 4.52 -> 4.40 ms; 2 neutral, 3 slower;
 // none at d=64, where it does not help)
@@ -93,7 +94,9 @@ __device__ __forceinline__ void fwd_item(int k, int T, int BH, bool causal, int&
   bh = g * kHeadGroup + r % hn;
 }
 
-template <int D, bool CAUSAL, bool QSMOOTH>
+// FP8 (SAGE_PV_FP8): P^ and V^ in E4M3 and P^V^ as a kind::f8f6f4 MMA (fp32 accumulator) -- a separate
+// instantiation, the INT8 path of Alg. 1 untouched
+template <int D, bool CAUSAL, bool QSMOOTH, bool FP8>
 __global__ void __launch_bounds__(kThreads, 2)
     sage_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ q_scale,
@@ -197,7 +200,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       // ---------------------------------------------------------- MMA issuer
       constexpr uint32_t kIdS = idesc_i8(128, 128, false, false);
       // P^ is s8 in 0..127, or u8 in 0..255 with SAGE_P_U8 (u8 x s8 MMA)
-      const uint32_t kIdPV = pu8 ? idesc_i8(128, D, false, true, true) : idesc_i8(128, D, false, true);
+      const uint32_t kIdPV = FP8 ? idesc_e4m3(128, D, false, true)
+                                 : pu8 ? idesc_i8(128, D, false, true, true) : idesc_i8(128, D, false, true);
       const uint32_t q_addr = smem_u32(smem + L::kQ);
       const uint32_t k0 = smem_u32(smem + L::kK), v0 = smem_u32(smem + L::kV);
       const uint32_t p_addr = smem_u32(smem + L::kP);
@@ -224,10 +228,17 @@ __global__ void __launch_bounds__(kThreads, 2)
           const uint32_t v_addr = v0 + st * L::kTile;
 #pragma unroll
           for (int kk = 0; kk < kBlk / 32; ++kk) {
-            if constexpr (kPTmem)
-              mma_i8_ts(tbuf(j), tbuf(j) + D + kk * 8, desc_mnmajor(v_addr, D, kk * 32), kIdPV, kk > 0);
-            else
-              mma_i8(tbuf(j), desc_kmajor(p_addr, 128, kk * 32), desc_mnmajor(v_addr, D, kk * 32), kIdPV, kk > 0);
+            if constexpr (kPTmem) {
+              if constexpr (FP8)
+                mma_f8_ts(tbuf(j), tbuf(j) + D + kk * 8, desc_mnmajor(v_addr, D, kk * 32), kIdPV, kk > 0);
+              else
+                mma_i8_ts(tbuf(j), tbuf(j) + D + kk * 8, desc_mnmajor(v_addr, D, kk * 32), kIdPV, kk > 0);
+            } else {
+              if constexpr (FP8)
+                mma_f8(tbuf(j), desc_kmajor(p_addr, 128, kk * 32), desc_mnmajor(v_addr, D, kk * 32), kIdPV, kk > 0);
+              else
+                mma_i8(tbuf(j), desc_kmajor(p_addr, 128, kk * 32), desc_mnmajor(v_addr, D, kk * 32), kIdPV, kk > 0);
+            }
           }
           mma_commit(v_empty + st);
           mma_commit(o_full);
@@ -283,8 +294,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     const float tau2 = tau * kLog2e;
     // P^ levels: 127, or 255 for the unsigned variant (SAGE_P_U8)
-    const float log2_pmax = pu8 ? kLog2_255 : kLog2_127;
-    const float inv_pmax = pu8 ? 1.f / 255.f : 1.f / 127.f;
+    const float log2_pmax = FP8 ? kLog2_448 : pu8 ? kLog2_255 : kLog2_127;
+    const float inv_pmax = FP8 ? 1.f / 448.f : pu8 ? 1.f / 255.f : 1.f / 127.f;
     uint8_t* prow = smem + L::kP;
     int gt = 0;  // global tile count of this CTA
     for (int k = blockIdx.x; k < W; k += gridDim.x) {
@@ -318,7 +329,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int e = 0; e < 32; e += 2) {
           float2 acc = make_float2(oacc[c0 + e], oacc[c0 + e + 1]);
           if (rescale) acc = fmul2(acc, make_float2(alpha, alpha));
-          acc = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f, acc);
+          const float2 pv = FP8 ? make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1]))  // fp32 D
+                                : make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1]));
+          acc = ffma2(pv, f, acc);
           oacc[c0 + e] = acc.x;
           oacc[c0 + e + 1] = acc.y;
         }
@@ -446,9 +459,13 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (c0 + e + 3 > r) b.y = 0.f;
           }
           rs2 = fadd2(rs2, fadd2(a, b));
-          const float2 qa = fadd2(a, make_float2(kMagic, kMagic));
-          const float2 qb = fadd2(b, make_float2(kMagic, kMagic));
-          pk[e4] = pack4_magic(qa.x, qa.y, qb.x, qb.y);
+          if constexpr (FP8) {
+            pk[e4] = e4m3x2(a.x, a.y) | (e4m3x2(b.x, b.y) << 16);
+          } else {
+            const float2 qa = fadd2(a, make_float2(kMagic, kMagic));
+            const float2 qb = fadd2(b, make_float2(kMagic, kMagic));
+            pk[e4] = pack4_magic(qa.x, qa.y, qb.x, qb.y);
+          }
         }
         if (FDUMPING && g_fdump.p) {
           uint8_t* dst = g_fdump.p + ((size_t)bh * N + (size_t)i * kBlk + r) * N + (size_t)j * kBlk + c0;
@@ -525,9 +542,9 @@ int sm_count() {
   return cache[dev];
 }
 
-template <int D, bool C, bool QS>
+template <int D, bool C, bool QS, bool F8>
 cudaError_t launch_t(const FwdArgs& a, cudaStream_t s) {
-  auto kern = sage_fwd_kernel<D, C, QS>;
+  auto kern = sage_fwd_kernel<D, C, QS, F8>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem<D>::kAlloc);
   if (e != cudaSuccess) return e;
   const int T = a.N / kBlk;
@@ -549,13 +566,15 @@ cudaError_t read_fwd_trace(void* host, size_t bytes) {
   return cudaMemcpyFromSymbol(host, g_trace_fwd, bytes);
 }
 
+template <int D, bool F8>
+cudaError_t launch_d(const FwdArgs& a, cudaStream_t s) {
+  if (a.causal) return a.qsmooth ? launch_t<D, true, true, F8>(a, s) : launch_t<D, true, false, F8>(a, s);
+  return a.qsmooth ? launch_t<D, false, true, F8>(a, s) : launch_t<D, false, false, F8>(a, s);
+}
+
 cudaError_t launch_fwd(const FwdArgs& a, cudaStream_t s) {
-  if (a.d == 128) {
-    if (a.causal) return a.qsmooth ? launch_t<128, true, true>(a, s) : launch_t<128, true, false>(a, s);
-    return a.qsmooth ? launch_t<128, false, true>(a, s) : launch_t<128, false, false>(a, s);
-  }
-  if (a.causal) return a.qsmooth ? launch_t<64, true, true>(a, s) : launch_t<64, true, false>(a, s);
-  return a.qsmooth ? launch_t<64, false, true>(a, s) : launch_t<64, false, false>(a, s);
+  if (a.d == 128) return a.pvfp8 ? launch_d<128, true>(a, s) : launch_d<128, false>(a, s);
+  return a.pvfp8 ? launch_d<64, true>(a, s) : launch_d<64, false>(a, s);
 }
 
 }  // namespace sage

@@ -44,6 +44,7 @@ struct QuantJob {
   float* rstd;         // QK-norm (NormIn): rstd out [BH*N]
   const float* gamma;  // or null
   float eps;
+  int fp8;             // SAGE_PV_FP8 (V only): E4M3 values with scale amax/448 instead of INT8 with amax/127
 };
 struct QuantJobs {
   QuantJob j[3];
@@ -76,6 +77,7 @@ struct FwdArgs {
   bool pu8;    // SAGE_P_U8: P^ in 0..255 (u8 x s8 PV)
   bool fp16;   // SAGE_FP16: fp16 I/O
   bool f32out; // SAGE_FP32_OUT: O written as fp32
+  bool pvfp8;  // SAGE_PV_FP8: P^ and V^ in E4M3, P^V^ as a kind::f8f6f4 MMA with fp32 accumulation
   int ablate;  // profiling only (SAGE_ABLATE bit 8: timeline, bit 16: sage_debug_fwd_dump)
 };
 cudaError_t launch_fwd(const FwdArgs& a, cudaStream_t s);

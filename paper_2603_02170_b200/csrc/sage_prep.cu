@@ -255,8 +255,11 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T)
   amax = red[0];
 #pragma unroll
   for (int w = 1; w < 8; ++w) amax = fmaxf(amax, red[w]);
-  const float sc = __fdiv_rn(amax, 127.f);
-  const float inv = amax > 0.f ? __fdiv_rn(127.f, amax) : 0.f;
+  // INT8: scale = fl32(amax/127), q = RNE(fl32(x * fl32(127/amax))); E4M3 (SAGE_PV_FP8, V only):
+  // scale = fl32(amax/448), q = e4m3_rne(fl32(x * fl32(448/amax))), saturating
+  const float qmax = job.fp8 ? 448.f : 127.f;
+  const float sc = __fdiv_rn(amax, qmax);
+  const float inv = amax > 0.f ? __fdiv_rn(qmax, amax) : 0.f;
   if (threadIdx.x == 0) scale[blk] = sc;
   int8_t* qb = xq + blk * kBlk * D;
 #pragma unroll
@@ -267,8 +270,17 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T)
 #pragma unroll
     for (int e = 0; e < kVec; ++e) v[e] = __fsub_rn(v[e], m[e]);
     uint32_t w[2];
+    if (job.fp8) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) w[h] = quant4(v + 4 * h, inv);
+      for (int h = 0; h < 2; ++h) {
+        const float* x = v + 4 * h;
+        w[h] = e4m3x2(__fmul_rn(x[0], inv), __fmul_rn(x[1], inv)) |
+               (e4m3x2(__fmul_rn(x[2], inv), __fmul_rn(x[3], inv)) << 16);
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) w[h] = quant4(v + 4 * h, inv);
+    }
     *reinterpret_cast<uint2*>(qb + (size_t)r * D + g * kVec) = make_uint2(w[0], w[1]);
   }
 }

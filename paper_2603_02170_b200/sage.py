@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("SAGE_LIB") or os.path.join(_HERE, "libsage.so")
 
 SAGE_CAUSAL, SAGE_K_SMOOTH, SAGE_Q_SMOOTH, SAGE_P_U8, SAGE_QK_NORM, SAGE_DETERMINISTIC, SAGE_P_COLSCALE = \
     1, 2, 4, 8, 16, 32, 64
-SAGE_FINE_BWD, SAGE_FP16, SAGE_FP32_OUT = 128, 256, 512
+SAGE_FINE_BWD, SAGE_FP16, SAGE_FP32_OUT, SAGE_PV_FP8 = 128, 256, 512, 1024
 _STATUS = {0: "SAGE_OK", 1: "SAGE_ERR_INVALID_VALUE", 2: "SAGE_ERR_UNSUPPORTED", 3: "SAGE_ERR_MISALIGNED",
            4: "SAGE_ERR_WORKSPACE", 5: "SAGE_ERR_CUDA", 6: "SAGE_ERR_ARCH"}
 
@@ -105,11 +105,11 @@ def _check(status, what):
 
 def make_params(batch, heads, seqlen, head_dim, causal=False, k_smooth=True, q_smooth=False, softmax_scale=None,
                 p_u8=False, qk_norm=False, deterministic=False, p_colscale=False, fine_bwd=False, fp16=False,
-                fp32_out=False):
+                fp32_out=False, pv_fp8=False):
     flags = (SAGE_CAUSAL if causal else 0) | (SAGE_K_SMOOTH if k_smooth else 0) | (SAGE_Q_SMOOTH if q_smooth else 0) | \
         (SAGE_P_U8 if p_u8 else 0) | (SAGE_QK_NORM if qk_norm else 0) | (SAGE_DETERMINISTIC if deterministic else 0) | \
         (SAGE_P_COLSCALE if p_colscale else 0) | (SAGE_FINE_BWD if fine_bwd else 0) | (SAGE_FP16 if fp16 else 0) | \
-        (SAGE_FP32_OUT if fp32_out else 0)
+        (SAGE_FP32_OUT if fp32_out else 0) | (SAGE_PV_FP8 if pv_fp8 else 0)
     return SageParams(batch, heads, seqlen, head_dim, flags, 0.0 if softmax_scale is None else softmax_scale)
 
 
@@ -221,17 +221,19 @@ def _out_dtype(io_dtype, fp32_out):
 
 def forward(q, k, v, causal=False, k_smooth=True, q_smooth=False, softmax_scale=None, out=None, lse=None,
             ctx=None, workspace=None, stream=None, p_u8=False, deterministic=False, p_colscale=False,
-            fine_bwd=False, fp32_out=False):
+            fine_bwd=False, fp32_out=False, pv_fp8=False):
     """sage_fwd (Alg. 1): returns (o, lse, SageCtx).  q, k, v: CUDA bf16 (or fp16) [B, H, N, d].
     p_u8: the unsigned-P^ variant (SAGE_P_U8); deterministic: a bitwise reproducible backward
     (SAGE_DETERMINISTIC); p_colscale: per-key psi(P) in the backward (SAGE_P_COLSCALE); fine_bwd: per-key
     psi(P) and per-key / per-query psi(dS) (SAGE_FINE_BWD); fp32_out: O (and later dQ, dK, dV) in fp32
-    (SAGE_FP32_OUT).  The backward inherits them through the ctx."""
+    (SAGE_FP32_OUT); pv_fp8: the forward's P^V^ in FP8 E4M3 (SAGE_PV_FP8).  The backward inherits them
+    through the ctx."""
     _check_io(q, k, v)
     B, H, N, d = q.shape
     dev = q.device
     p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8, deterministic=deterministic,
-                    p_colscale=p_colscale, fine_bwd=fine_bwd, fp16=q.dtype == torch.float16, fp32_out=fp32_out)
+                    p_colscale=p_colscale, fine_bwd=fine_bwd, fp16=q.dtype == torch.float16, fp32_out=fp32_out,
+                    pv_fp8=pv_fp8)
     nctx = lib().sage_ctx_bytes(ctypes.byref(p))
     if nctx == 0:
         raise SageError(f"unsupported shape/flags {tuple(q.shape)} (N % 128 == 0, d in {{64, 128}})")
