@@ -1,7 +1,6 @@
-// sage_fwd.cu -- K2: SageBwd forward, Alg. 1, persistent: two CTAs resident per SM
-// (TMEM 256 columns, <= 113 KB smem, setmaxnreg) walk the (head, 128-query block i) work items, so one
-// CTA's softmax overlaps the other's MMAs and TMEM round trips and the next item's start overlaps the
-// current item's end.  Within a CTA
+// sage_fwd.cu -- K2: SageBwd forward, Alg. 1, one CTA per
+// (head, 128-query block i), two CTAs resident per SM (TMEM 256 columns, <= 113 KB smem,
+// setmaxnreg) so one CTA's softmax overlaps the other's MMAs and TMEM round trips.  Within a CTA
 // S is double-buffered in TMEM (PV_j reuses S_j's buffer once S_j is consumed), and the O update
 // for tile j-1 runs before tile j's exponential pass, so S_{j+1} is on the tensor cores while
 // tile j is being exponentiated.
@@ -70,29 +69,11 @@ struct FwdSmem {
   static constexpr int kP = kV + kStages * kTile;  // [128][128] int8 P^, K-major 128B-swizzled
   static constexpr int kBias = kP + kBlk * kBlk;   // 2 x 128 floats (Q-smoothing)
   static constexpr int kBar = kBias + 2 * kBlk * 4;
-  static constexpr int kNumBars = 1 + 4 * kStages + 6;
+  static constexpr int kNumBars = 1 + 4 * kStages + 5;
   static constexpr int kTmemSlot = kBar + kNumBars * 8;
   static constexpr int kBytes = kTmemSlot + 16;
   static constexpr int kAlloc = kBytes + 1024;  // slack for 1024-byte alignment
 };
-
-// Persistent schedule: gridDim.x CTAs (2 per SM) walk the W = BH * T work items (one (head, 128-query block)
-// each) with stride gridDim.x.  Causal items are ordered longest first (LPT) within groups of kHeadGroup
-// heads, so the concurrently running items share K^/V^ of a few heads through L2; non-causal items are
-// head-major.  Every pipeline index (K/V stages, S buffers, barrier phases) runs on the CTA's global tile
-// count, so the next item's Q load and first S MMAs overlap the current item's last tile.
-constexpr int kHeadGroup = 8;
-__device__ __forceinline__ void fwd_item(int k, int T, int BH, bool causal, int& bh, int& i) {
-  if (!causal) {
-    bh = k / T;
-    i = k - bh * T;
-    return;
-  }
-  const int g = k / (kHeadGroup * T), r = k - g * kHeadGroup * T;
-  const int hn = min(kHeadGroup, BH - g * kHeadGroup);
-  i = T - 1 - r / hn;
-  bh = g * kHeadGroup + r % hn;
-}
 
 // FP8 (SAGE_PV_FP8): P^ and V^ in E4M3 and P^V^ as a kind::f8f6f4 MMA (fp32 accumulator) -- a separate
 // instantiation, the INT8 path of Alg. 1 untouched
@@ -120,13 +101,17 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* p_full = s_full + 2;         // softmax -> MMA (4 warps): S_j read, P^_j written
   uint64_t* o_full = s_full + 3;         // MMA -> softmax: PV_j in TMEM (P^_j read)
   uint64_t* o_empty = s_full + 4;        // softmax -> MMA (4 warps): PV_j drained
-  uint64_t* q_empty = s_full + 5;        // MMA -> TMA: the item's last S MMA has read Q^_i
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
   float* bias_s = reinterpret_cast<float*>(smem + L::kBias);
 
   const int T = N / kBlk;
   const int warp = threadIdx.x / 32;
-  const int W = BH * T;  // work items
+  // head-major order (the CTAs of one head share K^/V^ through L2); causal: longest (high i) first
+  const int tile = blockIdx.x;
+  const int bh = tile / T;
+  const int i = CAUSAL ? (T - 1 - tile % T) : (tile % T);
+  const int nj = CAUSAL ? i + 1 : T;
+  const int row0 = bh * N + i * kBlk;  // first global row of this q block
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -141,7 +126,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_init(p_full, 4);
     mbar_init(o_full, 1);
     mbar_init(o_empty, 4);
-    mbar_init(q_empty, 1);
     fence_mbar_init();
   }
   if (warp == 5) tmem_alloc(tmem_slot, 256);
@@ -163,38 +147,26 @@ __global__ void __launch_bounds__(kThreads, 2)
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
+        mbar_expect_tx(q_full, L::kTile);
+        tma_load_2d(smem + L::kQ, &tm_q, q_full, 0, row0);
       }
       __syncwarp();
-      int gt = 0, n = 0;  // global tile count, item ordinal
-      for (int k = blockIdx.x; k < W; k += gridDim.x, ++n) {
-        int bh, i;
-        fwd_item(k, T, BH, CAUSAL, bh, i);
-        const int nj = CAUSAL ? i + 1 : T;
-        mbar_wait(q_empty, (n & 1) ^ 1);  // the previous item's S MMAs are done with Q^
+      for (int j = 0; j < nj; ++j) {
+        const int st = j % kStages;
+        const uint32_t ph = (j / kStages) & 1;
+        const int krow = bh * N + j * kBlk;
+        mbar_wait(k_empty + st, ph ^ 1);
         if (elect_one()) {
-          mbar_expect_tx(q_full, L::kTile);
-          tma_load_2d(smem + L::kQ, &tm_q, q_full, 0, bh * N + i * kBlk);
+          mbar_expect_tx(k_full + st, L::kTile);
+          tma_load_2d(smem + L::kK + st * L::kTile, &tm_k, k_full + st, 0, krow);
         }
         __syncwarp();
-        for (int j = 0; j < nj; ++j) {
-          const int gg = gt + j;
-          const int st = gg % kStages;
-          const uint32_t ph = (gg / kStages) & 1;
-          const int krow = bh * N + j * kBlk;
-          mbar_wait(k_empty + st, ph ^ 1);
-          if (elect_one()) {
-            mbar_expect_tx(k_full + st, L::kTile);
-            tma_load_2d(smem + L::kK + st * L::kTile, &tm_k, k_full + st, 0, krow);
-          }
-          __syncwarp();
-          mbar_wait(v_empty + st, ph ^ 1);
-          if (elect_one()) {
-            mbar_expect_tx(v_full + st, L::kTile);
-            tma_load_2d(smem + L::kV + st * L::kTile, &tm_v, v_full + st, 0, krow);
-          }
-          __syncwarp();
+        mbar_wait(v_empty + st, ph ^ 1);
+        if (elect_one()) {
+          mbar_expect_tx(v_full + st, L::kTile);
+          tma_load_2d(smem + L::kV + st * L::kTile, &tm_v, v_full + st, 0, krow);
         }
-        gt += nj;
+        __syncwarp();
       }
     } else if (warp == 5) {
       // ---------------------------------------------------------- MMA issuer
@@ -246,45 +218,17 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         __syncwarp();
       };
-      // S cursor: two tiles ahead of PV, across item boundaries (global tile gs = item sk's tile sj)
-      int sk = blockIdx.x, sj = 0, sn = 0, s_nj = 0, gs = 0;
-      auto s_item_nj = [&](int k) {
-        int bh, i;
-        fwd_item(k, T, BH, CAUSAL, bh, i);
-        return CAUSAL ? i + 1 : T;
-      };
-      if (sk < W) s_nj = s_item_nj(sk);
-      auto issue_next_s = [&]() {
-        if (sk >= W) return;
-        if (sj == 0) {
-          mbar_wait(q_full, sn & 1);  // this item's Q^_i
-          tc_fence_after();
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      if (nj > 1) issue_s(1);
+      for (int j = 0; j < nj; ++j) {
+        mbar_wait(p_full, j & 1);  // S_j consumed, P^_j written (and PV_{j-1} drained)
+        TRF(6, j);
+        issue_pv(j);               // into S_j's buffer
+        if (j + 2 < nj) {
+          mbar_wait(o_empty, j & 1);  // PV_j drained (done early in tile j+1)
+          issue_s(j + 2);            // into the same buffer
         }
-        issue_s(gs);
-        if (sj == s_nj - 1 && elect_one()) mma_commit(q_empty);  // the item's last S: Q^ may be reloaded
-        __syncwarp();
-        ++gs;
-        if (++sj == s_nj) {
-          sj = 0;
-          ++sn;
-          sk += gridDim.x;
-          if (sk < W) s_nj = s_item_nj(sk);
-        }
-      };
-      issue_next_s();
-      issue_next_s();
-      int gt = 0;
-      for (int k = blockIdx.x; k < W; k += gridDim.x) {
-        const int nj = s_item_nj(k);
-        for (int j = 0; j < nj; ++j) {
-          const int gg = gt + j;
-          mbar_wait(p_full, gg & 1);  // S_gg consumed, P^_gg written (and PV_{gg-1} drained)
-          TRF(6, gg);
-          issue_pv(gg);               // into S_gg's buffer
-          mbar_wait(o_empty, gg & 1);  // PV_gg drained (early in the next tile, or in the item's epilogue)
-          issue_next_s();              // S_{gg+2} into the same buffer
-        }
-        gt += nj;
       }
     }
   } else {
@@ -292,27 +236,21 @@ __global__ void __launch_bounds__(kThreads, 2)
     // ------------------------------------------------------------ softmax / correction (128 threads)
     const int r = threadIdx.x;  // query row within the block == TMEM lane
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const float sq = q_scale[(size_t)bh * T + i];
     const float tau2 = tau * kLog2e;
     // P^ levels: 127, or 255 for the unsigned variant (SAGE_P_U8)
     const float log2_pmax = FP8 ? kLog2_448 : pu8 ? kLog2_255 : kLog2_127;
     const float inv_pmax = FP8 ? 1.f / 448.f : pu8 ? 1.f / 255.f : 1.f / 127.f;
-    uint8_t* prow = smem + L::kP;
-    int gt = 0;  // global tile count of this CTA
-    for (int k = blockIdx.x; k < W; k += gridDim.x) {
-    int bh, i;
-    fwd_item(k, T, BH, CAUSAL, bh, i);
-    const int nj = CAUSAL ? i + 1 : T;
-    const int row0 = bh * N + i * kBlk;  // first global row of this q block
-    const float sq = q_scale[(size_t)bh * T + i];
     float oacc[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) oacc[c] = 0.f;
     float m = -INFINITY, l = 0.f;
     float prev_alpha = 0.f, prev_spv = 0.f;
+    uint8_t* prow = smem + L::kP;
 
     // O = alpha O + PV s_P s_V  (Alg. 1 line 10, reading A7); alpha == 1 skips the rescale
-    auto correct = [&](int jj, float alpha, float spv) {  // jj: the item's tile; its global tile gt + jj
-      const uint32_t tPV = tbuf(gt + jj);
+    auto correct = [&](int jj, float alpha, float spv) {
+      const uint32_t tPV = tbuf(jj);
       const float2 f = make_float2(spv, spv);
       const bool rescale = __any_sync(0xffffffffu, alpha != 1.f);
 #pragma unroll
@@ -344,23 +282,22 @@ __global__ void __launch_bounds__(kThreads, 2)
       const float c2 = sq * k_scale[(size_t)bh * T + j] * tau2;  // int32 -> log2-domain logit
       const float sv = v_scale[(size_t)bh * T + j];
       const bool diag = CAUSAL && (j == i);
-      const int gg = gt + j;  // global tile: pipeline buffers and barrier phases
-      const float* bj = bias_s + (gg & 1) * kBlk;
+      const float* bj = bias_s + (j & 1) * kBlk;
       if constexpr (QSMOOTH) {
         // bias row (tau*log2e * mu_Qi . K_sm[n]) for this kv tile, shared by all rows; two slots
-        // so one barrier per tile suffices (slot gg&1 was last read in tile gg-2)
-        bias_s[(gg & 1) * kBlk + r] = bias[((size_t)bh * T + i) * N + (size_t)j * kBlk + r] * tau2;
+        // so one barrier per tile suffices (slot j&1 was last read in tile j-2)
+        bias_s[(j & 1) * kBlk + r] = bias[((size_t)bh * T + i) * N + (size_t)j * kBlk + r] * tau2;
         named_bar_sync(1, 128);
       }
-      mbar_wait(s_full + (gg & 1), (gg >> 1) & 1);
+      mbar_wait(s_full + (j & 1), (j >> 1) & 1);
       tc_fence_after();
-      if (r == 0) TRF(2, gg);
+      if (r == 0) TRF(2, j);
       if (FDUMPING && g_fdump.s) {  // the int32 S accumulator of tile (i, j), unmasked (Alg. 1 line 7)
         int32_t* dst = g_fdump.s + ((size_t)bh * N + (size_t)i * kBlk + r) * N + (size_t)j * kBlk;
 #pragma unroll 1
         for (int c0 = 0; c0 < kBlk; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(tbuf(gg) + c0 + lane_off, v);
+          tmem_ld32(tbuf(j) + c0 + lane_off, v);
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
@@ -374,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int c0 = 0; c0 < kBlk; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(tbuf(gg) + c0 + lane_off, v);
+          tmem_ld32(tbuf(j) + c0 + lane_off, v);
           tmem_wait_ld();
           if (diag) {
 #pragma unroll
@@ -386,13 +323,13 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
         }
         rm = __int2float_rn(mx) * c2;  // max commutes with the positive scale
-        if (r == 0) TRF(3, gg);
+        if (r == 0) TRF(3, j);
       } else {
         rm = -INFINITY;
 #pragma unroll
         for (int c0 = 0; c0 < kBlk; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(tbuf(gg) + c0 + lane_off, v);
+          tmem_ld32(tbuf(j) + c0 + lane_off, v);
           tmem_wait_ld();
           if (diag) {
 #pragma unroll
@@ -418,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       // O update for tile j-1 first: PV_{j-1} is ready by now, and draining it frees its buffer
       // for S_{j+1}, which then runs on the tensor cores during this tile's pass 2
       if (j > 0) {
-        mbar_wait(o_full, (gg - 1) & 1);
+        mbar_wait(o_full, (j - 1) & 1);
         tc_fence_after();
         correct(j - 1, prev_alpha, prev_spv);
       }
@@ -429,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
       for (int c0 = 0; c0 < kBlk; c0 += 32) {
         uint32_t v[32];
-        tmem_ld32(tbuf(gg) + c0 + lane_off, v);
+        tmem_ld32(tbuf(j) + c0 + lane_off, v);
         tmem_wait_ld();
         uint32_t pk[8];
 #pragma unroll
@@ -482,14 +419,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
       if constexpr (kPTmem) {
-        tmem_st32(tbuf(gg) + D + lane_off, pw);  // S_j's columns [D, D+32) have all been read
+        tmem_st32(tbuf(j) + D + lane_off, pw);  // S_j's columns [D, D+32) have all been read
         tmem_wait_st();
       } else {
         fence_proxy_async_smem();
       }
       tc_fence_before();
       warp_arrive(p_full);
-      if (r == 0) TRF(4, gg);
+      if (r == 0) TRF(4, j);
       // l = alpha l + e^{rowmax - m_ij} sum(e^{S - rowmax})  (line 8, reading A7)
       l = fmaf(alpha, l, e_rm * inv_pmax * (rs2.x + rs2.y));
       const float spv = e_rm * inv_pmax * sv;
@@ -498,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       prev_alpha = alpha;
       prev_spv = spv;
     }
-    mbar_wait(o_full, (gt + nj - 1) & 1);
+    mbar_wait(o_full, (nj - 1) & 1);
     tc_fence_after();
     correct(nj - 1, prev_alpha, prev_spv);
     // epilogue: O = acc / l (Alg. 1 line 13), L = m + ln l (line 14, natural log)
@@ -520,8 +457,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
     lse[(size_t)row0 + r] = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
-    gt += nj;
-    }  // items
   }
   __syncwarp();
   tc_fence_before();
@@ -532,28 +467,15 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
-// SM count of the current device (persistent grid size), cached per device
-int sm_count() {
-  static int cache[64] = {0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
-  if (!cache[dev] && cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-    return 148;
-  return cache[dev];
-}
-
 template <int D, bool C, bool QS, bool F8>
 cudaError_t launch_t(const FwdArgs& a, cudaStream_t s) {
   auto kern = sage_fwd_kernel<D, C, QS, F8>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem<D>::kAlloc);
   if (e != cudaSuccess) return e;
   const int T = a.N / kBlk;
-  const long long items = (long long)a.BH * T;
-  // persistent: two CTAs per SM (the kernel's residency), each walking items with stride gridDim.x
-  const int grid = (int)(items < 2LL * sm_count() ? items : 2LL * sm_count());
-  kern<<<grid, kThreads, FwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_v, a.q_scale, a.k_scale, a.v_scale,
-                                                  a.bias, a.o, a.lse, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
-                                                  a.fp16 ? 1 : 0, a.f32out ? 1 : 0, a.ablate);
+  kern<<<a.BH * T, kThreads, FwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_v, a.q_scale, a.k_scale, a.v_scale,
+                                                       a.bias, a.o, a.lse, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
+                                                       a.fp16 ? 1 : 0, a.f32out ? 1 : 0, a.ablate);
   return cudaGetLastError();
 }
 

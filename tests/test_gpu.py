@@ -592,3 +592,43 @@ def test_repeatable_under_reuse(d, causal, qs):
         for name, a, b in zip(("o", "lse", "dk", "dv"), ref[:2] + ref[3:], (o, lse, dk, dv)):
             assert torch.equal(a, b), name
         assert rel_l2(f64(ref[2]), f64(dq)) < 1e-4
+
+
+# ------------------------------------------------------------------ FP8 E4M3 P^V^ (SAGE_PV_FP8, NEXT-4)
+PV_FP8_CASES = [
+    (1, 2, 384, 64, True, True, False, "qknorm"),
+    (1, 2, 256, 128, False, True, False, "gauss"),
+    (1, 2, 384, 128, True, True, True, "outlier_kq"),
+]
+
+
+@pytest.mark.parametrize("B,H,N,d,causal,ks,qs,recipe", PV_FP8_CASES)
+def test_pv_fp8_parity(B, H, N, d, causal, ks, qs, recipe):
+    """SAGE_PV_FP8 (reading A30) against the oracle's ORC_PV_FP8 mode: V^ in E4M3 and its scales bit-exact
+    (Tier A, psi_block_e4m3 per 128-row block), O, L and the (unchanged) backward within the tolerance."""
+    q, k, v, do = make_inputs(B, H, N, d, recipe, seed=1400 + N + d)
+    dev = "cuda"
+    qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
+    o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, k_smooth=ks, q_smooth=qs, pv_fp8=True)
+    dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
+    torch.cuda.synchronize()
+    BH, T = B * H, N // 128
+    p = ctx.params
+    wsf = sage._ws.get(p, False, torch.device(dev))
+    wv = sage.ws_view(p, False, wsf)
+    base = wsf.data_ptr()
+    v8 = wsf[wv.v_i8 - base: wv.v_i8 - base + BH * N * d].view(torch.float8_e4m3fn).float().cpu().numpy()
+    sv = wsf[wv.v_scale - base: wv.v_scale - base + BH * T * 4].view(torch.float32).cpu().numpy().reshape(BH, T)
+    vf = f64(v).reshape(BH, N, d)
+    for h in range(BH):
+        for t in range(T):
+            ref_q, ref_s = oracle.psi_block_e4m3(vf[h, t * 128:(t + 1) * 128])
+            np.testing.assert_array_equal(v8.reshape(BH, N, d)[h, t * 128:(t + 1) * 128], ref_q)
+            assert sv[h, t] == np.float32(ref_s)
+    heads = list(range(BH))
+    sel = lambda t: f64(t).reshape(BH, N, d)
+    kw = dict(causal=causal, k_smooth=ks, q_smooth=qs)
+    f = oracle.fwd(sel(q), sel(k), sel(v), pv_fp8=True, **kw)
+    b = oracle.bwd(sel(q), sel(k), sel(v), round_bf16(f["o"]), sel(do), f["lse"], **kw)
+    gpu = dict(o=o, lse=lse, dq=dq, dk=dk, dv=dv)
+    _assert_ok(_compare(gpu, f, b, heads, B, H, N, d), ("pv_fp8", B, H, N, d, causal, qs))

@@ -125,3 +125,36 @@ def test_fused_tiles(trace_lib, B, H, N, d, causal, ks, qs, recipe, u8):
             sp_ulp = max(sp_ulp, float((np.abs(sp_g - sp_r) / ulp).max()))
     assert max_p_diff <= 1 and n_same / n_p >= 0.9999, (max_p_diff, n_same / n_p)
     assert sp_ulp <= 64, sp_ulp
+
+
+@pytest.mark.parametrize("d,causal", [(64, True), (128, False)])
+def test_fused_tiles_pv_fp8(trace_lib, d, causal):
+    """SAGE_PV_FP8 (Tier B on the fused kernel): K2's fp32 P^V^ accumulator (kind::f8f6f4) equals its own
+    dumped E4M3 P^ times the E4M3 V^ within fp32 accumulation (1e-6 of the sum of |products|); every dumped
+    P^ is a finite E4M3 value in [0, 448] with 448 attained in every processed row (the row max)."""
+    B, H, N = 1, 2, 384
+    BH, T = B * H, N // 128
+    q, k, v, do = make_inputs(B, H, N, d, "qknorm", seed=1500 + d)
+    dev = torch.device("cuda")
+    qd, kd, vd = (t.to(dev) for t in (q, k, v))
+    fb = sage.debug_fwd_dump(BH, N, d, dev)
+    o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, pv_fp8=True)
+    torch.cuda.synchronize()
+    sage.debug_fwd_dump(0, 0, 0, None)
+    wsf = sage._ws.get(ctx.params, False, dev)
+    v8 = _ws_tensor(wsf, sage.ws_view(ctx.params, False, wsf).v_i8, BH * N * d, torch.int8, (BH, N, d))
+    v8 = torch.from_numpy(v8).view(torch.float8_e4m3fn).double().numpy()
+    p8 = fb["p_hat"].cpu().view(torch.float8_e4m3fn).double().numpy()
+    pv = fb["pv"].cpu().view(torch.float32).double().numpy()
+    blk = lambda t: slice(t * 128, (t + 1) * 128)
+    same = total = 0
+    for h in range(BH):
+        for i in range(T):
+            for j in range(T):
+                if causal and j > i:
+                    continue
+                P, V = p8[h][blk(i), blk(j)], v8[h][blk(j)]
+                ref = P @ V
+                bound = 1e-6 * (np.abs(P) @ np.abs(V)) + 1e-30
+                assert (np.abs(pv[h, j, blk(i)] - ref) <= bound).all(), (h, i, j)
+                assert np.isfinite(P).all() and P.min() >= 0 and (P.max(axis=1) == 448.0).all(), (h, i, j)
