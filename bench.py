@@ -330,17 +330,17 @@ def _parity_rows(c, lo, outs):
 
 
 def config_dict(c, l2, world, args):
-    qk_norm, p_u8, det, fine = args.qk_norm, args.p_u8, args.deterministic, args.fine_bwd
+    qk_norm, p_u8, det, fine, f8 = args.qk_norm, args.p_u8, args.deterministic, args.fine_bwd, args.pv_fp8
     BH = c.batch * c.heads
     par = (f"heads split over {world} ranks (strong: rank r owns flattened heads [r*{BH}/{world}, (r+1)*{BH}/{world}))"
            if args.scaling == "strong" else f"{world} ranks x a full config of distinct heads (weak)")
     return {"workload": f"{c.name}: B={c.batch} H={c.heads} N={c.seqlen} d={c.head_dim} "
                         f"{'causal' if c.causal else 'non-causal'} K-smooth={c.k_smooth} Q-smooth={c.q_smooth} "
                         f"inputs={c.recipe}" + (" +QK-norm (fused)" if qk_norm else "") + (" P^ u8" if p_u8 else "")
-                        + (" deterministic" if det else "") + (" fine-bwd" if fine else ""),
+                        + (" deterministic" if det else "") + (" fine-bwd" if fine else "") + (" PV fp8" if f8 else ""),
             "batch": c.batch, "heads": c.heads, "seqlen": c.seqlen, "head_dim": c.head_dim, "causal": c.causal,
             "k_smooth": c.k_smooth, "q_smooth": c.q_smooth, "qk_norm": qk_norm, "p_u8": p_u8,
-            "deterministic": det, "fine_bwd": fine, "l2": l2, "parallelism": par}
+            "deterministic": det, "fine_bwd": fine, "pv_fp8": f8, "l2": l2, "parallelism": par}
 
 
 # ---------------------------------------------------------------------- GPU arm
@@ -363,6 +363,7 @@ def main():
     ap.add_argument("--p-u8", action="store_true", help="unsigned P^ variant (SAGE_P_U8)")
     ap.add_argument("--deterministic", action="store_true", help="bitwise reproducible dQ (SAGE_DETERMINISTIC)")
     ap.add_argument("--fine-bwd", action="store_true", help="per-key / per-query backward psi (SAGE_FINE_BWD)")
+    ap.add_argument("--pv-fp8", action="store_true", help="the forward's P^V^ in FP8 E4M3 (SAGE_PV_FP8)")
     args = ap.parse_args()
     assert args.warmup >= 3, "at least 3 warm-up steps"
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -394,6 +395,8 @@ def main():
         kw["deterministic"] = True
     if args.fine_bwd:
         kw["fine_bwd"] = True
+    if args.pv_fp8:
+        kw["pv_fp8"] = True
     if args.qk_norm:
         # the config's Q, K serve as the pre-norm X_q, X_k; gamma ~ U(0.5, 2) seeded
         g = torch.Generator().manual_seed(c.seed + 7)
@@ -443,7 +446,7 @@ def main():
     # the step's outputs (after the timed loop: every step recomputes the same values), kept for parity
     outs = dict(o=o, lse=lse, dq=dq, dk=dk, dv=dv)
     parity = None
-    if not args.no_parity and not (args.qk_norm or args.p_u8 or args.deterministic or args.fine_bwd):
+    if not args.no_parity and not (args.qk_norm or args.p_u8 or args.deterministic or args.fine_bwd or args.pv_fp8):
         torch.cuda.synchronize()
         parity = _parity_rows(c, lo, outs)
 

@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int T = N / kBlk;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t one = blockDim.x / kThreads;  // a runtime 1 (i2f2 on the FMA pipe, SAGE_I2F_FMA)
   const int tile = blockIdx.x;
   // head-major order: the T CTAs of one head run together and share its Q^/dO/dO^ tiles and
   // its dQ accumulator through L2; within a head, low j (most query blocks when causal) first.
@@ -570,8 +571,8 @@ if (cm) {
 #pragma unroll
         for (int e4 = 0; e4 < 8; ++e4) {
           float4 l4 = Ls4[cc * 8 + e4];
-          float2 a = make_float2(__int2float_rn((int)v[4 * e4]), __int2float_rn((int)v[4 * e4 + 1]));
-          float2 b = make_float2(__int2float_rn((int)v[4 * e4 + 2]), __int2float_rn((int)v[4 * e4 + 3]));
+          float2 a = i2f2(v[4 * e4], v[4 * e4 + 1], one);
+          float2 b = i2f2(v[4 * e4 + 2], v[4 * e4 + 3], one);
           float2 na = make_float2(-l4.x, -l4.y), nb = make_float2(-l4.z, -l4.w);
           if constexpr (QSMOOTH) {
             na = fadd2(na, make_float2(b2, b2));
@@ -785,7 +786,7 @@ if (cm) {
           }
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
-            const float2 x = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f,
+            const float2 x = ffma2(i2f2(v[e], v[e + 1], one), f,
                                    make_float2(__uint_as_float(a[e]), __uint_as_float(a[e + 1])));
             a[e] = __float_as_uint(x.x);
             a[e + 1] = __float_as_uint(x.y);
@@ -835,7 +836,7 @@ if (cm) {
               dump_words(g_dacc.dv + (((size_t)bh * T + i) * N + j * kBlk + r) * D + c0, v, 32);
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {
-              float2 x = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f,
+              float2 x = ffma2(i2f2(v[e], v[e + 1], one), f,
                                make_float2(dv_acc[c0 + e], dv_acc[c0 + e + 1]));
               dv_acc[c0 + e] = x.x;
               dv_acc[c0 + e + 1] = x.y;
@@ -879,7 +880,7 @@ if (cm) {
               const float2 m2 = *reinterpret_cast<const float2*>(muq + cc);
               acc = ffma2(make_float2(fb, fb), m2, acc);
             }
-            float2 x = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f, acc);
+            float2 x = ffma2(i2f2(v[e], v[e + 1], one), f, acc);
             dk_acc[cc] = x.x;
             dk_acc[cc + 1] = x.y;
           }
@@ -925,8 +926,8 @@ if (cm) {
               uint8_t* box = stage + bx * L::kDqBox;
 #pragma unroll
               for (int e = 0; e < 32; e += 4) {
-                float2 a = fmul2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])), f);
-                float2 b = fmul2(make_float2(__int2float_rn((int)v[e + 2]), __int2float_rn((int)v[e + 3])), f);
+                float2 a = fmul2(i2f2(v[e], v[e + 1], one), f);
+                float2 b = fmul2(i2f2(v[e + 2], v[e + 3], one), f);
                 *reinterpret_cast<float4*>(box + sw_offset(lane, e / 4, 128)) = make_float4(a.x, a.y, b.x, b.y);
               }
             }

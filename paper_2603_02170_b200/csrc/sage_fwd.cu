@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   const int T = N / kBlk;
   const int warp = threadIdx.x / 32;
+  const uint32_t one = blockDim.x / kThreads;  // a runtime 1 (i2f2 on the FMA pipe, SAGE_I2F_FMA)
   // head-major order (the CTAs of one head share K^/V^ through L2); causal: longest (high i) first
   const int tile = blockIdx.x;
   const int bh = tile / T;
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           float2 acc = make_float2(oacc[c0 + e], oacc[c0 + e + 1]);
           if (rescale) acc = fmul2(acc, make_float2(alpha, alpha));
           const float2 pv = FP8 ? make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1]))  // fp32 D
-                                : make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1]));
+                                : i2f2(v[e], v[e + 1], one);
           acc = ffma2(pv, f, acc);
           oacc[c0 + e] = acc.x;
           oacc[c0 + e + 1] = acc.y;
@@ -339,9 +340,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
             for (int e = 0; e < 32; e += 4) {
               const float4 b4 = *reinterpret_cast<const float4*>(bj + c0 + e);
-              const float2 a = ffma2(make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1])),
+              const float2 a = ffma2(i2f2(v[e], v[e + 1], one),
                                      make_float2(c2, c2), make_float2(b4.x, b4.y));
-              const float2 b = ffma2(make_float2(__int2float_rn((int)v[e + 2]), __int2float_rn((int)v[e + 3])),
+              const float2 b = ffma2(i2f2(v[e + 2], v[e + 3], one),
                                      make_float2(c2, c2), make_float2(b4.z, b4.w));
               rm = fmax3(rm, fmax3(a.x, a.y, b.x), b.y);
             }
@@ -372,8 +373,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int e4 = 0; e4 < 8; ++e4) {
           const int e = e4 * 4;
-          float2 a = make_float2(__int2float_rn((int)v[e]), __int2float_rn((int)v[e + 1]));
-          float2 b = make_float2(__int2float_rn((int)v[e + 2]), __int2float_rn((int)v[e + 3]));
+          float2 a = i2f2(v[e], v[e + 1], one);
+          float2 b = i2f2(v[e + 2], v[e + 3], one);
           if constexpr (QSMOOTH) {
             const float4 b4 = *reinterpret_cast<const float4*>(bj + c0 + e);
             a = ffma2(a, make_float2(c2, c2), fadd2(make_float2(b4.x, b4.y), make_float2(-sub, -sub)));

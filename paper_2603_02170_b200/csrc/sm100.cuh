@@ -440,6 +440,25 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(j.x) << 23)),
                      __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(j.y) << 23)));
 }
+// Two int32 accumulator values (|x| < 2^22: every tile accumulator here, d * 127 * 255 < 2^23) -> fp32,
+// exactly.  SAGE_I2F_FMA=0: two I2FP (ALU pipe).  =1: x * one + bits(1.5 * 2^23) as an IMAD on the FMA pipe
+// (`one` must be a runtime 1 the compiler cannot fold, or ptxas turns the IMAD into an ALU IADD3), then one
+// packed FADD2 of -1.5 * 2^23 -- moves the conversions off the ALU pipe.
+#ifndef SAGE_I2F_FMA
+#define SAGE_I2F_FMA 0
+#endif
+__device__ __forceinline__ float2 i2f2(uint32_t a, uint32_t b, uint32_t one) {
+#if SAGE_I2F_FMA
+  uint32_t fa, fb;
+  asm("mad.lo.u32 %0, %1, %2, 0x4B400000;" : "=r"(fa) : "r"(a), "r"(one));
+  asm("mad.lo.u32 %0, %1, %2, 0x4B400000;" : "=r"(fb) : "r"(b), "r"(one));
+  return fadd2(make_float2(__uint_as_float(fa), __uint_as_float(fb)), make_float2(-kMagic, -kMagic));
+#else
+  (void)one;
+  return make_float2(__int2float_rn((int)a), __int2float_rn((int)b));
+#endif
+}
+
 // two fp32 values -> one 32-bit word of the I/O type: bf16x2, or fp16x2 with SAGE_FP16 (RNE)
 __device__ __forceinline__ uint32_t pack2_io(float a, float b, bool fp16) {
   if (fp16) {
