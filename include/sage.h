@@ -19,8 +19,8 @@
  * all-zero blocks, causal masking, ...) are listed in DESIGN.md section 3.
  *
  * Conventions
- *   - Tensors Q, K, V, O, dO, dQ, dK, dV: bf16 (fp16 with SAGE_FP16), contiguous [B, H, N, d] (d innermost),
- *     16-byte aligned device pointers on the current device.  N % 128 == 0, d in {64, 128}.  With
+ *   - Tensors Q, K, V, O, dO, dQ, dK, dV: bf16 (fp16 with SAGE_FP16), [B, H, N, d] with d innermost and the
+ *     strides of sage_params (contiguous by default), 16-byte aligned device pointers on the current device.  N % 128 == 0, d in {64, 128}.  With
  *     SAGE_FP32_OUT the outputs O, dQ, dK, dV are fp32 instead.
  *   - lse: fp32 [B, H, N], natural log (Alg. 1 line 14).
  *   - Ownership: the caller allocates every buffer (device memory), including the
@@ -106,6 +106,12 @@ typedef struct {
   int32_t batch, heads, seqlen, head_dim; /* B, H, N, d */
   uint32_t flags;                         /* SAGE_* bit set */
   float softmax_scale;                    /* tau; 0 => 1/sqrt(d) (reading A6) */
+  /* Element strides of the batch, head and token dimensions of every I/O tensor (Q, K, V, O, dO, dQ, dK, dV,
+   * and X_q, X_k, dX_q, dX_k with QK-norm; the head dimension d is contiguous): row (b, h, n) starts at
+   * b * stride_b + h * stride_h + n * stride_n.  All three 0 = contiguous [B, H, N, d].  Otherwise each must
+   * be a multiple of 8 elements and stride_n >= d (e.g. a [B, N, H, d] tensor: stride_b = N H d,
+   * stride_h = d, stride_n = H d).  lse stays contiguous [B, H, N]. */
+  int64_t stride_b, stride_h, stride_n;
 } sage_params;
 
 /* The forward->backward context (Alg. 2's inputs): a caller-owned device buffer plus a host

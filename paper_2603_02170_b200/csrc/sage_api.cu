@@ -68,6 +68,7 @@ struct Dims {
   size_t BH, N, d, T;
   bool causal, ks, qs, pu8, qkn, det, pcol, fine, fp16, f32out, pvfp8;
   float tau;
+  IoLayout io;  // element strides of the I/O tensors
 };
 
 bool dims_of(const sage_params* p, Dims* o) {
@@ -100,6 +101,16 @@ bool dims_of(const sage_params* p, Dims* o) {
   if (o->det && (o->pcol || o->fine)) return false;  // one backward variant at a time
   if (o->f32out && o->qkn) return false;              // the QK-norm outputs dX are I/O-typed
   o->tau = p->softmax_scale > 0.f ? p->softmax_scale : 1.f / std::sqrt((float)p->head_dim);
+  // I/O layout: all strides 0 = contiguous [B, H, N, d]; otherwise every stride >= 1 and a multiple of 8
+  // elements (16-byte rows for the vector loads and the TMA maps), the token stride at least d
+  const long long sb = p->stride_b, sh = p->stride_h, sn = p->stride_n;
+  if (sb == 0 && sh == 0 && sn == 0) {
+    o->io = IoLayout{(long long)p->heads * p->seqlen * p->head_dim, (long long)p->seqlen * p->head_dim,
+                     (long long)p->head_dim, p->heads};
+  } else {
+    if (sb <= 0 || sh <= 0 || sn < p->head_dim || (sb | sh | sn) % 8) return false;
+    o->io = IoLayout{sb, sh, sn, p->heads};
+  }
   return true;
 }
 
@@ -239,6 +250,10 @@ uint64_t params_tag(const sage_params* p) {
   mix((uint32_t)p->head_dim);
   mix(p->flags);
   mix(sc);
+  for (long long v : {(long long)p->stride_b, (long long)p->stride_h, (long long)p->stride_n}) {
+    mix((uint32_t)v);
+    mix((uint32_t)((unsigned long long)v >> 32));
+  }
   return h ? h : 1;
 }
 
@@ -278,6 +293,59 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, TmapType type, uint64_t rows
   }
   if (!make_tmap_2d_uncached(m, base, type, rows, cols, box_rows, box_cols)) return false;
   *victim = TmapEntry{base, rows, cols, box_rows, box_cols, (uint32_t)type, (uint32_t)dev, ++g_tmap_clock, *m};
+  return true;
+}
+
+bool make_tmap_io(CUtensorMap* m, const void* base, TmapType type, int B, int N, int d, const IoLayout& io,
+                  uint32_t box_rows, uint32_t box_cols) {
+  // a contiguous tensor is the 2-D map the kernels' 4-D coordinates reduce to; otherwise a 4-D map
+  // (d, N, H, B) with the caller's strides.  Cached like the 2-D maps (keyed by base, shape and strides).
+  struct Entry {
+    const void* base;
+    long long sb, sh, sn;
+    int B, H, N, d, type, device;
+    uint32_t box_rows, box_cols;
+    uint64_t stamp;
+    CUtensorMap map;
+  };
+  constexpr int kCache = 16;
+  thread_local Entry cache[kCache];
+  thread_local uint64_t clock = 0;
+  int dev = 0;
+  (void)cudaGetDevice(&dev);
+  Entry* victim = &cache[0];
+  for (auto& e : cache) {
+    if (e.stamp && e.base == base && e.sb == io.sb && e.sh == io.sh && e.sn == io.sn && e.B == B && e.H == io.H &&
+        e.N == N && e.d == d && e.type == (int)type && e.device == dev && e.box_rows == box_rows && e.box_cols == box_cols) {
+      e.stamp = ++clock;
+      *m = e.map;
+      return true;
+    }
+    if (e.stamp < victim->stamp) victim = &e;
+  }
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  const uint32_t esz = type == kF32 ? 4 : (type == kBF16 || type == kF16) ? 2 : 1;
+  const CUtensorMapDataType dt = type == kF32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : type == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                 : type == kF16  ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)N, (cuuint64_t)io.H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)io.sn * esz, (cuuint64_t)io.sh * esz, (cuuint64_t)io.sb * esz};
+  cuuint32_t box[4] = {box_cols, box_rows, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const uint32_t row_bytes = box_cols * esz;
+  CUtensorMapSwizzle sw = row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = enc(m, dt, 4, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    if (std::getenv("SAGE_DEBUG"))
+      std::fprintf(stderr, "[libsage] cuTensorMapEncodeTiled (4-D) -> %d\n", (int)r);
+    return false;
+  }
+  *victim = Entry{base, io.sb, io.sh, io.sn, B, io.H, N, d, (int)type, dev, box_rows, box_cols, ++clock, *m};
   return true;
 }
 
@@ -453,11 +521,11 @@ sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v,
   // QK-norm: the row statistics and normalised values are formed on the fly in K0/K1
   // K0: smoothing statistics
   if (D.ks) {
-    if ((e = launch_colsum(kb, partk, BH, N, d, s, nk, h)) != cudaSuccess) return cuda_fail(e);
+    if ((e = launch_colsum(kb, partk, BH, N, d, s, nk, h, D.io)) != cudaSuccess) return cuda_fail(e);
     if ((e = launch_colmean(partk, muk, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
   }
   if (D.qs) {
-    if ((e = launch_colsum(qb, partq, BH, N, d, s, nq, h)) != cudaSuccess) return cuda_fail(e);
+    if ((e = launch_colsum(qb, partq, BH, N, d, s, nq, h, D.io)) != cudaSuccess) return cuda_fail(e);
     if ((e = launch_blockmean(partq, muq, BH, N, d, s)) != cudaSuccess) return cuda_fail(e);
   }
   // K1: per-block psi (Alg. 1 line 3)
@@ -466,10 +534,11 @@ sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v,
   qj.j[1] = QuantJob{kb, muk, D.ks ? 1 : 0, k8, sk, rk, gk, eps};
   qj.j[0].fp8 = qj.j[1].fp8 = 0;
   qj.j[2] = QuantJob{vb, nullptr, 0, v8, sv, nullptr, nullptr, 0.f, D.pvfp8 ? 1 : 0};
-  if ((e = launch_quantize(qj, 3, BH, N, d, s, h)) != cudaSuccess) return cuda_fail(e);
+  if ((e = launch_quantize(qj, 3, BH, N, d, s, h, D.io)) != cudaSuccess) return cuda_fail(e);
   // mu_K is all-zero when K-smoothing is off (ctx is caller memory: make it so)
   if (!D.ks && (e = launch_fill(muk, D.BH * D.d, 0.f, s)) != cudaSuccess) return cuda_fail(e);
-  if (D.qs && (e = launch_qsmooth_bias(kb, muk, muq, bias, BH, N, d, s, nk, h)) != cudaSuccess) return cuda_fail(e);
+  if (D.qs && (e = launch_qsmooth_bias(kb, muk, muq, bias, BH, N, d, s, nk, h, D.io)) != cudaSuccess)
+    return cuda_fail(e);
   // K2: fused INT8 forward (Alg. 1 lines 4-14)
   a.q_scale = sq;
   a.k_scale = sk;
@@ -479,6 +548,7 @@ sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v,
   a.fp16 = D.fp16;
   a.f32out = D.f32out;
   a.pvfp8 = D.pvfp8;
+  a.io = D.io;
   a.lse = lse;
   a.BH = BH;
   a.N = N;
@@ -521,20 +591,22 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
   int8_t *q8 = at<int8_t>(cx, C.q8), *k8 = at<int8_t>(cx, C.k8), *do8 = at<int8_t>(ws, W.do8);
   float *sq = at<float>(cx, C.sq), *sk = at<float>(cx, C.sk), *sdo = at<float>(ws, W.sdo);
   float *delta = at<float>(ws, W.delta), *l2 = at<float>(ws, W.l2);
-  // SAGE_FP32_OUT: dQ is reduced straight into the caller's fp32 dq (zeroed by K3; no K5)
-  float* dqacc = D.f32out ? static_cast<float*>(dq) : at<float>(ws, W.dq);
+  // SAGE_FP32_OUT with contiguous outputs: dQ is reduced straight into the caller's fp32 dq (zeroed by K3; no K5)
+  const bool dq_direct = D.f32out && D.io.contiguous((int)D.N, (int)D.d);
+  float* dqacc = dq_direct ? static_cast<float*>(dq) : at<float>(ws, W.dq);
 
   BwdArgs a{};
   const uint64_t rows = D.BH * D.N;
   if (!make_tmap_2d(&a.tm_q, q8, kU8, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_k, k8, kU8, rows, d, kBlk, d) ||
-      !make_tmap_2d(&a.tm_doq, do8, kU8, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_v, v, D.fp16 ? kF16 : kBF16, rows, d, kBlk, 64) ||
-      !make_tmap_2d(&a.tm_do, dO, D.fp16 ? kF16 : kBF16, rows, d, kBlk, 64) ||
+      !make_tmap_2d(&a.tm_doq, do8, kU8, rows, d, kBlk, d) ||
+      !make_tmap_io(&a.tm_v, v, D.fp16 ? kF16 : kBF16, BH / D.io.H, N, d, D.io, kBlk, 64) ||
+      !make_tmap_io(&a.tm_do, dO, D.fp16 ? kF16 : kBF16, BH / D.io.H, N, d, D.io, kBlk, 64) ||
       !make_tmap_2d(&a.tm_dq, dqacc, kF32, rows, d, 32, 32))
     return cuda_fail(cudaErrorInvalidValue);
   cudaError_t e;
   // K3: delta, psi(dO), L*log2(e), zero dQ accumulator (Alg. 2 lines 2, 6)
   unsigned* dqflags = D.det ? at<unsigned>(ws, W.flags) : nullptr;
-  if ((e = launch_bwd_prep(o, dO, lse, delta, l2, do8, sdo, dqacc, BH, N, d, s, dqflags, D.fp16, D.f32out)) !=
+  if ((e = launch_bwd_prep(o, dO, lse, delta, l2, do8, sdo, dqacc, BH, N, d, s, dqflags, D.fp16, D.f32out, D.io)) !=
       cudaSuccess)
     return cuda_fail(e);
   // K4: fused INT8 backward (Alg. 2 lines 3-11)
@@ -550,6 +622,7 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
   a.dv = dv;
   a.fp16 = D.fp16;
   a.f32out = D.f32out;
+  a.io = D.io;
   a.BH = BH;
   a.N = N;
   a.d = d;
@@ -569,17 +642,17 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
     const auto* rq = at<const float>(cx, C.rq);
     const auto* rk = at<const float>(cx, C.rk);
     if ((e = launch_norm_bwd(dqacc, nullptr, xq, rq, gq, dq, at<float>(ws, W.gq),
-                             dgq, D.BH * D.N, d, s, D.fp16)) != cudaSuccess)
+                             dgq, D.BH * D.N, d, s, D.fp16, D.io, N)) != cudaSuccess)
       return cuda_fail(e);
     if ((e = launch_norm_bwd(nullptr, dk, xk, rk, gk, dk, at<float>(ws, W.gk),
-                             dgk, D.BH * D.N, d, s, D.fp16)) != cudaSuccess)
+                             dgk, D.BH * D.N, d, s, D.fp16, D.io, N)) != cudaSuccess)
       return cuda_fail(e);
     if (g_prof.on) g_prof.launches += 6;  // 2 x (norm_bwd, dgamma stage 1, stage 2)
     return SAGE_OK;
   }
-  // K5 (not with SAGE_FP32_OUT: dq already holds the fp32 sum)
-  if (D.f32out) return SAGE_OK;
-  if ((e = launch_dq_finalize(dqacc, dq, D.BH * D.N * D.d, s, D.fp16)) != cudaSuccess)
+  // K5 (not when dq already holds the fp32 sum)
+  if (dq_direct) return SAGE_OK;
+  if ((e = launch_dq_finalize(dqacc, dq, BH, N, d, s, D.fp16, D.io, D.f32out)) != cudaSuccess)
     return cuda_fail(e);
   if (g_prof.on) g_prof.launches += 1;  // K5
   return SAGE_OK;

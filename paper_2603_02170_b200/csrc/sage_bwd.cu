@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* __restrict__ l2g, const float* __restrict__ deltag, const float* __restrict__ bias,
                     const float* __restrict__ mu_q, float* __restrict__ dq_acc, void* __restrict__ dk_out,
                     void* __restrict__ dv_out, int N, int BH, float tau, int pu8, int fp16, int f32out,
-                    unsigned* __restrict__ dq_flags, int ablate_arg) {
+                    unsigned* __restrict__ dq_flags, IoLayout io, int ablate_arg) {
   constexpr bool fine = VAR == 3;
   constexpr bool pcol = VAR == 2 || fine;
   const int ablate = SAGE_TRACE ? ablate_arg : 0;
@@ -301,7 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(kv_full, 3 * L::kTile);
         tma_load_2d(smem + L::kK, &tm_k, kv_full, 0, krow);
 #pragma unroll
-        for (int p = 0; p < D / 64; ++p) tma_load_2d(smem + L::kV + p * 16384, &tm_v, kv_full, p * 64, krow);
+        for (int p = 0; p < D / 64; ++p)
+          tma_load_4d(smem + L::kV + p * 16384, &tm_v, kv_full, p * 64, j * kBlk, bh % io.H, bh / io.H);
       }
       __syncwarp();
       for (int it = 0; it < n_it; ++it) {
@@ -317,7 +318,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(st + L::kSQ, &tm_q, q_full + s, 0, qrow);
           if constexpr (!L::kSplitDO) {
 #pragma unroll
-            for (int p = 0; p < D / 64; ++p) tma_load_2d(st + L::kSDO + p * 16384, &tm_do, q_full + s, p * 64, qrow);
+            for (int p = 0; p < D / 64; ++p)
+              tma_load_4d(st + L::kSDO + p * 16384, &tm_do, q_full + s, p * 64, i * kBlk, bh % io.H, bh / io.H);
           }
           tma_load_2d(st + L::kSDOQ, &tm_doq, q_full + s, 0, qrow);
           bulk_load(st + L::kSL, l2g + qrow, 512, q_full + s);
@@ -329,7 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (elect_one()) {
             mbar_expect_tx(do_full, L::kDOTx);
 #pragma unroll
-            for (int p = 0; p < D / 64; ++p) tma_load_2d(smem + L::kDO + p * 16384, &tm_do, do_full, p * 64, qrow);
+            for (int p = 0; p < D / 64; ++p)
+              tma_load_4d(smem + L::kDO + p * 16384, &tm_do, do_full, p * 64, i * kBlk, bh % io.H, bh / io.H);
           }
           __syncwarp();
         }
@@ -960,7 +963,7 @@ if (cm) {
       tc_fence_after();
     }
     // epilogue: dK_j, dV_j rows -> bf16
-    const size_t orow = ((size_t)krow + r) * D;
+    const long long orow = io.row(bh, (long long)j * kBlk + r);  // dK, dV in the I/O layout
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 32) {
       float vv[32];
@@ -1020,7 +1023,7 @@ cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
   kern<<<a.BH * T, kThreads, kSmem, s>>>(a.tm_q, a.tm_k, a.tm_doq, a.tm_v, a.tm_do, a.tm_dq, a.q_scale,
                                                        a.k_scale, a.do_scale, a.l2, a.delta, a.bias, a.mu_q,
                                                        a.dq_acc, a.dk, a.dv, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
-                                                       a.fp16 ? 1 : 0, a.f32out ? 1 : 0, a.dq_flags, a.ablate);
+                                                       a.fp16 ? 1 : 0, a.f32out ? 1 : 0, a.dq_flags, a.io, a.ablate);
   return cudaGetLastError();
 }
 

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ q_scale,
                     const float* __restrict__ k_scale, const float* __restrict__ v_scale,
                     const float* __restrict__ bias, void* __restrict__ o_out, float* __restrict__ lse, int N,
-                    int BH, float tau, int pu8, int fp16, int f32out, int ablate_arg) {
+                    int BH, float tau, int pu8, int fp16, int f32out, IoLayout io, int ablate_arg) {
   const int ablate = SAGE_TRACE ? ablate_arg : 0;
   using L = FwdSmem<D>;
   constexpr int kStages = L::kStages;
@@ -442,13 +442,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     // epilogue: O = acc / l (Alg. 1 line 13), L = m + ln l (line 14, natural log)
     const float inv_l = l > 0.f ? 1.f / l : 0.f;
     if (f32out) {  // SAGE_FP32_OUT
-      float4* orow = reinterpret_cast<float4*>(static_cast<float*>(o_out) + ((size_t)row0 + r) * D);
+      float4* orow = reinterpret_cast<float4*>(static_cast<float*>(o_out) + io.row(bh, (long long)i * kBlk + r));
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 4)
         orow[c0 / 4] = make_float4(oacc[c0] * inv_l, oacc[c0 + 1] * inv_l, oacc[c0 + 2] * inv_l, oacc[c0 + 3] * inv_l);
     } else {
       // O in the I/O type (bf16, or fp16 with SAGE_FP16): 8 values per 16-byte store
-      uint4* orow = reinterpret_cast<uint4*>(static_cast<uint16_t*>(o_out) + ((size_t)row0 + r) * D);
+      uint4* orow = reinterpret_cast<uint4*>(static_cast<uint16_t*>(o_out) + io.row(bh, (long long)i * kBlk + r));
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 8) {
         uint32_t h[4];
@@ -476,7 +476,7 @@ cudaError_t launch_t(const FwdArgs& a, cudaStream_t s) {
   const int T = a.N / kBlk;
   kern<<<a.BH * T, kThreads, FwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_v, a.q_scale, a.k_scale, a.v_scale,
                                                        a.bias, a.o, a.lse, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
-                                                       a.fp16 ? 1 : 0, a.f32out ? 1 : 0, a.ablate);
+                                                       a.fp16 ? 1 : 0, a.f32out ? 1 : 0, a.io, a.ablate);
   return cudaGetLastError();
 }
 

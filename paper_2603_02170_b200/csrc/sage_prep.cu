@@ -131,13 +131,13 @@ __device__ __forceinline__ float warp_max(float v) {
 // result for any realistic input; it is fixed anyway.
 template <typename T, int D, bool QKN>
 __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, double* __restrict__ part,
-                                                     NormIn nrm) {
+                                                     NormIn nrm, IoLayout io, int nT) {
   constexpr int kGroups = D / kVec;        // 8 (d=64) or 16 (d=128)
   constexpr int kR = 256 / kGroups;        // 32 or 16 row phases
   __shared__ double red[kR][D];
   const long long chunk = blockIdx.x;      // bh * T + t
   const int g = threadIdx.x % kGroups, q = threadIdx.x / kGroups;
-  const T* p = x + chunk * kBlk * D + g * kVec;
+  const T* p = x + io.row(chunk / nT, (chunk % nT) * kBlk) + g * kVec;
   double acc[kVec];
   float gam[kVec];
 #pragma unroll
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, do
   constexpr int kRows = kBlk / kR;  // rows per thread: all loads issued before any arithmetic
   uint4 raw[kRows];
 #pragma unroll
-  for (int k = 0; k < kRows; ++k) raw[k] = *reinterpret_cast<const uint4*>(p + (size_t)(q + k * kR) * D);
+  for (int k = 0; k < kRows; ++k) raw[k] = *reinterpret_cast<const uint4*>(p + (q + k * kR) * io.sn);
   __shared__ double ssq[QKN ? nrm_smem_rows * kGroups : 1];
   __shared__ float rs_s[QKN ? kBlk : 1];
   if constexpr (QKN) chunk_rstd<T, kGroups, D, kRows, kR>(raw, g, q, ssq, rs_s, nrm.eps, nullptr);
@@ -196,7 +196,7 @@ __global__ void blockmean_kernel(const double* __restrict__ part, float* __restr
 // One CTA quantises one 128 x d block: x_sm = fl32(x - mu); amax; scale = fl32(amax/127);
 // inv = fl32(127/amax) (0 for an all-zero block, A3); q = clamp(RNE(fl32(x_sm*inv)), +-127).
 template <typename TI, int D, bool QKN>
-__global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T) {
+__global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T, IoLayout io) {
   // blockIdx.y selects the tensor (Q, K, V): one launch for all three psi passes
   const QuantJob& job = jobs.j[blockIdx.y];
   const TI* __restrict__ x = static_cast<const TI*>(job.x);
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T)
   const long long blk = blockIdx.x;               // bh * T + t
   const int bh = (int)(blk / T), t = (int)(blk % T);
   const int g = threadIdx.x % kGroups, r0 = threadIdx.x / kGroups;
-  const TI* xb = x + blk * kBlk * D;
+  const TI* xb = x + io.row(bh, (long long)t * kBlk);
   float m[kVec];
 #pragma unroll
   for (int e = 0; e < kVec; ++e) {
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T)
   uint4 raw[kIters];
 #pragma unroll
   for (int it = 0; it < kIters; ++it)
-    raw[it] = *reinterpret_cast<const uint4*>(xb + (size_t)(r0 + it * kRowsPerPass) * D + g * kVec);
+    raw[it] = *reinterpret_cast<const uint4*>(xb + (r0 + it * kRowsPerPass) * io.sn + g * kVec);
   // QK-norm row statistics (A24), kept for the backward (QKN launches: every job with gamma)
   __shared__ double ssq[QKN ? nrm_smem_rows * kGroups : 1];
   __shared__ float rs_s[QKN ? kBlk : 1];
@@ -299,7 +299,7 @@ template <typename TI, int D>
 __global__ void __launch_bounds__(128, SAGE_BIAS_MINB) qsmooth_bias_kernel(const TI* __restrict__ k,
                                                            const float* __restrict__ mu_k,
                                                            const float* __restrict__ mu_q, float* __restrict__ bias,
-                                                           int N, NormIn nrm) {
+                                                           int N, NormIn nrm, IoLayout io) {
   __shared__ float4 mq[kBiasI][D / 4];
   const int T = N / kBlk;
   const long long blk = blockIdx.x;    // bh * T + jn
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(128, SAGE_BIAS_MINB) qsmooth_bias_kernel(const
   for (int e = threadIdx.x; e < ni * (D / 4); e += blockDim.x)
     mq[e / (D / 4)][e % (D / 4)] = reinterpret_cast<const float4*>(mu_q + ((size_t)bh * T + i0) * D)[e];
   float ks[D];
-  const TI* krow = k + (blk * kBlk + n) * D;
+  const TI* krow = k + io.row(bh, (long long)jn * kBlk + n);
   const float* mk = mu_k + (size_t)bh * D;
   const float rs = nrm.gamma ? nrm.rstd[blk * kBlk + n] : 1.f;  // written by K1's K job
   uint4 raw[D / kVec];  // the whole K row in flight before any use (the loads' latency dominates)
@@ -371,28 +371,29 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const TO* __restrict__ o,
                                                        const float* __restrict__ lse, float* __restrict__ delta,
                                                        float* __restrict__ l2, int8_t* __restrict__ do_q,
                                                        float* __restrict__ do_scale, float* __restrict__ dq_acc,
-                                                       unsigned* __restrict__ dq_flags) {
+                                                       unsigned* __restrict__ dq_flags, IoLayout io, int nT) {
   constexpr int kGroups = D / kVec;            // threads per row
   constexpr int kRowsPerPass = 256 / kGroups;
   constexpr int kIters = kBlk / kRowsPerPass;
   __shared__ float red[8];
   const long long blk = blockIdx.x;
   const int g = threadIdx.x % kGroups, r0 = threadIdx.x / kGroups;
-  const size_t base = (size_t)blk * kBlk * D;
+  const size_t base = (size_t)blk * kBlk * D;                      // the contiguous buffers (dO^, dQ accumulator)
+  const long long iob = io.row(blk / nT, (blk % nT) * (long long)kBlk);  // O and dO in the I/O layout
   float v[kIters][kVec];
   float amax = 0.f;
   // dO rows in flight before any arithmetic (kIters 16-byte loads per thread); O's alongside
   uint4 rdo[kIters];
 #pragma unroll
   for (int it = 0; it < kIters; ++it)
-    rdo[it] = *reinterpret_cast<const uint4*>(dO + base + (size_t)(r0 + it * kRowsPerPass) * D + g * kVec);
+    rdo[it] = *reinterpret_cast<const uint4*>(dO + iob + (r0 + it * kRowsPerPass) * io.sn + g * kVec);
 #pragma unroll
   for (int it = 0; it < kIters; ++it) {
     const int r = r0 + it * kRowsPerPass;
     const size_t off = base + (size_t)r * D + g * kVec;
     float fo[kVec];
     unpack8<T>(rdo[it], v[it]);
-    load_o8<TO>(o + off, fo);
+    load_o8<TO>(o + iob + r * io.sn + g * kVec, fo);
     double dot = 0.0;
 #pragma unroll
     for (int e = 0; e < kVec; ++e) {
@@ -434,14 +435,23 @@ __global__ void fill_kernel(float* __restrict__ x, size_t n, float v) {
   if (i < n) x[i] = v;
 }
 
-template <typename T>
-__global__ void dq_finalize_kernel(const float* __restrict__ acc, T* __restrict__ dq, size_t n8) {
+// 8 elements per thread, from the contiguous accumulator to dQ in the I/O layout (the I/O type, or fp32)
+template <typename T, bool F32>
+__global__ void dq_finalize_kernel(const float* __restrict__ acc, void* __restrict__ dq, size_t n8, int N, int d,
+                                   IoLayout io) {
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n8) return;
   float4 a = reinterpret_cast<const float4*>(acc)[2 * i];
   float4 b = reinterpret_cast<const float4*>(acc)[2 * i + 1];
-  const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-  reinterpret_cast<uint4*>(dq)[i] = pack8<T>(f);
+  const size_t e = i * 8, row = e / d;
+  const long long off = io.row((long long)(row / N), (long long)(row % N)) + (long long)(e % d);
+  if constexpr (F32) {
+    reinterpret_cast<float4*>(static_cast<float*>(dq) + off)[0] = a;
+    reinterpret_cast<float4*>(static_cast<float*>(dq) + off)[1] = b;
+  } else {
+    const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    *reinterpret_cast<uint4*>(static_cast<T*>(dq) + off) = pack8<T>(f);
+  }
 }
 
 // ---------------------------------------------------------------- QK-norm backward
@@ -454,7 +464,7 @@ template <typename T, int D>
 __global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__ dy32, const T* dy16,
                                                        const T* __restrict__ x,
                                                        const float* __restrict__ rstd, const float* __restrict__ gamma,
-                                                       T* dx, float* __restrict__ gpart) {
+                                                       T* dx, float* __restrict__ gpart, IoLayout io, int N) {
   constexpr int kPer = D / 32;  // 4 or 2
   constexpr int kRows = 16;
   __shared__ float red[8][D];
@@ -470,10 +480,11 @@ __global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__
   float dy[kRows][kPer], xv[kRows][kPer], rs[kRows];
 #pragma unroll
   for (int rr = 0; rr < kRows; ++rr) {
-    const size_t off = (row0 + rr) * D + lane * kPer;
+    const size_t off = (row0 + rr) * D + lane * kPer;  // the contiguous fp32 dQ accumulator
+    const long long ioff = io.row((long long)((row0 + rr) / N), (long long)((row0 + rr) % N)) + lane * kPer;
     rs[rr] = rstd[row0 + rr];
     if constexpr (kPer == 4) {
-      const uint2 xu = *reinterpret_cast<const uint2*>(x + off);
+      const uint2 xu = *reinterpret_cast<const uint2*>(x + ioff);
       const float2 x0 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(&xu.x));
       const float2 x1 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(&xu.y));
       xv[rr][0] = x0.x; xv[rr][1] = x0.y; xv[rr][2] = x1.x; xv[rr][3] = x1.y;
@@ -481,19 +492,19 @@ __global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__
         const float4 f = *reinterpret_cast<const float4*>(dy32 + off);
         dy[rr][0] = f.x; dy[rr][1] = f.y; dy[rr][2] = f.z; dy[rr][3] = f.w;
       } else {
-        const uint2 du = *reinterpret_cast<const uint2*>(dy16 + off);
+        const uint2 du = *reinterpret_cast<const uint2*>(dy16 + ioff);
         const float2 d0 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(&du.x));
         const float2 d1 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(&du.y));
         dy[rr][0] = d0.x; dy[rr][1] = d0.y; dy[rr][2] = d1.x; dy[rr][3] = d1.y;
       }
     } else {
-      const float2 x0 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(x + off));
+      const float2 x0 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(x + ioff));
       xv[rr][0] = x0.x; xv[rr][1] = x0.y;
       if (dy32) {
         const float2 f = *reinterpret_cast<const float2*>(dy32 + off);
         dy[rr][0] = f.x; dy[rr][1] = f.y;
       } else {
-        const float2 d0 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(dy16 + off));
+        const float2 d0 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(dy16 + ioff));
         dy[rr][0] = d0.x; dy[rr][1] = d0.y;
       }
     }
@@ -518,7 +529,7 @@ __global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__
   }
 #pragma unroll
   for (int rr = 0; rr < kRows; ++rr) {
-    const size_t off = (row0 + rr) * D + lane * kPer;
+    const long long off = io.row((long long)((row0 + rr) / N), (long long)((row0 + rr) % N)) + lane * kPer;
     const float mean = dot[rr] * (1.f / D);
     typename Io<T>::T2 h[kPer / 2];
 #pragma unroll
@@ -573,36 +584,39 @@ __global__ void dgamma_stage2_kernel(const double* __restrict__ part2, float* __
     }                                      \
   } while (0)
 
-cudaError_t launch_colsum(const void* x, double* part, int BH, int N, int d, cudaStream_t s, NormIn nrm, bool fp16) {
+cudaError_t launch_colsum(const void* x, double* part, int BH, int N, int d, cudaStream_t s, NormIn nrm, bool fp16,
+                          IoLayout io) {
+  const int nT = N / kBlk;
   const unsigned grid = (unsigned)(BH * (N / kBlk));
   SAGE_IO_DISPATCH(fp16, {
     const IoT* xt = static_cast<const IoT*>(x);
     if (nrm.gamma) {
       if (d == 128)
-        colsum_kernel<IoT, 128, true><<<grid, 256, 0, s>>>(xt, part, nrm);
+        colsum_kernel<IoT, 128, true><<<grid, 256, 0, s>>>(xt, part, nrm, io, nT);
       else
-        colsum_kernel<IoT, 64, true><<<grid, 256, 0, s>>>(xt, part, nrm);
+        colsum_kernel<IoT, 64, true><<<grid, 256, 0, s>>>(xt, part, nrm, io, nT);
     } else {
       if (d == 128)
-        colsum_kernel<IoT, 128, false><<<grid, 256, 0, s>>>(xt, part, nrm);
+        colsum_kernel<IoT, 128, false><<<grid, 256, 0, s>>>(xt, part, nrm, io, nT);
       else
-        colsum_kernel<IoT, 64, false><<<grid, 256, 0, s>>>(xt, part, nrm);
+        colsum_kernel<IoT, 64, false><<<grid, 256, 0, s>>>(xt, part, nrm, io, nT);
     }
   });
   return cudaGetLastError();
 }
 
 cudaError_t launch_norm_bwd(const float* dy32, const void* dy16, const void* x, const float* rstd, const float* gamma,
-                            void* dx, float* gpart, float* dgamma, size_t rows, int d, cudaStream_t s, bool fp16) {
+                            void* dx, float* gpart, float* dgamma, size_t rows, int d, cudaStream_t s, bool fp16,
+                            IoLayout io, int N) {
   const unsigned nblk = (unsigned)(rows / kBlk);
   SAGE_IO_DISPATCH(fp16, {
     const IoT* dyt = static_cast<const IoT*>(dy16);
     const IoT* xt = static_cast<const IoT*>(x);
     IoT* dxt = static_cast<IoT*>(dx);
     if (d == 128)
-      norm_bwd_kernel<IoT, 128><<<nblk, 256, 0, s>>>(dy32, dyt, xt, rstd, gamma, dxt, gpart);
+      norm_bwd_kernel<IoT, 128><<<nblk, 256, 0, s>>>(dy32, dyt, xt, rstd, gamma, dxt, gpart, io, N);
     else
-      norm_bwd_kernel<IoT, 64><<<nblk, 256, 0, s>>>(dy32, dyt, xt, rstd, gamma, dxt, gpart);
+      norm_bwd_kernel<IoT, 64><<<nblk, 256, 0, s>>>(dy32, dyt, xt, rstd, gamma, dxt, gpart, io, N);
   });
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -627,7 +641,8 @@ cudaError_t launch_blockmean(const double* part, float* mu_q, int BH, int N, int
   return cudaGetLastError();
 }
 
-cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int d, cudaStream_t s, bool fp16) {
+cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int d, cudaStream_t s, bool fp16,
+                            IoLayout io) {
   int T = N / kBlk;
   dim3 grid((unsigned)(BH * T), (unsigned)njobs);
   bool qkn = false;
@@ -635,51 +650,52 @@ cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int
   SAGE_IO_DISPATCH(fp16, {
     if (qkn) {
       if (d == 128)
-        quantize_kernel<IoT, 128, true><<<grid, 256, 0, s>>>(jobs, T);
+        quantize_kernel<IoT, 128, true><<<grid, 256, 0, s>>>(jobs, T, io);
       else
-        quantize_kernel<IoT, 64, true><<<grid, 256, 0, s>>>(jobs, T);
+        quantize_kernel<IoT, 64, true><<<grid, 256, 0, s>>>(jobs, T, io);
     } else {
       if (d == 128)
-        quantize_kernel<IoT, 128, false><<<grid, 256, 0, s>>>(jobs, T);
+        quantize_kernel<IoT, 128, false><<<grid, 256, 0, s>>>(jobs, T, io);
       else
-        quantize_kernel<IoT, 64, false><<<grid, 256, 0, s>>>(jobs, T);
+        quantize_kernel<IoT, 64, false><<<grid, 256, 0, s>>>(jobs, T, io);
     }
   });
   return cudaGetLastError();
 }
 
 cudaError_t launch_qsmooth_bias(const void* k, const float* mu_k, const float* mu_q, float* bias, int BH, int N, int d,
-                                cudaStream_t s, NormIn nrm, bool fp16) {
+                                cudaStream_t s, NormIn nrm, bool fp16, IoLayout io) {
   const int T = N / kBlk;
   dim3 grid((unsigned)(BH * T), (unsigned)((T + kBiasI - 1) / kBiasI));
   SAGE_IO_DISPATCH(fp16, {
     const IoT* kt = static_cast<const IoT*>(k);
     if (d == 128)
-      qsmooth_bias_kernel<IoT, 128><<<grid, 128, 0, s>>>(kt, mu_k, mu_q, bias, N, nrm);
+      qsmooth_bias_kernel<IoT, 128><<<grid, 128, 0, s>>>(kt, mu_k, mu_q, bias, N, nrm, io);
     else
-      qsmooth_bias_kernel<IoT, 64><<<grid, 128, 0, s>>>(kt, mu_k, mu_q, bias, N, nrm);
+      qsmooth_bias_kernel<IoT, 64><<<grid, 128, 0, s>>>(kt, mu_k, mu_q, bias, N, nrm, io);
   });
   return cudaGetLastError();
 }
 
 cudaError_t launch_bwd_prep(const void* o, const void* dO, const float* lse, float* delta, float* l2, int8_t* do_q,
                             float* do_scale, float* dq_acc, int BH, int N, int d, cudaStream_t s, unsigned* dq_flags,
-                            bool fp16, bool o_f32) {
+                            bool fp16, bool o_f32, IoLayout io) {
+  const int nT = N / kBlk;
   unsigned grid = (unsigned)(BH * (N / kBlk));
   SAGE_IO_DISPATCH(fp16, {
     const IoT* dot = static_cast<const IoT*>(dO);
     if (o_f32) {
       const float* ot = static_cast<const float*>(o);
       if (d == 128)
-        bwd_prep_kernel<IoT, float, 128><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
+        bwd_prep_kernel<IoT, float, 128><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags, io, nT);
       else
-        bwd_prep_kernel<IoT, float, 64><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
+        bwd_prep_kernel<IoT, float, 64><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags, io, nT);
     } else {
       const IoT* ot = static_cast<const IoT*>(o);
       if (d == 128)
-        bwd_prep_kernel<IoT, IoT, 128><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
+        bwd_prep_kernel<IoT, IoT, 128><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags, io, nT);
       else
-        bwd_prep_kernel<IoT, IoT, 64><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags);
+        bwd_prep_kernel<IoT, IoT, 64><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags, io, nT);
     }
   });
   return cudaGetLastError();
@@ -690,10 +706,15 @@ cudaError_t launch_fill(float* x, size_t n, float v, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_dq_finalize(const float* dq_acc, void* dq, size_t n, cudaStream_t s, bool fp16) {
-  size_t n8 = n / 8;
-  SAGE_IO_DISPATCH(fp16, dq_finalize_kernel<IoT><<<(unsigned)((n8 + 255) / 256), 256, 0, s>>>(
-                             dq_acc, static_cast<IoT*>(dq), n8));
+cudaError_t launch_dq_finalize(const float* dq_acc, void* dq, int BH, int N, int d, cudaStream_t s, bool fp16,
+                               IoLayout io, bool f32) {
+  const size_t n8 = (size_t)BH * N * d / 8;
+  const unsigned grid = (unsigned)((n8 + 255) / 256);
+  if (f32) {
+    dq_finalize_kernel<float, true><<<grid, 256, 0, s>>>(dq_acc, dq, n8, N, d, io);
+    return cudaGetLastError();
+  }
+  SAGE_IO_DISPATCH(fp16, dq_finalize_kernel<IoT, false><<<grid, 256, 0, s>>>(dq_acc, dq, n8, N, d, io));
   return cudaGetLastError();
 }
 

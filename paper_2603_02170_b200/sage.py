@@ -29,7 +29,8 @@ SYMBOLS = ("sage_ctx_bytes", "sage_workspace_bytes", "sage_params_tag", "sage_fw
 
 class SageParams(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("heads", ctypes.c_int32), ("seqlen", ctypes.c_int32),
-                ("head_dim", ctypes.c_int32), ("flags", ctypes.c_uint32), ("softmax_scale", ctypes.c_float)]
+                ("head_dim", ctypes.c_int32), ("flags", ctypes.c_uint32), ("softmax_scale", ctypes.c_float),
+                ("stride_b", ctypes.c_int64), ("stride_h", ctypes.c_int64), ("stride_n", ctypes.c_int64)]
 
 
 class SageCtxDesc(ctypes.Structure):
@@ -105,12 +106,14 @@ def _check(status, what):
 
 def make_params(batch, heads, seqlen, head_dim, causal=False, k_smooth=True, q_smooth=False, softmax_scale=None,
                 p_u8=False, qk_norm=False, deterministic=False, p_colscale=False, fine_bwd=False, fp16=False,
-                fp32_out=False, pv_fp8=False):
+                fp32_out=False, pv_fp8=False, strides=None):
     flags = (SAGE_CAUSAL if causal else 0) | (SAGE_K_SMOOTH if k_smooth else 0) | (SAGE_Q_SMOOTH if q_smooth else 0) | \
         (SAGE_P_U8 if p_u8 else 0) | (SAGE_QK_NORM if qk_norm else 0) | (SAGE_DETERMINISTIC if deterministic else 0) | \
         (SAGE_P_COLSCALE if p_colscale else 0) | (SAGE_FINE_BWD if fine_bwd else 0) | (SAGE_FP16 if fp16 else 0) | \
         (SAGE_FP32_OUT if fp32_out else 0) | (SAGE_PV_FP8 if pv_fp8 else 0)
-    return SageParams(batch, heads, seqlen, head_dim, flags, 0.0 if softmax_scale is None else softmax_scale)
+    sb, sh, sn = (0, 0, 0) if strides is None else strides
+    return SageParams(batch, heads, seqlen, head_dim, flags, 0.0 if softmax_scale is None else softmax_scale,
+                      sb, sh, sn)
 
 
 def _ptr(t):
@@ -124,30 +127,60 @@ def _stream(stream, device=None):
 
 
 def _check_io(*ts):
-    """All tensors contiguous CUDA [B, H, N, d] of one I/O dtype: bf16, or fp16 (SAGE_FP16)."""
+    """CUDA [B, H, N, d] tensors of one I/O dtype (bf16, or fp16 with SAGE_FP16), shape and device."""
     ref = ts[0]
     for t in ts:
-        if not (t.is_cuda and t.dtype in (torch.bfloat16, torch.float16) and t.is_contiguous() and t.dim() == 4):
-            raise SageError("tensors must be contiguous CUDA bf16 or fp16 [B, H, N, d]")
+        if not (t.is_cuda and t.dtype in (torch.bfloat16, torch.float16) and t.dim() == 4):
+            raise SageError("tensors must be CUDA bf16 or fp16 [B, H, N, d]")
         if t.shape != ref.shape or t.device != ref.device or t.dtype != ref.dtype:
             raise SageError("shape/device/dtype mismatch")
 
 
-def _check_out(t, shape, dtype, device, what):
-    """A caller-provided output: contiguous, of the expected shape, dtype and device."""
-    if not (t.is_cuda and t.is_contiguous() and tuple(t.shape) == tuple(shape) and t.dtype == dtype
-            and t.device == device):
-        raise SageError(f"{what}: expected a contiguous {dtype} {tuple(shape)} tensor on {device}, got "
-                        f"{t.dtype} {tuple(t.shape)} on {t.device}")
+def _layout_ok(t):
+    """The library's strided I/O layout: d contiguous, the other strides multiples of 8 elements, the token
+    stride >= d, and a 16-byte aligned base."""
+    sb, sh, sn, sd = t.stride()
+    return sd == 1 and sn >= t.shape[3] and sb % 8 == 0 and sh % 8 == 0 and sn % 8 == 0 and t.data_ptr() % 16 == 0
+
+
+def _io_layout(*ts):
+    """(strides for sage_params or None, the tensors): ts share one layout the library can address directly
+    (no copy), else all are made contiguous."""
+    st = ts[0].stride()
+    if all(t.stride() == st for t in ts) and all(_layout_ok(t) for t in ts):
+        B, H, N, d = ts[0].shape
+        if st == (H * N * d, N * d, d, 1):
+            return None, ts
+        return (st[0], st[1], st[2]), ts
+    return None, tuple(t.contiguous() for t in ts)
+
+
+def _to_layout(t, ref_stride):
+    """t in the given [B, H, N, d] element strides (a copy only if it differs)."""
+    if t.stride() == tuple(ref_stride):
+        return t
+    out = torch.empty_strided(t.shape, ref_stride, dtype=t.dtype, device=t.device)
+    out.copy_(t)
+    return out
+
+
+def _check_out(t, shape, dtype, device, what, stride=None):
+    """A caller-provided output: of the expected shape, dtype, device and strides (contiguous by default)."""
+    ok_stride = t.is_contiguous() if stride is None else tuple(t.stride()) == tuple(stride)
+    if not (t.is_cuda and ok_stride and tuple(t.shape) == tuple(shape) and t.dtype == dtype and t.device == device):
+        raise SageError(f"{what}: expected a {dtype} {tuple(shape)} tensor (strides {stride or 'contiguous'}) on "
+                        f"{device}, got {t.dtype} {tuple(t.shape)} strides {tuple(t.stride())} on {t.device}")
 
 
 class SageCtx:
     """Forward->backward state (Alg. 2 inputs): the caller-owned ctx buffer, the params it was
     produced under and the params tag sage_fwd wrote (sage_bwd rejects a ctx from other params)."""
 
-    def __init__(self, params, ctx, shape):
+    def __init__(self, params, ctx, shape, io_stride=None):
         self.params, self.buf, self.shape = params, ctx, shape
         self.desc = SageCtxDesc(ctx.data_ptr(), ctx.numel(), 0)
+        B, H, N, d = shape
+        self.io_stride = tuple(io_stride) if io_stride is not None else (H * N * d, N * d, d, 1)
 
     @property
     def out_dtype(self):
@@ -229,24 +262,26 @@ def forward(q, k, v, causal=False, k_smooth=True, q_smooth=False, softmax_scale=
     (SAGE_FP32_OUT); pv_fp8: the forward's P^V^ in FP8 E4M3 (SAGE_PV_FP8).  The backward inherits them
     through the ctx."""
     _check_io(q, k, v)
+    strides, (q, k, v) = _io_layout(q, k, v)
     B, H, N, d = q.shape
     dev = q.device
     p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8, deterministic=deterministic,
                     p_colscale=p_colscale, fine_bwd=fine_bwd, fp16=q.dtype == torch.float16, fp32_out=fp32_out,
-                    pv_fp8=pv_fp8)
+                    pv_fp8=pv_fp8, strides=strides)
     nctx = lib().sage_ctx_bytes(ctypes.byref(p))
     if nctx == 0:
         raise SageError(f"unsupported shape/flags {tuple(q.shape)} (N % 128 == 0, d in {{64, 128}})")
     with torch.cuda.device(dev):
-        o = torch.empty(q.shape, dtype=_out_dtype(q.dtype, fp32_out), device=dev) if out is None else out
-        _check_out(o, q.shape, _out_dtype(q.dtype, fp32_out), dev, "out")
+        o = torch.empty_strided(q.shape, q.stride(), dtype=_out_dtype(q.dtype, fp32_out), device=dev) \
+            if out is None else out
+        _check_out(o, q.shape, _out_dtype(q.dtype, fp32_out), dev, "out", q.stride())
         lse = torch.empty((B, H, N), dtype=torch.float32, device=dev) if lse is None else lse
         _check_out(lse, (B, H, N), torch.float32, dev, "lse")
         ctxb = torch.empty(nctx, dtype=torch.uint8, device=dev) if ctx is None else ctx
         if ctxb.device != dev or ctxb.numel() < nctx:
             raise SageError("ctx buffer too small or on another device")
         ws = _ws.get(p, False, dev, stream) if workspace is None else workspace
-        c = SageCtx(p, ctxb, (B, H, N, d))
+        c = SageCtx(p, ctxb, (B, H, N, d), q.stride())
         _check(lib().sage_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), ctypes.byref(c.desc),
                               _ptr(ws), ws.numel(), _stream(stream, dev)), "sage_fwd")
     return o, lse, c
@@ -262,14 +297,17 @@ def backward(ctx, v, o, lse, do, dq=None, dk=None, dv=None, workspace=None, stre
     if (do.dtype == torch.float16) != bool(ctx.params.flags & SAGE_FP16):
         raise SageError("the backward's dtype differs from the forward's")
     B, H, N, d = ctx.shape
-    _check_out(o, ctx.shape, ctx.out_dtype, dev, "o")
+    st = ctx.io_stride
+    _check_out(o, ctx.shape, ctx.out_dtype, dev, "o", st)
     _check_out(lse, (B, H, N), torch.float32, dev, "lse")
+    v, do = _to_layout(v, st), _to_layout(do, st)  # the forward's layout (a copy only if it differs)
     with torch.cuda.device(dev):
-        dq = torch.empty(ctx.shape, dtype=ctx.out_dtype, device=dev) if dq is None else dq
-        dk = torch.empty(ctx.shape, dtype=ctx.out_dtype, device=dev) if dk is None else dk
-        dv = torch.empty(ctx.shape, dtype=ctx.out_dtype, device=dev) if dv is None else dv
+        mk = lambda: torch.empty_strided(ctx.shape, st, dtype=ctx.out_dtype, device=dev)
+        dq = mk() if dq is None else dq
+        dk = mk() if dk is None else dk
+        dv = mk() if dv is None else dv
         for t, n in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
-            _check_out(t, ctx.shape, ctx.out_dtype, dev, n)
+            _check_out(t, ctx.shape, ctx.out_dtype, dev, n, st)
         ws = _ws.get(ctx.params, True, dev, stream) if workspace is None else workspace
         _check(lib().sage_bwd(ctypes.byref(ctx.params), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), ctypes.byref(ctx.desc),
                               _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream(stream, dev)), "sage_bwd")
@@ -287,26 +325,27 @@ def forward_qknorm(xq, xk, v, gamma_q, gamma_k, eps=1e-6, causal=False, k_smooth
     """sage_fwd_qknorm: QK-norm fused in front of Alg. 1.  xq, xk: the pre-norm bf16
     [B, H, N, d]; gamma_q, gamma_k: fp32 [d].  Returns (o, lse, SageCtx)."""
     _check_io(xq, xk, v)
+    strides, (xq, xk, v) = _io_layout(xq, xk, v)
     B, H, N, d = xq.shape
     dev = xq.device
     _check_gamma(gamma_q, d, dev)
     _check_gamma(gamma_k, d, dev)
     p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8, qk_norm=True,
                     deterministic=deterministic, p_colscale=p_colscale, fine_bwd=fine_bwd,
-                    fp16=xq.dtype == torch.float16)
+                    fp16=xq.dtype == torch.float16, strides=strides)
     nctx = lib().sage_ctx_bytes(ctypes.byref(p))
     if nctx == 0:
         raise SageError(f"unsupported shape/flags {tuple(xq.shape)}")
     with torch.cuda.device(dev):
-        o = torch.empty_like(xq) if out is None else out
-        _check_out(o, xq.shape, xq.dtype, dev, "out")
+        o = torch.empty_strided(xq.shape, xq.stride(), dtype=xq.dtype, device=dev) if out is None else out
+        _check_out(o, xq.shape, xq.dtype, dev, "out", xq.stride())
         lse = torch.empty((B, H, N), dtype=torch.float32, device=dev) if lse is None else lse
         _check_out(lse, (B, H, N), torch.float32, dev, "lse")
         ctxb = torch.empty(nctx, dtype=torch.uint8, device=dev) if ctx is None else ctx
         if ctxb.device != dev or ctxb.numel() < nctx:
             raise SageError("ctx buffer too small or on another device")
         ws = _ws.get(p, False, dev, stream) if workspace is None else workspace
-        c = SageCtx(p, ctxb, (B, H, N, d))
+        c = SageCtx(p, ctxb, (B, H, N, d), xq.stride())
         _check(lib().sage_fwd_qknorm(ctypes.byref(p), _ptr(xq), _ptr(xk), _ptr(v), _ptr(gamma_q), _ptr(gamma_k),
                                      float(eps), _ptr(o), _ptr(lse), ctypes.byref(c.desc), _ptr(ws), ws.numel(),
                                      _stream(stream, dev)), "sage_fwd_qknorm")
@@ -320,18 +359,20 @@ def backward_qknorm(ctx, xq, xk, gamma_q, gamma_k, v, o, lse, do, out=None, work
     dev = do.device
     if tuple(do.shape) != tuple(ctx.shape) or ctx.buf.device != dev:
         raise SageError("backward_qknorm: tensors do not match the forward's ctx")
+    st = ctx.io_stride
+    xq, xk, v, o, do = (_to_layout(t, st) for t in (xq, xk, v, o, do))
     _check_gamma(gamma_q, d, dev)
     _check_gamma(gamma_k, d, dev)
     B, H, N, _ = ctx.shape
     _check_out(lse, (B, H, N), torch.float32, dev, "lse")
     with torch.cuda.device(dev):
         if out is None:
-            out = (torch.empty_like(do), torch.empty_like(do), torch.empty_like(do),
-                   torch.empty(d, dtype=torch.float32, device=dev),
+            mk = lambda: torch.empty_strided(ctx.shape, st, dtype=do.dtype, device=dev)
+            out = (mk(), mk(), mk(), torch.empty(d, dtype=torch.float32, device=dev),
                    torch.empty(d, dtype=torch.float32, device=dev))
         dxq, dxk, dv, dgq, dgk = out
         for t, n in ((dxq, "dxq"), (dxk, "dxk"), (dv, "dv")):
-            _check_out(t, ctx.shape, do.dtype, dev, n)
+            _check_out(t, ctx.shape, do.dtype, dev, n, st)
         _check_gamma(dgq, d, dev)
         _check_gamma(dgk, d, dev)
         ws = _ws.get(ctx.params, True, dev, stream) if workspace is None else workspace
@@ -371,8 +412,7 @@ class SageAttentionFn(torch.autograd.Function):
 
     @staticmethod
     def forward(fctx, q, k, v, causal, k_smooth, q_smooth, softmax_scale):
-        o, lse, c = forward(q.contiguous(), k.contiguous(), v.contiguous(), causal, k_smooth, q_smooth,
-                            softmax_scale)
+        o, lse, c = forward(q, k, v, causal, k_smooth, q_smooth, softmax_scale)
         fctx.sage = c
         fctx.save_for_backward(v, o, lse)
         return o
@@ -380,7 +420,7 @@ class SageAttentionFn(torch.autograd.Function):
     @staticmethod
     def backward(fctx, do):
         v, o, lse = fctx.saved_tensors
-        dq, dk, dv = backward(fctx.sage, v, o, lse, do.contiguous())
+        dq, dk, dv = backward(fctx.sage, v, o, lse, do)
         return dq, dk, dv, None, None, None, None
 
 

@@ -60,10 +60,24 @@ def test_params_tag(L):
               make_params(2, 3, 384, 64, causal=True), make_params(2, 3, 256, 128, causal=True),
               make_params(2, 3, 256, 64), make_params(2, 3, 256, 64, causal=True, q_smooth=True),
               make_params(2, 3, 256, 64, causal=True, softmax_scale=0.2),
-              make_params(2, 3, 256, 64, causal=True, p_u8=True), make_params(2, 3, 256, 64, causal=True, fp32_out=True)]
+              make_params(2, 3, 256, 64, causal=True, p_u8=True), make_params(2, 3, 256, 64, causal=True, fp32_out=True),
+              make_params(2, 3, 256, 64, causal=True, strides=(256 * 3 * 64, 64, 3 * 64))]
     tags = {L.sage_params_tag(ctypes.byref(o)) for o in others}
     assert t0 not in tags and len(tags) == len(others)
     assert L.sage_params_tag(ctypes.byref(make_params(1, 1, 100, 64))) == 0
+
+
+def test_stride_validation(L):
+    """sage_params strides (S:8(b) layouts): all zero = contiguous; otherwise multiples of 8 elements with the
+    token stride >= d; the ctx / workspace sizes do not depend on the I/O layout (internal buffers are
+    contiguous)."""
+    from paper_2603_02170_b200.sage import make_params
+    B, H, N, d = 2, 3, 256, 64
+    n0 = L.sage_ctx_bytes(ctypes.byref(make_params(B, H, N, d)))
+    bshd = (N * H * d, d, H * d)  # a [B, N, H, d] tensor viewed as [B, H, N, d]
+    assert L.sage_ctx_bytes(ctypes.byref(make_params(B, H, N, d, strides=bshd))) == n0
+    for bad in ((N * H * d, d, H * d + 4), (N * H * d, d, 32), (N * H * d, 0, H * d), (-8, d, H * d)):
+        assert L.sage_ctx_bytes(ctypes.byref(make_params(B, H, N, d, strides=bad))) == 0, bad
 
 
 def test_error_paths_do_not_launch(L):

@@ -632,3 +632,47 @@ def test_pv_fp8_parity(B, H, N, d, causal, ks, qs, recipe):
     b = oracle.bwd(sel(q), sel(k), sel(v), round_bf16(f["o"]), sel(do), f["lse"], **kw)
     gpu = dict(o=o, lse=lse, dq=dq, dk=dk, dv=dv)
     _assert_ok(_compare(gpu, f, b, heads, B, H, N, d), ("pv_fp8", B, H, N, d, causal, qs))
+
+
+# ------------------------------------------------------------------ strided I/O layouts (sage_params strides)
+@pytest.mark.parametrize("d,causal,qs", [(64, True, False), (128, False, True), (128, True, False)])
+def test_strided_bshd_layout(d, causal, qs):
+    """Q, K, V, dO given as [B, N, H, d] tensors viewed as [B, H, N, d] (no copy: the library addresses rows
+    through sage_params strides, 4-D TMA maps for V and dO): O, L, dK, dV bitwise identical to the contiguous
+    run, dQ within its fp32 reduction-order noise, and the outputs come back in the inputs' layout."""
+    B, H, N = 2, 2, 384
+    q, k, v, do = make_inputs(B, H, N, d, "outlier_kq", seed=1600 + d)
+    dev = "cuda"
+    cont = [t.to(dev) for t in (q, k, v, do)]
+    strided = [t.transpose(1, 2).contiguous().to(dev).transpose(1, 2) for t in (q, k, v, do)]
+    assert not strided[0].is_contiguous()
+    res = []
+    for qd, kd, vd, dod in (cont, strided):
+        o, lse, ctx = sage.forward(qd, kd, vd, causal=causal, q_smooth=qs)
+        dq, dk, dv = sage.backward(ctx, vd, o, lse, dod)
+        torch.cuda.synchronize()
+        res.append((o, lse, dq, dk, dv, ctx))
+    (o0, l0, dq0, dk0, dv0, c0), (o1, l1, dq1, dk1, dv1, c1) = res
+    assert c1.params.stride_n == H * d and o1.stride() == strided[0].stride() and dq1.stride() == strided[0].stride()
+    assert torch.equal(o0, o1) and torch.equal(l0, l1) and torch.equal(dk0, dk1) and torch.equal(dv0, dv1)
+    assert rel_l2(f64(dq0), f64(dq1)) < 1e-4
+
+
+def test_strided_qknorm_and_fp32_out():
+    """The strided layout through the fused QK-norm entry points and with SAGE_FP32_OUT (dQ then goes through
+    the workspace accumulator and K5 into the strided fp32 output)."""
+    B, H, N, d = 1, 2, 256, 128
+    xq, xk, v, do, gq, gk = _qkn_inputs(B, H, N, d, seed=1700)
+    dev = "cuda"
+    gqd, gkd = gq.to(dev), gk.to(dev)
+    outs = []
+    for tr in (False, True):
+        ts = [t.to(dev) if not tr else t.transpose(1, 2).contiguous().to(dev).transpose(1, 2) for t in (xq, xk, v, do)]
+        o, lse, ctx = sage.forward_qknorm(ts[0], ts[1], ts[2], gqd, gkd, 1e-6, causal=True)
+        g = sage.backward_qknorm(ctx, ts[0], ts[1], gqd, gkd, ts[2], o, lse, ts[3])
+        of, lf, cf = sage.forward(ts[0], ts[1], ts[2], causal=True, fp32_out=True)
+        gf = sage.backward(cf, ts[2], of, lf, ts[3])
+        torch.cuda.synchronize()
+        outs.append((o, lse) + tuple(g) + (of, lf) + tuple(gf))
+    for a, b in zip(outs[0], outs[1]):  # dQ / dX_q and dgamma see the fp32 reduction order: tolerance
+        assert rel_l2(f64(a), f64(b)) < 1e-4, (a.shape, rel_l2(f64(a), f64(b)))
