@@ -807,6 +807,7 @@ if (cm) {
     const int r = (warp % 4) * 32 + lane;  // TMEM lane: key row (dV, dK) or query row (dQ)
     const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
     const float sk = k_scale[(size_t)bh * T + j];
+    const long long orow = io.row(bh, (long long)j * kBlk + r);  // dK, dV in the I/O layout
     constexpr int kRegV = kAlias ? 1 : D;  // dV_j in registers (d=64) or in TMEM (d=128)
     float dv_acc[kRegV];
     float dk_acc[D];
@@ -963,7 +964,6 @@ if (cm) {
       tc_fence_after();
     }
     // epilogue: dK_j, dV_j rows -> bf16
-    const long long orow = io.row(bh, (long long)j * kBlk + r);  // dK, dV in the I/O layout
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 32) {
       float vv[32];

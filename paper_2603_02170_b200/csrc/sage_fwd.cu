@@ -37,6 +37,9 @@ constexpr float kLog2_448 = 8.807354922057604f;
 #ifndef SAGE_K2_REGS
 #define SAGE_K2_REGS 216  // measured: 184 -> 216 takes C3 K2 0.966 -> 0.893 ms, C4 4.39 -> 4.35 ms
 #endif
+#ifndef SAGE_K2_PAIR
+#define SAGE_K2_PAIR 1  // d=128: pass 1 and the O update load two 32-column TMEM chunks per wait
+#endif                  // (measured: C3 K2 0.911 -> 0.877 ms, C4 4.44 -> 4.40; d=64 neutral, so off there)
 #ifndef SAGE_K2_POLY
 #define SAGE_K2_POLY 1
 #endif
@@ -237,6 +240,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     // ------------------------------------------------------------ softmax / correction (128 threads)
     const int r = threadIdx.x;  // query row within the block == TMEM lane
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    // this row's O in the I/O layout, formed before the tile loop (the strides are not live inside it)
+    const long long o_off = io.row(bh, (long long)i * kBlk + r);
     const float sq = q_scale[(size_t)bh * T + i];
     const float tau2 = tau * kLog2e;
     // P^ levels: 127, or 255 for the unsigned variant (SAGE_P_U8)
@@ -254,11 +259,17 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t tPV = tbuf(jj);
       const float2 f = make_float2(spv, spv);
       const bool rescale = __any_sync(0xffffffffu, alpha != 1.f);
+      constexpr int kPair = (SAGE_K2_PAIR && D == 128) ? 2 : 1;  // 32-column chunks per TMEM wait
 #pragma unroll
-      for (int c0 = 0; c0 < D; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(tPV + c0 + lane_off, v);
+      for (int cp = 0; cp < D; cp += 32 * kPair) {
+        uint32_t vv[kPair][32];
+#pragma unroll
+        for (int h = 0; h < kPair; ++h) tmem_ld32(tPV + cp + 32 * h + lane_off, vv[h]);
         tmem_wait_ld();
+#pragma unroll
+        for (int h = 0; h < kPair; ++h) {
+        const int c0 = cp + 32 * h;
+        uint32_t(&v)[32] = vv[h];
         if (FDUMPING && g_fdump.pv) {
           int32_t* dst = g_fdump.pv + (((size_t)bh * T + jj) * N + (size_t)i * kBlk + r) * D + c0;
 #pragma unroll
@@ -273,6 +284,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           acc = ffma2(pv, f, acc);
           oacc[c0 + e] = acc.x;
           oacc[c0 + e + 1] = acc.y;
+        }
         }
       }
       tc_fence_before();
@@ -309,18 +321,25 @@ __global__ void __launch_bounds__(kThreads, 2)
       float rm;
       if constexpr (!QSMOOTH) {
         int mx = INT_MIN;
+        constexpr int kPair1 = (SAGE_K2_PAIR && D == 128) ? 2 : 1;
 #pragma unroll
-        for (int c0 = 0; c0 < kBlk; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tbuf(j) + c0 + lane_off, v);
+        for (int cp = 0; cp < kBlk; cp += 32 * kPair1) {
+          uint32_t vv[kPair1][32];
+#pragma unroll
+          for (int h = 0; h < kPair1; ++h) tmem_ld32(tbuf(j) + cp + 32 * h + lane_off, vv[h]);
           tmem_wait_ld();
-          if (diag) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (c0 + e <= r) mx = max(mx, (int)v[e]);
-          } else {
+          for (int h = 0; h < kPair1; ++h) {
+            const int c0 = cp + 32 * h;
+            uint32_t(&v)[32] = vv[h];
+            if (diag) {
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) mx = max(mx, max((int)v[e], (int)v[e + 1]));
+              for (int e = 0; e < 32; ++e)
+                if (c0 + e <= r) mx = max(mx, (int)v[e]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; e += 2) mx = max(mx, max((int)v[e], (int)v[e + 1]));
+            }
           }
         }
         rm = __int2float_rn(mx) * c2;  // max commutes with the positive scale
@@ -442,13 +461,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     // epilogue: O = acc / l (Alg. 1 line 13), L = m + ln l (line 14, natural log)
     const float inv_l = l > 0.f ? 1.f / l : 0.f;
     if (f32out) {  // SAGE_FP32_OUT
-      float4* orow = reinterpret_cast<float4*>(static_cast<float*>(o_out) + io.row(bh, (long long)i * kBlk + r));
+      float4* orow = reinterpret_cast<float4*>(static_cast<float*>(o_out) + o_off);
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 4)
         orow[c0 / 4] = make_float4(oacc[c0] * inv_l, oacc[c0 + 1] * inv_l, oacc[c0 + 2] * inv_l, oacc[c0 + 3] * inv_l);
     } else {
       // O in the I/O type (bf16, or fp16 with SAGE_FP16): 8 values per 16-byte store
-      uint4* orow = reinterpret_cast<uint4*>(static_cast<uint16_t*>(o_out) + io.row(bh, (long long)i * kBlk + r));
+      uint4* orow = reinterpret_cast<uint4*>(static_cast<uint16_t*>(o_out) + o_off);
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 8) {
         uint32_t h[4];
