@@ -104,6 +104,10 @@ struct BwdSmem {
 #ifndef SAGE_K4_DKQ128
 #define SAGE_K4_DKQ128 1  // d=128: dK shares the dQ region (1) or dP's (0, round 1)
 #endif
+#ifndef SAGE_K4_DVDP
+#define SAGE_K4_DVDP 0  // d=128: the dV tile on dP's columns, so S_{i+1} goes out as soon as S_i is in
+                        // registers (1; C4 K4 +1.4%, C3 -1.6%: DESIGN.md 7.3), or on S's (0)
+#endif
 #ifndef SAGE_TRACE
 #define SAGE_TRACE 0
 #endif
@@ -276,7 +280,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS = tmem;
   const uint32_t tDP = tmem + 128;
-  const uint32_t tDV = kAlias ? tmem : tmem + 256;
+  constexpr bool kDvDp = kAlias && SAGE_K4_DKQ128 && SAGE_K4_DVDP;
+  const uint32_t tDV = kAlias ? (kDvDp ? tmem + 128 : tmem) : tmem + 256;
   // d=128: dK_i and then dQ_i take turns in the third region, so dP_{i+1} never waits for the dK drain
   constexpr bool kDkQ = kAlias && SAGE_K4_DKQ128;
   const uint32_t tDK = kAlias ? (kDkQ ? tmem + 256 : tmem + 128) : tmem + 256 + D;
@@ -487,6 +492,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             issue_dp(it + 1);
           }
+        } else if constexpr (kDvDp) {
+          // d=128 (SAGE_K4_DVDP): S_{i+1} goes out once S_i is in registers (s_free); dV_i lands on
+          // dP's columns (read by p_ready), so dP_{i+1} waits for the compute warps' dV drain.
+          if (more) {
+            mbar_wait(s_free, ph);
+            tc_fence_after();
+            issue_s(it + 1);
+          }
+          mbar_wait(p_ready, ph);
+          if (lane == 0) TR(17, it);
+          tc_fence_after();
+          issue_dv(it);
+          mbar_wait(ds_ready, ph);
+          if (it > 0) mbar_wait(dq_drained, pph);  // dQ_{i-1} drained out of the third region
+          if (lane == 0) TR(20, it);
+          tc_fence_after();
+          issue_dk(it);
+          if (more) {
+            mbar_wait(dv_drained, ph);
+            tc_fence_after();
+            issue_dp(it + 1);
+          }
+          mbar_wait(dkq_drained, ph);  // dK_i drained
+          tc_fence_after();
+          issue_dq(it);
         } else {
           // d=128: dV_i lands on S's columns (read by p_ready), so S_{i+1} waits until the compute
           // warps have drained dV_i; dP_{i+1} goes out right behind dV_i (dP_i was read by p_ready).
@@ -593,7 +623,7 @@ if (cm) {
 }
       if (threadIdx.x == 128) TR(18, it);
       tc_fence_before();
-      if constexpr (!kAlias) warp_arrive(s_free);  // S^T consumed: S_{i+1} may be issued
+      if constexpr (!kAlias || kDvDp) warp_arrive(s_free);  // S^T consumed: S_{i+1} may be issued
       if (diag) {  // causal: key r attends query q only if r <= q (reading A14)
 #pragma unroll
         for (int e = 0; e < 64; ++e)
