@@ -129,7 +129,7 @@ def fwd(q, k, v, *, causal=False, k_smooth=True, q_smooth=False, quant=True, blk
     dumped p8 is zero (the E4M3 P^ is not an integer); sv holds the E4M3 block scales amax/448."""
     q, k, v = _f64(q), _f64(k), _f64(v)
     BH, N, d = q.shape
-    T = N // blk
+    T = -(-N // blk)  # ceil: a ragged N has a short last block (reading A33)
     qsel = _sel(q_blocks, BH, T)
     flags = _flags(causal, k_smooth, q_smooth, quant, p_u8, pv_fp8=pv_fp8)
     out = dict(o=np.zeros((BH, N, d)), lse=np.zeros((BH, N)),
@@ -164,7 +164,7 @@ def bwd(q, k, v, o_stored, do, lse, *, causal=False, k_smooth=True, q_smooth=Fal
     computed for q_blocks and dK, dV for k_blocks (other rows stay zero), bitwise as in the full run."""
     q, k, v, o_stored, do, lse = map(_f64, (q, k, v, o_stored, do, lse))
     BH, N, d = q.shape
-    T = N // blk
+    T = -(-N // blk)  # ceil: a ragged N has a short last block (reading A33)
     if q_blocks is not None or k_blocks is not None:
         qsel, ksel = _sel(q_blocks or [], BH, T), _sel(k_blocks or [], BH, T)
     else:

@@ -22,7 +22,12 @@
  * may use it.
  *
  * Layout: every tensor is [BH][N][d] row-major (heads flattened), scales are
- * [BH][T] with T = N / blk, lse is [BH][N] in natural log.
+ * [BH][T] with T = ceil(N / blk), lse is [BH][N] in natural log.
+ *
+ * Ragged N (reading A33): when blk does not divide N the last block Q_{T-1} (and
+ * K_{T-1}, V_{T-1}, dO_{T-1}) holds the remaining N - (T-1) blk rows; every
+ * per-block statistic (psi scale, mu_Qi) is taken over the rows the block holds,
+ * and a tile's missing rows / columns are absent (no logits, P = dS = 0).
  */
 #include <math.h>
 #include <stdint.h>
@@ -155,17 +160,23 @@ double oracle_psi_token_row(const double *pt, int n, double rm_minus_m, int pmax
   return psi_token_row(pt, n, rm_minus_m, (double)pmax, q);
 }
 
+/* rows of block t (reading A33: the last block of a ragged N is short) */
+static int rows_in(int N, int blk, int t) {
+  int r = N - t * blk;
+  return r < blk ? r : blk;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Smoothing.  Column mean in double, in a fixed order: sequential
  * over the rows of each blk-row chunk, then sequential over chunks (A17);
  * rounded once to FP32 unless quant_off.                                     */
 static void column_mean(const double *x, int N, int d, int blk, int quant_off, double *mu) {
-  int T = N / blk;
+  int T = (N + blk - 1) / blk;
   for (int c = 0; c < d; ++c) {
     double total = 0.0;
     for (int t = 0; t < T; ++t) {
       double part = 0.0;
-      for (int r = 0; r < blk; ++r) part += x[(size_t)(t * blk + r) * d + c];
+      for (int r = 0; r < rows_in(N, blk, t); ++r) part += x[(size_t)(t * blk + r) * d + c];
       total += part;
     }
     double m = total / (double)N;
@@ -198,7 +209,7 @@ static void prep_free(head_prep *h) {
 }
 
 static void prep_head(head_prep *h, const double *q, const double *k, int N, int d, int blk, int flags) {
-  int T = N / blk, qo = (flags & ORC_QUANT_OFF) != 0;
+  int T = (N + blk - 1) / blk, qo = (flags & ORC_QUANT_OFF) != 0;
   size_t nd = (size_t)N * d;
   h->N = N; h->d = d; h->blk = blk; h->T = T; h->flags = flags;
   h->qs = malloc(nd * sizeof(double)); h->ks = malloc(nd * sizeof(double));
@@ -215,8 +226,9 @@ static void prep_head(head_prep *h, const double *q, const double *k, int N, int
   /* Q-smoothing: mu_Qi = mean_row(Q_i), block-wise (A12). */
   for (int t = 0; t < T; ++t) {
     double *mq = h->mu_q + (size_t)t * d;
-    if (flags & ORC_Q_SMOOTH) column_mean(q + (size_t)t * blk * d, blk, d, blk, qo, mq);
-    for (int r = 0; r < blk; ++r)
+    int nb = rows_in(N, blk, t);
+    if (flags & ORC_Q_SMOOTH) column_mean(q + (size_t)t * blk * d, nb, d, blk, qo, mq);
+    for (int r = 0; r < nb; ++r)
       for (int c = 0; c < d; ++c) {
         size_t e = (size_t)(t * blk + r) * d + c;
         h->qs[e] = smooth_sub(q[e], mq[c], qo);
@@ -233,15 +245,17 @@ static void prep_head(head_prep *h, const double *q, const double *k, int N, int
   /* Alg. 1 line 3: per-block psi of Q_i, K_j. */
   for (int t = 0; t < T; ++t) {
     size_t off = (size_t)t * blk * d;
-    psi_block(h->qs + off, blk * d, 1, qo, 127.0, h->q8 + off, &h->sq[t], h->qx + off);
-    psi_block(h->ks + off, blk * d, 1, qo, 127.0, h->k8 + off, &h->sk[t], h->kx + off);
+    int nbd = rows_in(N, blk, t) * d;
+    psi_block(h->qs + off, nbd, 1, qo, 127.0, h->q8 + off, &h->sq[t], h->qx + off);
+    psi_block(h->ks + off, nbd, 1, qo, 127.0, h->k8 + off, &h->sk[t], h->kx + off);
   }
 }
 
 /* S_ij = MM(Q^_i, K^_j) x s_Q x s_K (Alg. 1 line 7 / Alg. 2 line 5), times the
  * softmax scale tau (A6), plus tau*bias_i with Q-smoothing.  The
  * integer product accumulates in int32; |acc| <= d*127^2 < 2^31.
- * Masked entries (A14) are set to -INFINITY.                                  */
+ * Masked entries (A14), and the rows / columns a short last block lacks (A33),
+ * are set to -INFINITY.                                                      */
 static void s_tile(const head_prep *h, int i, int j, double tau, double *S) {
   int blk = h->blk, d = h->d, N = h->N, qo = (h->flags & ORC_QUANT_OFF) != 0;
   int causal = (h->flags & ORC_CAUSAL) != 0;
@@ -250,6 +264,10 @@ static void s_tile(const head_prep *h, int i, int j, double tau, double *S) {
     for (int n = 0; n < blk; ++n) {
       int gn = j * blk + n;
       double s;
+      if (gr >= N || gn >= N) {
+        S[(size_t)r * blk + n] = -INFINITY;
+        continue;
+      }
       if (qo) {
         double acc = 0.0;
         for (int c = 0; c < d; ++c) acc += h->qs[(size_t)gr * d + c] * h->ks[(size_t)gn * d + c];
@@ -289,10 +307,11 @@ static void fwd_head(const double *q, const double *k, const double *v, int N, i
   int pv8 = (flags & ORC_PV_FP8) && !qo;
   for (int t = 0; t < T; ++t) {
     size_t off = (size_t)t * blk * d;
+    int nbd = rows_in(N, blk, t) * d;
     if (pv8)
-      psi_block_e4m3(v + off, blk * d, vx + off, &sv[t]);   /* v8 (int8) stays zero in this mode */
+      psi_block_e4m3(v + off, nbd, vx + off, &sv[t]);   /* v8 (int8) stays zero in this mode */
     else
-      psi_block(v + off, blk * d, 1, qo, 127.0, v8 + off, &sv[t], vx + off);
+      psi_block(v + off, nbd, 1, qo, 127.0, v8 + off, &sv[t], vx + off);
   }
   double *S = malloc((size_t)blk * blk * sizeof(double));
   double *Pt = malloc((size_t)blk * blk * sizeof(double));
@@ -306,10 +325,11 @@ static void fwd_head(const double *q, const double *k, const double *v, int N, i
     if (qsel && !qsel[i]) continue;
     for (int r = 0; r < blk; ++r) { m[r] = -INFINITY; l[r] = 0.0; }
     memset(acc, 0, (size_t)blk * d * sizeof(double));
-    int jmax = causal ? i : T - 1;
+    int jmax = causal ? i : T - 1, nbi = rows_in(N, blk, i);
     for (int j = 0; j <= jmax; ++j) {
+      int nbj = rows_in(N, blk, j);   /* keys this block holds (A33); P~ is 0 beyond them */
       s_tile(&h, i, j, tau, S);
-      for (int r = 0; r < blk; ++r) {
+      for (int r = 0; r < nbi; ++r) {
         const double *Sr = S + (size_t)r * blk;
         double rm = -INFINITY;
         for (int n = 0; n < blk; ++n) if (Sr[n] > rm) rm = Sr[n];
@@ -324,29 +344,29 @@ static void fwd_head(const double *q, const double *k, const double *v, int N, i
         if (qo) {
           for (int c = 0; c < d; ++c) {
             double pv = 0.0;
-            for (int n = 0; n < blk; ++n) pv += Pr[n] * vx[(size_t)(j * blk + n) * d + c];
+            for (int n = 0; n < nbj; ++n) pv += Pr[n] * vx[(size_t)(j * blk + n) * d + c];
             ar[c] = alpha * ar[c] + pv;
           }
         } else if (pv8) {
           /* line 9 in FP8: s_P = e^{rowmax - m}/448, P^ = e4m3(P~ / s_P); line 10: exact sum of E4M3 products */
           double sp = exp(rm - mnew) / 448.0;
           for (int n = 0; n < blk; ++n) Pq[n] = e4m3_rne(Pr[n] / sp);
-          if (p8o) for (int n = 0; n < blk; ++n) p8o[(size_t)(i * blk + r) * N + (size_t)j * blk + n] = 0;
+          if (p8o) for (int n = 0; n < nbj; ++n) p8o[(size_t)(i * blk + r) * N + (size_t)j * blk + n] = 0;
           if (spo) spo[(size_t)(i * blk + r) * T + j] = sp;
           for (int c = 0; c < d; ++c) {
             double pv = 0.0;
-            for (int n = 0; n < blk; ++n) pv += Pq[n] * vx[(size_t)(j * blk + n) * d + c];
+            for (int n = 0; n < nbj; ++n) pv += Pq[n] * vx[(size_t)(j * blk + n) * d + c];
             ar[c] = alpha * ar[c] + pv * sp * sv[j];
           }
         } else {
           int16_t *Phr = Ph + (size_t)r * blk;
           double sp = psi_token_row(Pr, blk, rm - mnew, pmax, Phr);   /* line 9 */
           /* optional dumps (test infrastructure: Tier-C of the forward), P^ [N q][N kv], s_P [N q][T] */
-          if (p8o) for (int n = 0; n < blk; ++n) p8o[(size_t)(i * blk + r) * N + (size_t)j * blk + n] = (uint8_t)Phr[n];
+          if (p8o) for (int n = 0; n < nbj; ++n) p8o[(size_t)(i * blk + r) * N + (size_t)j * blk + n] = (uint8_t)Phr[n];
           if (spo) spo[(size_t)(i * blk + r) * T + j] = sp;
           for (int c = 0; c < d; ++c) {                            /* line 10 */
             int32_t pv = 0;
-            for (int n = 0; n < blk; ++n)
+            for (int n = 0; n < nbj; ++n)
               pv += (int32_t)Phr[n] * (int32_t)v8[(size_t)(j * blk + n) * d + c];
             ar[c] = alpha * ar[c] + (double)pv * sp * sv[j];
           }
@@ -354,7 +374,7 @@ static void fwd_head(const double *q, const double *k, const double *v, int N, i
         m[r] = mnew;
       }
     }
-    for (int r = 0; r < blk; ++r) {              /* lines 13-14 */
+    for (int r = 0; r < nbi; ++r) {              /* lines 13-14 */
       size_t gr = (size_t)i * blk + r;
       for (int c = 0; c < d; ++c) o[gr * d + c] = l[r] > 0.0 ? acc[(size_t)r * d + c] / l[r] : 0.0;
       lse[gr] = l[r] > 0.0 ? m[r] + log(l[r]) : -INFINITY;
@@ -382,8 +402,8 @@ int oracle_fwd_sel(int BH, int N, int d, int blk, int flags, double tau,
                    float *mu_k, float *mu_q, double *bias,
                    int8_t *q8, int8_t *k8, int8_t *v8, float *sq, float *sk, float *sv,
                    uint8_t *p8, double *sp) {
-  if (BH <= 0 || N <= 0 || d <= 0 || blk <= 0 || N % blk) return -1;
-  int T = N / blk;
+  if (BH <= 0 || N <= 0 || d <= 0 || blk <= 0) return -1;
+  int T = (N + blk - 1) / blk;
   size_t nd = (size_t)N * d;
 #pragma omp parallel for schedule(dynamic, 1)
   for (int b = 0; b < BH; ++b) {
@@ -436,7 +456,7 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
   double *sdo = malloc(T * sizeof(double));
   for (int t = 0; t < T; ++t) {
     size_t off = (size_t)t * blk * d;
-    psi_block(dO + off, blk * d, 1, qo, 127.0, do8 + off, &sdo[t], dox + off);
+    psi_block(dO + off, rows_in(N, blk, t) * d, 1, qo, 127.0, do8 + off, &sdo[t], dox + off);
   }
   double *S = malloc(bb * sizeof(double)), *P = malloc(bb * sizeof(double));
   double *dS = malloc(bb * sizeof(double)), *Px = malloc(bb * sizeof(double)), *dSx = malloc(bb * sizeof(double));
@@ -457,6 +477,8 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
     for (int i = causal ? j : 0; i < T; ++i) {
       int want_q = all || (qsel && qsel[i]), want_k = all || (ksel && ksel[j]);
       if (!want_q && !want_k) continue;
+      /* rows / columns this tile holds (A33); P = dS = 0 beyond them */
+      int nbi = rows_in(N, blk, i), nbj = rows_in(N, blk, j);
       /* line 5: S_ij recomputed from Q^, K^; P_ij = exp(S_ij - L_i). */
       s_tile(&h, i, j, tau, S);
       for (int r = 0; r < blk; ++r)
@@ -480,16 +502,16 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
         for (int n = 0; n < blk; ++n) spcol[n] = sp;
       }
       /* line 7: dV_j += MM(P^_ij^T, dO^_i) x s_P x s_dO. */
-      for (int n = 0; n < blk; ++n)
+      for (int n = 0; n < nbj; ++n)
         for (int c = 0; c < d; ++c) {
           double val;
           if (qo) {
             double a = 0.0;
-            for (int r = 0; r < blk; ++r) a += Px[(size_t)r * blk + n] * dox[(size_t)(i * blk + r) * d + c];
+            for (int r = 0; r < nbi; ++r) a += Px[(size_t)r * blk + n] * dox[(size_t)(i * blk + r) * d + c];
             val = a;
           } else {
             int32_t a = 0;
-            for (int r = 0; r < blk; ++r)
+            for (int r = 0; r < nbi; ++r)
               a += (int32_t)Px[(size_t)r * blk + n] * (int32_t)do8[(size_t)(i * blk + r) * d + c];
             val = (double)a * spcol[n] * sdo[i];
           }
@@ -500,6 +522,10 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
       for (int r = 0; r < blk; ++r)
         for (int n = 0; n < blk; ++n) {
           double a = 0.0;
+          if (r >= nbi || n >= nbj) {
+            dS[(size_t)r * blk + n] = 0.0;
+            continue;
+          }
           for (int c = 0; c < d; ++c) a += dO[(size_t)(i * blk + r) * d + c] * v[(size_t)(j * blk + n) * d + c];
           dS[(size_t)r * blk + n] = P[(size_t)r * blk + n] * (a - delta[i * blk + r]);
         }
@@ -520,8 +546,8 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
         for (int e = 0; e < blk; ++e) sq_row[e] = sk_col[e] = sds;
       }
       /* optional tile dumps (test infrastructure: Tier-C and fidelity reports), [N q][N kv] */
-      for (int r = 0; r < blk; ++r)
-        for (int n = 0; n < blk; ++n) {
+      for (int r = 0; r < nbi; ++r)
+        for (int n = 0; n < nbj; ++n) {
           size_t g = (size_t)(i * blk + r) * N + (size_t)j * blk + n, t = (size_t)r * blk + n;
           if (p8_out) p8_out[g] = (uint8_t)Px[t];
           if (ds8_out) ds8_out[g] = dSk8[t];  /* the dK operand (= the tile's dS^ unless ORC_DS_FINE) */
@@ -530,16 +556,16 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
       if (sp_out) sp_out[(size_t)i * T + j] = (float)sp;
       if (sds_out) sds_out[(size_t)i * T + j] = (float)sds;
       /* line 10: dQ_i += MM(dS^_ij, K^_j) x s_dS x s_K  (x tau, A6). */
-      for (int r = 0; r < blk; ++r)
+      for (int r = 0; r < nbi; ++r)
         for (int c = 0; c < d; ++c) {
           double val;
           if (qo) {
             double a = 0.0;
-            for (int n = 0; n < blk; ++n) a += dSx[(size_t)r * blk + n] * h.kx[(size_t)(j * blk + n) * d + c];
+            for (int n = 0; n < nbj; ++n) a += dSx[(size_t)r * blk + n] * h.kx[(size_t)(j * blk + n) * d + c];
             val = a * tau;
           } else {
             int32_t a = 0;
-            for (int n = 0; n < blk; ++n)
+            for (int n = 0; n < nbj; ++n)
               a += (int32_t)dSq8[(size_t)r * blk + n] * (int32_t)h.k8[(size_t)(j * blk + n) * d + c];
             val = (double)a * sq_row[r] * h.sk[j] * tau;
           }
@@ -547,18 +573,18 @@ static void bwd_head(const double *q, const double *k, const double *v, const do
         }
       /* line 11: dK_j += MM(dS^_ij^T, Q^_i) x s_dS x s_Q  (x tau, A6);
        * with Q-smoothing also dK_bias = (dS^T 1) mu_Q^T  (A13). */
-      for (int n = 0; n < blk; ++n) {
+      for (int n = 0; n < nbj; ++n) {
         double colsum = 0.0;
-        for (int r = 0; r < blk; ++r) colsum += qo ? dSx[(size_t)r * blk + n] : (double)dSk8[(size_t)r * blk + n];
+        for (int r = 0; r < nbi; ++r) colsum += qo ? dSx[(size_t)r * blk + n] : (double)dSk8[(size_t)r * blk + n];
         for (int c = 0; c < d; ++c) {
           double val;
           if (qo) {
             double a = 0.0;
-            for (int r = 0; r < blk; ++r) a += dSx[(size_t)r * blk + n] * h.qx[(size_t)(i * blk + r) * d + c];
+            for (int r = 0; r < nbi; ++r) a += dSx[(size_t)r * blk + n] * h.qx[(size_t)(i * blk + r) * d + c];
             val = a * tau;
           } else {
             int32_t a = 0;
-            for (int r = 0; r < blk; ++r)
+            for (int r = 0; r < nbi; ++r)
               a += (int32_t)dSk8[(size_t)r * blk + n] * (int32_t)h.q8[(size_t)(i * blk + r) * d + c];
             val = (double)a * sk_col[n] * h.sq[i] * tau;
           }
@@ -583,8 +609,8 @@ int oracle_bwd_sel(int BH, int N, int d, int blk, int flags, double tau,
                    double *dq, double *dk, double *dv,
                    double *delta, int8_t *do8, float *sdo,
                    uint8_t *p8, float *sp, int8_t *ds8, float *sds, double *ds) {
-  if (BH <= 0 || N <= 0 || d <= 0 || blk <= 0 || N % blk) return -1;
-  int T = N / blk;
+  if (BH <= 0 || N <= 0 || d <= 0 || blk <= 0) return -1;
+  int T = (N + blk - 1) / blk;
   size_t nd = (size_t)N * d;
 #pragma omp parallel for schedule(dynamic, 1)
   for (int b = 0; b < BH; ++b) {

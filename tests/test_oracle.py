@@ -145,7 +145,7 @@ def test_ds_bound_appendix_b(orc):
 # --------------------------------------------------------------------------- tiled, quantisation off
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("smooth", ["none", "k", "qk"])
-@pytest.mark.parametrize("N,blk", [(64, 16), (64, 32), (96, 32), (128, 128)])
+@pytest.mark.parametrize("N,blk", [(64, 16), (64, 32), (96, 32), (128, 128), (80, 32), (50, 16), (33, 32)])
 def test_tiled_quant_off_equals_fpa(orc, causal, smooth, N, blk):
     """Alg. 1/2 with psi = identity == naive attention <= 1e-9.
     With smoothing this also pins: K-smoothing invariance, the
@@ -167,6 +167,48 @@ def test_tiled_quant_off_equals_fpa(orc, causal, smooth, N, blk):
     b = orc.bwd(q, k, v, f["o"], do, f["lse"], **kw)
     for name in ("dq", "dk", "dv"):
         assert rel_l2(ref[name], b[name]) <= 1e-9, name
+
+
+# --------------------------------------------------------------------------- ragged N (reading A33)
+@pytest.mark.parametrize("N,d", [(200, 64), (300, 128), (129, 64)])
+def test_ragged_causal_prefix(orc, N, d):
+    """A causal ragged-N run is the first N rows of the padded run: zero rows appended to Q, K, V and dO
+    change no block's psi scale (amax over zeros), and causal rows never see the later keys, so O, L, dQ and
+    dK of the first N rows are bit-identical; dV only through the P^ tile scales (padded queries)."""
+    rng = np.random.default_rng(N)
+    BH, Np = 2, -(-N // 128) * 128
+    q, k, v, do = (_rand(rng, BH, N, d) for _ in range(4))
+    pad = lambda x: np.concatenate([x, np.zeros((BH, Np - N, d))], 1)
+    f = orc.fwd(q, k, v, causal=True, k_smooth=False)
+    fp = orc.fwd(pad(q), pad(k), pad(v), causal=True, k_smooth=False)
+    np.testing.assert_array_equal(f["o"], fp["o"][:, :N])
+    np.testing.assert_array_equal(f["lse"], fp["lse"][:, :N])
+    np.testing.assert_array_equal(f["sq"], fp["sq"])
+    b = orc.bwd(q, k, v, f["o"], do, f["lse"], causal=True, k_smooth=False)
+    bp = orc.bwd(pad(q), pad(k), pad(v), fp["o"], pad(do), fp["lse"], causal=True, k_smooth=False)
+    np.testing.assert_array_equal(b["dq"], bp["dq"][:, :N])
+    np.testing.assert_array_equal(b["dk"], bp["dk"][:, :N])
+    assert rel_l2(bp["dv"][:, :N], b["dv"]) < 2e-3
+
+
+def test_ragged_block_statistics(orc):
+    """The short last block's statistics are over the rows it holds (A33): mu_K over all N rows, mu_Qi over
+    the block's rows, and s = fl32(amax / 127) over them."""
+    rng = np.random.default_rng(3)
+    N, d = 300, 64
+    q, k, v = (_rand(rng, 1, N, d) + 2.0 for _ in range(3))
+    out = orc.fwd(q, k, v, causal=False, k_smooth=True, q_smooth=True)
+    mu_k = np.array([math.fsum(k[0, :, c]) / N for c in range(d)], dtype=np.float32)
+    np.testing.assert_array_equal(out["mu_k"][0], mu_k)
+    last = q[0, 256:]
+    mu_q = np.array([math.fsum(last[:, c]) / 44 for c in range(d)], dtype=np.float32)
+    np.testing.assert_array_equal(out["mu_q"][0, 2], mu_q)
+    qsm = last.astype(np.float32) - mu_q
+    assert out["sq"][0, 2] == np.float32(np.float32(np.abs(qsm).max()) / np.float32(127))
+    ksm = k[0, 256:].astype(np.float32) - mu_k
+    assert out["sk"][0, 2] == np.float32(np.float32(np.abs(ksm).max()) / np.float32(127))
+    assert out["sv"][0, 2] == np.float32(np.float32(np.abs(v[0, 256:]).max()) / np.float32(127))
+    assert np.abs(out["q8"][0, 256:]).max() == 127 and out["o"].shape == (1, N, d)
 
 
 # --------------------------------------------------------------------------- tiled, quantised (the QO)
