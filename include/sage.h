@@ -20,8 +20,12 @@
  *
  * Conventions
  *   - Tensors Q, K, V, O, dO, dQ, dK, dV: bf16 (fp16 with SAGE_FP16), [B, H, N, d] with d innermost and the
- *     strides of sage_params (contiguous by default), 16-byte aligned device pointers on the current device.  N % 128 == 0, d in {64, 128}.  With
+ *     strides of sage_params (contiguous by default), 16-byte aligned device pointers on the current device.
+ *     1 <= N <= 32768, d in {64, 128}.  N need not be a multiple of 128: the last block of a head is then
+ *     short, with every per-block statistic taken over the rows it holds (reading A33).  With
  *     SAGE_FP32_OUT the outputs O, dQ, dK, dV are fp32 instead.
+ *   - The library's own buffers (ctx, workspace; the views below) pad every head to Np = 128 ceil(N/128)
+ *     rows; T = ceil(N/128) is the number of blocks.
  *   - lse: fp32 [B, H, N], natural log (Alg. 1 line 14).
  *   - Ownership: the caller allocates every buffer (device memory), including the
  *     forward->backward context `ctx` (sage_ctx_bytes) and the scratch workspace
@@ -50,7 +54,7 @@ extern "C" {
 
 typedef enum {
   SAGE_OK = 0,
-  SAGE_ERR_INVALID_VALUE = 1, /* null pointer, bad shape/flags, N % 128 != 0, d not in {64,128} */
+  SAGE_ERR_INVALID_VALUE = 1, /* null pointer, bad shape/flags, N outside [1, 32768], d not in {64,128} */
   SAGE_ERR_UNSUPPORTED = 2,   /* valid but not implemented combination */
   SAGE_ERR_MISALIGNED = 3,    /* a pointer is not 16-byte aligned */
   SAGE_ERR_WORKSPACE = 4,     /* ctx or workspace smaller than required */
@@ -72,7 +76,7 @@ enum {
   SAGE_DETERMINISTIC = 1u << 5, /* bitwise run-to-run reproducible dQ (reading A19; NEXT-4): the fp32
                               dQ reduction across key blocks happens in a fixed order, enforced by
                               per-(head, query block) flags in the workspace.  Slower backward.
-                              Non-causal requires N/128 <= the device's SM count
+                              Non-causal requires T <= the device's SM count
                               (SAGE_ERR_UNSUPPORTED otherwise).  Every other output is always
                               deterministic. */
   SAGE_P_COLSCALE = 1u << 6, /* variant (the dV half of SURVEY.md 8(f) NEXT-2): the backward's psi(P)
@@ -125,8 +129,8 @@ typedef struct {
   uint64_t params_tag; /* written by sage_fwd; 0 = not filled */
 } sage_ctx;
 
-/* Bytes of the context buffer: int8 Q^, K^ [B,H,N,d]; fp32 s_Q, s_K [B,H,N/128]; mu_K [B,H,d]; and with
- * SAGE_Q_SMOOTH mu_Q [B,H,N/128,d] and the bias [B,H,N/128,N] (Alg. 2 line 1 inputs).
+/* Bytes of the context buffer: int8 Q^, K^ [B,H,Np,d]; fp32 s_Q, s_K [B,H,T]; mu_K [B,H,d]; and with
+ * SAGE_Q_SMOOTH mu_Q [B,H,T,d] and the bias [B,H,T,Np] (Alg. 2 line 1 inputs).
  * 0 on invalid params. */
 SAGE_API size_t sage_ctx_bytes(const sage_params* p);
 
@@ -176,22 +180,22 @@ SAGE_API sage_status sage_bwd_qknorm(const sage_params* p, const void* xq, const
 
 /* Device pointers into a context / workspace buffer (for tests and tracing; no launch). */
 typedef struct {
-  int8_t *q_i8, *k_i8;        /* [B,H,N,d] psi(Q_sm or Q), psi(K_sm) */
-  float *q_scale, *k_scale;   /* [B,H,N/128] */
+  int8_t *q_i8, *k_i8;        /* [B,H,Np,d] psi(Q_sm or Q), psi(K_sm); rows N..Np-1 zero */
+  float *q_scale, *k_scale;   /* [B,H,T] */
   float* mu_k;                /* [B,H,d] */
-  float* mu_q;                /* [B,H,N/128,d] or NULL */
-  float* bias;                /* [B,H,N/128,N] or NULL: bias_i[n] = mu_Qi . K_sm[n] */
-  float *rstd_q, *rstd_k;     /* [B,H,N] QK-norm rstd of X_q / X_k rows, or NULL */
+  float* mu_q;                /* [B,H,T,d] or NULL */
+  float* bias;                /* [B,H,T,Np] or NULL: bias_i[n] = mu_Qi . K_sm[n] (0 for n >= N) */
+  float *rstd_q, *rstd_k;     /* [B,H,Np] QK-norm rstd of X_q / X_k rows, or NULL */
 } sage_ctx_view;
 SAGE_API sage_status sage_ctx_get_view(const sage_params* p, void* ctx, sage_ctx_view* out);
 
 typedef struct {
-  int8_t* v_i8;   /* fwd: [B,H,N,d] psi(V) */
-  float* v_scale; /* fwd: [B,H,N/128] */
-  int8_t* do_i8;  /* bwd: [B,H,N,d] psi(dO) */
-  float* do_scale;/* bwd: [B,H,N/128] */
-  float* delta;   /* bwd: [B,H,N] rowsum(dO o O) */
-  float* dq_acc;  /* bwd: [B,H,N,d] fp32 dQ accumulator */
+  int8_t* v_i8;   /* fwd: [B,H,Np,d] psi(V) */
+  float* v_scale; /* fwd: [B,H,T] */
+  int8_t* do_i8;  /* bwd: [B,H,Np,d] psi(dO) */
+  float* do_scale;/* bwd: [B,H,T] */
+  float* delta;   /* bwd: [B,H,Np] rowsum(dO o O), 0 on the padded rows */
+  float* dq_acc;  /* bwd: [B,H,Np,d] fp32 dQ accumulator */
 } sage_ws_view;
 SAGE_API sage_status sage_ws_get_view(const sage_params* p, int backward, void* ws, sage_ws_view* out);
 
@@ -212,7 +216,8 @@ SAGE_API sage_status sage_debug_trace(void* host_out, size_t bytes);
 
 /* Test only (libsage_trace.so; the production libsage.so returns SAGE_ERR_UNSUPPORTED): make every
  * later sage_bwd dump, for heads bh < `heads` (bh = b*H + h), K4's own backward intermediates
- * (Alg. 2 lines 5-11) into caller-owned device memory (T = N/128):
+ * (Alg. 2 lines 5-11) into caller-owned device memory (T = N/128; N % 128 == 0 only --
+ * a ragged N's backward runs without dumping):
  *   p_hat_t  int8 [heads][N kv][N q]  P^ of tile (i, j) transposed (key-major), psi(P) per tile (A11)
  *   ds_hat_t int8 [heads][N kv][N q]  dS^, same layout
  *   ds_t     fp32 [heads][N kv][N q]  dS = P o (dP - delta) before psi
@@ -229,7 +234,7 @@ SAGE_API sage_status sage_debug_dump(void* p_hat_t, float* s_p, void* ds_hat_t, 
 SAGE_API sage_status sage_debug_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t* dq_t, float* dp_t);
 
 /* Test only (libsage_trace.so): make every later sage_fwd dump, for heads bh < `heads`, K2's own
- * intermediates (Alg. 1 lines 7-10) into caller-owned device memory:
+ * intermediates (Alg. 1 lines 7-10) into caller-owned device memory (N % 128 == 0 only):
  *   s       int32 [heads][N q][N kv]    the S = Q^_i K^_j^T accumulator of every processed tile (line 7)
  *   p_hat   uint8 [heads][N q][N kv]    the per-token P^ (line 9), 0..127 (0..255 with SAGE_P_U8)
  *   s_p     fp32  [heads][N q][T j]     its per-row scale s_P = e^{rowmax - m_ij} / 127 (line 9)

@@ -65,7 +65,7 @@ constexpr size_t kAlign = 256;
 size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Dims {
-  size_t BH, N, d, T;
+  size_t BH, N, d, T, Np;  // T = ceil(N / 128) blocks; the library's per-row buffers have Np = 128 T rows per head
   bool causal, ks, qs, pu8, qkn, det, pcol, fine, fp16, f32out, pvfp8;
   float tau;
   IoLayout io;  // element strides of the I/O tensors
@@ -75,17 +75,18 @@ bool dims_of(const sage_params* p, Dims* o) {
   if (!p) return false;
   if (p->batch <= 0 || p->heads <= 0 || p->seqlen <= 0) return false;
   if (p->head_dim != 64 && p->head_dim != 128) return false;
-  if (p->seqlen % kBlk || p->seqlen > kMaxSeqLen) return false;
+  if (p->seqlen > kMaxSeqLen) return false;  // any N >= 1: a ragged N has a short last block (reading A33)
   if (p->flags & ~(uint32_t)(SAGE_CAUSAL | SAGE_K_SMOOTH | SAGE_Q_SMOOTH | SAGE_P_U8 | SAGE_QK_NORM | SAGE_DETERMINISTIC |
                              SAGE_P_COLSCALE | SAGE_FINE_BWD | SAGE_FP16 | SAGE_FP32_OUT | SAGE_PV_FP8))
     return false;
   if (!(p->softmax_scale >= 0.f) || std::isinf(p->softmax_scale)) return false;
   const size_t BH = (size_t)p->batch * p->heads;
-  if (BH * p->seqlen > (size_t)INT32_MAX / 2) return false;  // TMA row coordinates are int32
+  if (BH * (size_t)padded_len(p->seqlen) > (size_t)INT32_MAX / 2) return false;  // TMA row coordinates are int32
   o->BH = BH;
   o->N = p->seqlen;
   o->d = p->head_dim;
-  o->T = o->N / kBlk;
+  o->T = (size_t)num_blocks(p->seqlen);
+  o->Np = o->T * kBlk;
   o->causal = p->flags & SAGE_CAUSAL;
   o->ks = p->flags & SAGE_K_SMOOTH;
   o->qs = p->flags & SAGE_Q_SMOOTH;
@@ -120,16 +121,16 @@ struct CtxLayout {
 };
 CtxLayout ctx_layout(const Dims& D) {
   CtxLayout L{};
-  size_t off = 0, nd = D.BH * D.N * D.d;
+  size_t off = 0, nd = D.BH * D.Np * D.d;  // padded rows (A33)
   L.q8 = off; off += up(nd);
   L.k8 = off; off += up(nd);
   L.sq = off; off += up(D.BH * D.T * 4);
   L.sk = off; off += up(D.BH * D.T * 4);
   L.muk = off; off += up(D.BH * D.d * 4);
   L.muq = off; off += D.qs ? up(D.BH * D.T * D.d * 4) : 0;
-  L.bias = off; off += D.qs ? up(D.BH * D.T * D.N * 4) : 0;
-  L.rq = off; off += D.qkn ? up(D.BH * D.N * 4) : 0;  // QK-norm rstd of X_q, X_k rows
-  L.rk = off; off += D.qkn ? up(D.BH * D.N * 4) : 0;
+  L.bias = off; off += D.qs ? up(D.BH * D.T * D.Np * 4) : 0;
+  L.rq = off; off += D.qkn ? up(D.BH * D.Np * 4) : 0;  // QK-norm rstd of X_q, X_k rows
+  L.rk = off; off += D.qkn ? up(D.BH * D.Np * 4) : 0;
   L.total = off;
   return L;
 }
@@ -139,7 +140,7 @@ struct FwdWs {
 };
 FwdWs fwd_ws(const Dims& D) {
   FwdWs W{};
-  size_t off = 0, nd = D.BH * D.N * D.d;
+  size_t off = 0, nd = D.BH * D.Np * D.d;
   W.v8 = off; off += up(nd);
   W.sv = off; off += up(D.BH * D.T * 4);
   W.partk = off; off += up(D.BH * D.T * D.d * 8);
@@ -153,11 +154,11 @@ struct BwdWs {
 };
 BwdWs bwd_ws(const Dims& D) {
   BwdWs W{};
-  size_t off = 0, nd = D.BH * D.N * D.d;
+  size_t off = 0, nd = D.BH * D.Np * D.d;
   W.do8 = off; off += up(nd);
   W.sdo = off; off += up(D.BH * D.T * 4);
-  W.delta = off; off += up(D.BH * D.N * 4);
-  W.l2 = off; off += up(D.BH * D.N * 4);
+  W.delta = off; off += up(D.BH * D.Np * 4);
+  W.l2 = off; off += up(D.BH * D.Np * 4);
   W.dq = off; off += up(nd * 4);
   // QK-norm dgamma partials: per 128-row block (fp32), then per 64 blocks (fp64), see launch_norm_bwd
   const size_t gbytes = D.BH * D.T * D.d * 4 + 8 + (D.BH * D.T + 63) / 64 * D.d * 8;
@@ -512,7 +513,7 @@ sage_status fwd_impl(const Dims& D, const void* q, const void* k, const void* v,
   const NormIn nq{rq, gq, eps}, nk{rk, gk, eps};
 
   FwdArgs a{};
-  const uint64_t rows = D.BH * D.N;
+  const uint64_t rows = D.BH * D.Np;
   if (!make_tmap_2d(&a.tm_q, q8, kU8, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_k, k8, kU8, rows, d, kBlk, d) ||
       !make_tmap_2d(&a.tm_v, v8, kU8, rows, d, kBlk, d))
     return cuda_fail(cudaErrorInvalidValue);
@@ -592,11 +593,11 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
   float *sq = at<float>(cx, C.sq), *sk = at<float>(cx, C.sk), *sdo = at<float>(ws, W.sdo);
   float *delta = at<float>(ws, W.delta), *l2 = at<float>(ws, W.l2);
   // SAGE_FP32_OUT with contiguous outputs: dQ is reduced straight into the caller's fp32 dq (zeroed by K3; no K5)
-  const bool dq_direct = D.f32out && D.io.contiguous((int)D.N, (int)D.d);
+  const bool dq_direct = D.f32out && D.io.contiguous((int)D.N, (int)D.d) && D.Np == D.N;
   float* dqacc = dq_direct ? static_cast<float*>(dq) : at<float>(ws, W.dq);
 
   BwdArgs a{};
-  const uint64_t rows = D.BH * D.N;
+  const uint64_t rows = D.BH * D.Np;
   if (!make_tmap_2d(&a.tm_q, q8, kU8, rows, d, kBlk, d) || !make_tmap_2d(&a.tm_k, k8, kU8, rows, d, kBlk, d) ||
       !make_tmap_2d(&a.tm_doq, do8, kU8, rows, d, kBlk, d) ||
       !make_tmap_io(&a.tm_v, v, D.fp16 ? kF16 : kBF16, BH / D.io.H, N, d, D.io, kBlk, 64) ||
@@ -642,10 +643,10 @@ sage_status bwd_impl(const Dims& D, const void* v, const void* o, const float* l
     const auto* rq = at<const float>(cx, C.rq);
     const auto* rk = at<const float>(cx, C.rk);
     if ((e = launch_norm_bwd(dqacc, nullptr, xq, rq, gq, dq, at<float>(ws, W.gq),
-                             dgq, D.BH * D.N, d, s, D.fp16, D.io, N)) != cudaSuccess)
+                             dgq, D.BH * D.Np, d, s, D.fp16, D.io, N)) != cudaSuccess)
       return cuda_fail(e);
     if ((e = launch_norm_bwd(nullptr, dk, xk, rk, gk, dk, at<float>(ws, W.gk),
-                             dgk, D.BH * D.N, d, s, D.fp16, D.io, N)) != cudaSuccess)
+                             dgk, D.BH * D.Np, d, s, D.fp16, D.io, N)) != cudaSuccess)
       return cuda_fail(e);
     if (g_prof.on) g_prof.launches += 6;  // 2 x (norm_bwd, dgamma stage 1, stage 2)
     return SAGE_OK;

@@ -125,7 +125,7 @@ __device__ unsigned long long g_trace[kTrCtas * kTrTiles * kTrEvents];
 // warps write P^^T, dS^^T (int8) and the pre-psi dS^T (fp32) as [head][N kv][N q], and the tile
 // scales s_P, s_dS as [head][T i][T j], for heads bh < g_dump.heads (Tier C, fidelity reports).
 __device__ BwdDump g_dump;
-#define DUMPING (SAGE_TRACE && (ablate & 16) && bh < g_dump.heads)
+#define DUMPING (SAGE_TRACE && (ablate & 16) && bh < g_dump.heads && dump_ok)
 // ... and the int32 accumulators (sage_debug_dump_acc): S^T [head][N kv][N q], the dV / dK tiles
 // [head][T i][N kv][D], the dQ tiles [head][T j][N q][D], each before any scaling
 struct BwdDumpAcc {
@@ -225,7 +225,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* colmax = reinterpret_cast<int*>(smem + L::kColMax);    // FINE
   float* invq_s = reinterpret_cast<float*>(smem + L::kInvQ);  // FINE
 
-  const int T = N / kBlk;
+  // N need not be a multiple of 128 (reading A33): T blocks, the library's tiles padded to Np rows per head
+  const int T = num_blocks(N), Np = T * kBlk;
+  const bool dump_ok = N == Np;  // the tile dumps (test build) are laid out for N % 128 == 0 only
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t one = blockDim.x / kThreads;  // a runtime 1 (i2f2 on the FMA pipe, SAGE_I2F_FMA)
   const int tile = blockIdx.x;
@@ -242,7 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int i0 = CAUSAL ? j : 0;
   const int n_it = T - i0;
   auto i_of = [&](int it) { return (det && !CAUSAL) ? (j + it) % T : i0 + it; };
-  const int krow = bh * N + j * kBlk;
+  const int krow = bh * Np + j * kBlk;
+  const int kv_valid = N - j * kBlk;  // keys of this block (< 128 only in a ragged N's last block)
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       for (int it = 0; it < n_it; ++it) {
         const int s = it % kStages, i = i_of(it);
-        const int qrow = bh * N + i * kBlk;
+        const int qrow = bh * Np + i * kBlk;
         uint8_t* st = smem + L::kStage + s * L::kStageBytes;
         mbar_wait(q_empty + s, ((it / kStages) & 1) ^ 1);
         if (elect_one()) {
@@ -579,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float4* Ls4 = reinterpret_cast<const float4*>(st + L::kSL) + qc0 / 4;
       const float4* Ds4 = reinterpret_cast<const float4*>(st + L::kSDelta) + qc0 / 4;
       const float c2 = sc_q[i] * sk * tau2;  // int32 -> log2-domain logit
-      const float b2 = QSMOOTH ? bias[((size_t)bh * T + i) * N + (size_t)j * kBlk + r] * tau2 : 0.f;
+      const float b2 = QSMOOTH ? bias[((size_t)bh * T + i) * Np + (size_t)j * kBlk + r] * tau2 : 0.f;
       const bool diag = CAUSAL && (i == j);
       const bool cm = !(ablate & 2);
       float t[64];
@@ -629,8 +632,18 @@ if (cm) {
         for (int e = 0; e < 64; ++e)
           if (r > qc0 + e) t[e] = -INFINITY;
       }
+      // A key row the short last block of a ragged N lacks (A33; the missing queries have L = +inf, so
+      // their P is 0): its K^ and V rows are zero, so its P, dS reach dQ only through K^ = 0 and its own dV,
+      // dK rows, which are not written.  It must only stay out of the tile maxima (s_P, s_dS): its
+      // row max is dropped here and its |dS| max below (FINE: its per-query dS maxima need the full mask)
+      const bool kv_missing = r >= kv_valid;
+      if (fine && kv_missing) {
+#pragma unroll
+        for (int e = 0; e < 64; ++e) t[e] = -INFINITY;
+      }
 #pragma unroll
       for (int e = 0; e < 64; e += 4) tmax = fmaxf(tmax, fmax3(t[e], t[e + 1], fmaxf(t[e + 2], t[e + 3])));
+      if (kv_missing) tmax = -INFINITY;
 
       // -- step 2: psi(P) scale over the tile: amax = max P = 2^max(t)  (line 6, reading A11)
       if (threadIdx.x == 128) TR(19, it);
@@ -718,6 +731,7 @@ if (cm) {
       warp_arrive(p_ready);  // P^^T written; S^T and dP^T read (their TMEM columns may be reused)
       if (threadIdx.x == 128) TR(6, it);
 
+      if (kv_missing) dsmax = 0.f;
       // -- step 5: psi(dS) scale over the tile (FINE: one per key row for dK, one per query for dQ)
       float amax_ds;
       if constexpr (fine) {
@@ -972,7 +986,7 @@ if (cm) {
 #pragma unroll
             for (int bx = 0; bx < L::kDqBoxes; ++bx)
               tma_reduce_add_2d(&tm_dq, stage + bx * L::kDqBox, (qq * L::kDqBoxes + bx) * 32,
-                                bh * N + i * kBlk + (warp % 4) * 32);
+                                bh * Np + i * kBlk + (warp % 4) * 32);
             bulk_commit();
           }
         }
@@ -993,7 +1007,7 @@ if (cm) {
       mbar_wait(dv_drained, (n_it - 1) & 1);
       tc_fence_after();
     }
-    // epilogue: dK_j, dV_j rows -> bf16
+    // epilogue: dK_j, dV_j rows -> bf16 (not the rows a short last block lacks, A33)
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 32) {
       float vv[32];
@@ -1011,6 +1025,7 @@ if (cm) {
 #pragma unroll
         for (int e = 0; e < 32; ++e) vv[e] = dv_acc[c0 + e];
       }
+      if (r >= kv_valid) continue;  // (after the warp-collective TMEM loads)
       if (f32out) {  // SAGE_FP32_OUT
 #pragma unroll
         for (int e4 = 0; e4 < 32; e4 += 4) {
@@ -1049,7 +1064,7 @@ cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
   constexpr int kSmem = BwdSmem<D, VAR == 3>::kAlloc;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
   if (e != cudaSuccess) return e;
-  const int T = a.N / kBlk;
+  const int T = num_blocks(a.N);
   kern<<<a.BH * T, kThreads, kSmem, s>>>(a.tm_q, a.tm_k, a.tm_doq, a.tm_v, a.tm_do, a.tm_dq, a.q_scale,
                                                        a.k_scale, a.do_scale, a.l2, a.delta, a.bias, a.mu_q,
                                                        a.dq_acc, a.dk, a.dv, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,

@@ -79,8 +79,10 @@ struct FwdSmem {
 };
 
 // FP8 (SAGE_PV_FP8): P^ and V^ in E4M3 and P^V^ as a kind::f8f6f4 MMA (fp32 accumulator) -- a separate
-// instantiation, the INT8 path of Alg. 1 untouched
-template <int D, bool CAUSAL, bool QSMOOTH, bool FP8>
+// instantiation, the INT8 path of Alg. 1 untouched.  RAG: N is not a multiple of 128 (reading A33; the
+// last kv tile's missing keys are masked -- a separate instantiation keeps the check out of the common
+// kernels' inner loops, where it cost 8-20%)
+template <int D, bool CAUSAL, bool QSMOOTH, bool FP8, bool RAG>
 __global__ void __launch_bounds__(kThreads, 2)
     sage_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ q_scale,
@@ -107,7 +109,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
   float* bias_s = reinterpret_cast<float*>(smem + L::kBias);
 
-  const int T = N / kBlk;
+  // N need not be a multiple of 128 (reading A33): T blocks, the library's tiles padded to Np rows per head
+  const int T = num_blocks(N), Np = T * kBlk;
   const int warp = threadIdx.x / 32;
   const uint32_t one = blockDim.x / kThreads;  // a runtime 1 (i2f2 on the FMA pipe, SAGE_I2F_FMA)
   // head-major order (the CTAs of one head share K^/V^ through L2); causal: longest (high i) first
@@ -115,7 +118,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int bh = tile / T;
   const int i = CAUSAL ? (T - 1 - tile % T) : (tile % T);
   const int nj = CAUSAL ? i + 1 : T;
-  const int row0 = bh * N + i * kBlk;  // first global row of this q block
+  const int row0 = bh * Np + i * kBlk;  // first row of this q block in the padded int8 tiles
+  const int kv_last = N - (T - 1) * kBlk;  // keys of the last kv block (128 unless N is ragged)
+  // the tile dumps (test build) are laid out for N % 128 == 0 only
+  const bool dump_ok = N == Np;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -158,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int j = 0; j < nj; ++j) {
         const int st = j % kStages;
         const uint32_t ph = (j / kStages) & 1;
-        const int krow = bh * N + j * kBlk;
+        const int krow = bh * Np + j * kBlk;
         mbar_wait(k_empty + st, ph ^ 1);
         if (elect_one()) {
           mbar_expect_tx(k_full + st, L::kTile);
@@ -270,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int h = 0; h < kPair; ++h) {
         const int c0 = cp + 32 * h;
         uint32_t(&v)[32] = vv[h];
-        if (FDUMPING && g_fdump.pv) {
+        if (FDUMPING && dump_ok && g_fdump.pv) {
           int32_t* dst = g_fdump.pv + (((size_t)bh * T + jj) * N + (size_t)i * kBlk + r) * D + c0;
 #pragma unroll
           for (int e = 0; e < 32; e += 4) *reinterpret_cast<uint4*>(dst + e) = make_uint4(v[e], v[e + 1], v[e + 2], v[e + 3]);
@@ -294,18 +300,23 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int j = 0; j < nj; ++j) {
       const float c2 = sq * k_scale[(size_t)bh * T + j] * tau2;  // int32 -> log2-domain logit
       const float sv = v_scale[(size_t)bh * T + j];
+      // columns c < lim take part: the causal mask (key n > query r, reading A14) and the keys a short
+      // last block lacks (A33); lim >= 1 always
       const bool diag = CAUSAL && (j == i);
+      const bool ragged = RAG && j == T - 1;
+      const int lim = RAG ? min(diag ? r + 1 : kBlk, ragged ? kv_last : kBlk) : r + 1;
+      const bool masked = diag || ragged;
       const float* bj = bias_s + (j & 1) * kBlk;
       if constexpr (QSMOOTH) {
         // bias row (tau*log2e * mu_Qi . K_sm[n]) for this kv tile, shared by all rows; two slots
         // so one barrier per tile suffices (slot j&1 was last read in tile j-2)
-        bias_s[(j & 1) * kBlk + r] = bias[((size_t)bh * T + i) * N + (size_t)j * kBlk + r] * tau2;
+        bias_s[(j & 1) * kBlk + r] = bias[((size_t)bh * T + i) * Np + (size_t)j * kBlk + r] * tau2;
         named_bar_sync(1, 128);
       }
       mbar_wait(s_full + (j & 1), (j >> 1) & 1);
       tc_fence_after();
       if (r == 0) TRF(2, j);
-      if (FDUMPING && g_fdump.s) {  // the int32 S accumulator of tile (i, j), unmasked (Alg. 1 line 7)
+      if (FDUMPING && dump_ok && g_fdump.s) {  // the int32 S accumulator of tile (i, j), unmasked (Alg. 1 line 7)
         int32_t* dst = g_fdump.s + ((size_t)bh * N + (size_t)i * kBlk + r) * N + (size_t)j * kBlk;
 #pragma unroll 1
         for (int c0 = 0; c0 < kBlk; c0 += 32) {
@@ -332,10 +343,10 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (int h = 0; h < kPair1; ++h) {
             const int c0 = cp + 32 * h;
             uint32_t(&v)[32] = vv[h];
-            if (diag) {
+            if (masked) {
 #pragma unroll
               for (int e = 0; e < 32; ++e)
-                if (c0 + e <= r) mx = max(mx, (int)v[e]);
+                if (c0 + e < lim) mx = max(mx, (int)v[e]);
             } else {
 #pragma unroll
               for (int e = 0; e < 32; e += 2) mx = max(mx, max((int)v[e], (int)v[e + 1]));
@@ -351,10 +362,10 @@ __global__ void __launch_bounds__(kThreads, 2)
           uint32_t v[32];
           tmem_ld32(tbuf(j) + c0 + lane_off, v);
           tmem_wait_ld();
-          if (diag) {
+          if (masked) {
 #pragma unroll
             for (int e = 0; e < 32; ++e)
-              if (c0 + e <= r) rm = fmaxf(rm, fmaf(__int2float_rn((int)v[e]), c2, bj[c0 + e]));
+              if (c0 + e < lim) rm = fmaxf(rm, fmaf(__int2float_rn((int)v[e]), c2, bj[c0 + e]));
           } else {  // packed: two logits per FFMA2, a three-input max per pair
 #pragma unroll
             for (int e = 0; e < 32; e += 4) {
@@ -409,11 +420,11 @@ __global__ void __launch_bounds__(kThreads, 2)
             a = make_float2(ex2(a.x), ex2(a.y));
             b = make_float2(ex2(b.x), ex2(b.y));
           }
-          if (diag) {  // causal mask (reading A14): key n > query r -> P = 0
-            if (c0 + e > r) a.x = 0.f;
-            if (c0 + e + 1 > r) a.y = 0.f;
-            if (c0 + e + 2 > r) b.x = 0.f;
-            if (c0 + e + 3 > r) b.y = 0.f;
+          if (masked) {  // causal mask (reading A14), missing keys (A33) -> P = 0
+            if (c0 + e >= lim) a.x = 0.f;
+            if (c0 + e + 1 >= lim) a.y = 0.f;
+            if (c0 + e + 2 >= lim) b.x = 0.f;
+            if (c0 + e + 3 >= lim) b.y = 0.f;
           }
           rs2 = fadd2(rs2, fadd2(a, b));
           if constexpr (FP8) {
@@ -424,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             pk[e4] = pack4_magic(qa.x, qa.y, qb.x, qb.y);
           }
         }
-        if (FDUMPING && g_fdump.p) {
+        if (FDUMPING && dump_ok && g_fdump.p) {
           uint8_t* dst = g_fdump.p + ((size_t)bh * N + (size_t)i * kBlk + r) * N + (size_t)j * kBlk + c0;
           *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(dst + 16) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
@@ -450,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       // l = alpha l + e^{rowmax - m_ij} sum(e^{S - rowmax})  (line 8, reading A7)
       l = fmaf(alpha, l, e_rm * inv_pmax * (rs2.x + rs2.y));
       const float spv = e_rm * inv_pmax * sv;
-      if (FDUMPING && g_fdump.sp) g_fdump.sp[((size_t)bh * N + (size_t)i * kBlk + r) * T + j] = e_rm * inv_pmax;
+      if (FDUMPING && dump_ok && g_fdump.sp) g_fdump.sp[((size_t)bh * N + (size_t)i * kBlk + r) * T + j] = e_rm * inv_pmax;
       m = m_new;
       prev_alpha = alpha;
       prev_spv = spv;
@@ -458,9 +469,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_wait(o_full, (nj - 1) & 1);
     tc_fence_after();
     correct(nj - 1, prev_alpha, prev_spv);
-    // epilogue: O = acc / l (Alg. 1 line 13), L = m + ln l (line 14, natural log)
+    // epilogue: O = acc / l (Alg. 1 line 13), L = m + ln l (line 14, natural log); the padded rows of a
+    // short last block (A33) are not written
     const float inv_l = l > 0.f ? 1.f / l : 0.f;
-    if (f32out) {  // SAGE_FP32_OUT
+    if (i * kBlk + r >= N) {
+    } else if (f32out) {  // SAGE_FP32_OUT
       float4* orow = reinterpret_cast<float4*>(static_cast<float*>(o_out) + o_off);
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 4)
@@ -476,7 +489,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         orow[c0 / 8] = make_uint4(h[0], h[1], h[2], h[3]);
       }
     }
-    lse[(size_t)row0 + r] = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+    if (i * kBlk + r < N)
+      lse[(size_t)bh * N + i * kBlk + r] = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
   }
   __syncwarp();
   tc_fence_before();
@@ -487,12 +501,12 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
-template <int D, bool C, bool QS, bool F8>
+template <int D, bool C, bool QS, bool F8, bool RAG>
 cudaError_t launch_t(const FwdArgs& a, cudaStream_t s) {
-  auto kern = sage_fwd_kernel<D, C, QS, F8>;
+  auto kern = sage_fwd_kernel<D, C, QS, F8, RAG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem<D>::kAlloc);
   if (e != cudaSuccess) return e;
-  const int T = a.N / kBlk;
+  const int T = num_blocks(a.N);
   kern<<<a.BH * T, kThreads, FwdSmem<D>::kAlloc, s>>>(a.tm_q, a.tm_k, a.tm_v, a.q_scale, a.k_scale, a.v_scale,
                                                        a.bias, a.o, a.lse, a.N, a.BH, a.tau, a.pu8 ? 1 : 0,
                                                        a.fp16 ? 1 : 0, a.f32out ? 1 : 0, a.io, a.ablate);
@@ -508,10 +522,15 @@ cudaError_t read_fwd_trace(void* host, size_t bytes) {
   return cudaMemcpyFromSymbol(host, g_trace_fwd, bytes);
 }
 
+template <int D, bool F8, bool RAG>
+cudaError_t launch_r(const FwdArgs& a, cudaStream_t s) {
+  if (a.causal) return a.qsmooth ? launch_t<D, true, true, F8, RAG>(a, s) : launch_t<D, true, false, F8, RAG>(a, s);
+  return a.qsmooth ? launch_t<D, false, true, F8, RAG>(a, s) : launch_t<D, false, false, F8, RAG>(a, s);
+}
+
 template <int D, bool F8>
 cudaError_t launch_d(const FwdArgs& a, cudaStream_t s) {
-  if (a.causal) return a.qsmooth ? launch_t<D, true, true, F8>(a, s) : launch_t<D, true, false, F8>(a, s);
-  return a.qsmooth ? launch_t<D, false, true, F8>(a, s) : launch_t<D, false, false, F8>(a, s);
+  return a.N % kBlk ? launch_r<D, F8, true>(a, s) : launch_r<D, F8, false>(a, s);
 }
 
 cudaError_t launch_fwd(const FwdArgs& a, cudaStream_t s) {

@@ -10,6 +10,11 @@ namespace sage {
 
 constexpr int kBlk = 128;  // B_q = B_kv = 128 (reading A5): tcgen05 M = 128 tiles
 constexpr int kMaxSeqLen = 32768;  // per-head scale rows are staged in shared memory (T <= 256)
+// N need not be a multiple of 128 (reading A33): a head has T = ceil(N / 128) blocks, the last one short.
+// The library's own per-row buffers (int8 tiles, L, delta, the Q-smoothing bias, the fp32 dQ accumulator,
+// QK-norm rstd) give every head Np = 128 T rows; rows N .. Np-1 hold zeros (or masked values).
+__host__ __device__ __forceinline__ int num_blocks(int N) { return (N + kBlk - 1) / kBlk; }
+__host__ __device__ __forceinline__ int padded_len(int N) { return num_blocks(N) * kBlk; }
 
 // Layout of the I/O tensors (Q, K, V, O, dO, dQ, dK, dV; X_q, X_k, dX_q, dX_k with QK-norm): element
 // strides of the batch, head and token dimensions (the head dimension d is contiguous).  Row (bh, n) of
@@ -32,7 +37,7 @@ struct IoLayout {
 // rstd[row] = fl32(1 / sqrt(mean(x^2) + eps)) computed from the row as it is loaded (K0, K1; K1
 // stores it for the backward) or read back (the Q-smoothing bias kernel, after K1).
 struct NormIn {
-  float* rstd;         // [BH*N]
+  float* rstd;         // [BH*Np]
   const float* gamma;  // [d] or null (no QK-norm)
   float eps;
 };

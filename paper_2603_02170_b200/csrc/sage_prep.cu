@@ -129,15 +129,18 @@ __device__ __forceinline__ float warp_max(float v) {
 // loads), then the R partials are combined in fixed order q = 0..R-1.  Sums of bf16 values in
 // double are exact unless a column spans > 53-8-log2(N) binades, so the order cannot change the
 // result for any realistic input; it is fixed anyway.
-template <typename T, int D, bool QKN>
+// RAG (every kernel below): N is not a multiple of 128 (reading A33).  The short-block checks compile
+// away for RAG = false, so the common case keeps its unconditional load batches.
+template <typename T, int D, bool QKN, bool RAG>
 __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, double* __restrict__ part,
-                                                     NormIn nrm, IoLayout io, int nT) {
+                                                     NormIn nrm, IoLayout io, int nT, int N) {
   constexpr int kGroups = D / kVec;        // 8 (d=64) or 16 (d=128)
   constexpr int kR = 256 / kGroups;        // 32 or 16 row phases
   __shared__ double red[kR][D];
   const long long chunk = blockIdx.x;      // bh * T + t
   const int g = threadIdx.x % kGroups, q = threadIdx.x / kGroups;
   const T* p = x + io.row(chunk / nT, (chunk % nT) * kBlk) + g * kVec;
+  const int nv = RAG ? min(kBlk, N - (int)(chunk % nT) * kBlk) : kBlk;  // rows this chunk holds (A33)
   double acc[kVec];
   float gam[kVec];
 #pragma unroll
@@ -148,7 +151,8 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, do
   constexpr int kRows = kBlk / kR;  // rows per thread: all loads issued before any arithmetic
   uint4 raw[kRows];
 #pragma unroll
-  for (int k = 0; k < kRows; ++k) raw[k] = *reinterpret_cast<const uint4*>(p + (q + k * kR) * io.sn);
+  for (int k = 0; k < kRows; ++k)
+    raw[k] = q + k * kR < nv ? *reinterpret_cast<const uint4*>(p + (q + k * kR) * io.sn) : make_uint4(0, 0, 0, 0);
   __shared__ double ssq[QKN ? nrm_smem_rows * kGroups : 1];
   __shared__ float rs_s[QKN ? kBlk : 1];
   if constexpr (QKN) chunk_rstd<T, kGroups, D, kRows, kR>(raw, g, q, ssq, rs_s, nrm.eps, nullptr);
@@ -179,24 +183,26 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, do
 __global__ void colmean_kernel(const double* __restrict__ part, float* __restrict__ mu, int N, int d, int BH) {
   int item = blockIdx.x * blockDim.x + threadIdx.x;
   if (item >= BH * d) return;
-  int bh = item / d, c = item % d, T = N / kBlk;
+  int bh = item / d, c = item % d, T = num_blocks(N);
   const double* p = part + (size_t)bh * T * d + c;
   double total = 0.0;
   for (int t = 0; t < T; ++t) total += p[(size_t)t * d];
   mu[item] = __double2float_rn(total / (double)N);
 }
 
-__global__ void blockmean_kernel(const double* __restrict__ part, float* __restrict__ mu_q, size_t n) {
+// mu_Q[bh][t][c] = fl32(part / rows of block t)  (the last block of a ragged N is short, A33)
+__global__ void blockmean_kernel(const double* __restrict__ part, float* __restrict__ mu_q, size_t n, int d, int N) {
   size_t item = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (item >= n) return;
-  mu_q[item] = __double2float_rn(part[item] / (double)kBlk);
+  const int t = (int)((item / d) % num_blocks(N));
+  mu_q[item] = __double2float_rn(part[item] / (double)min(kBlk, N - t * kBlk));
 }
 
 // ---------------------------------------------------------------- K1: psi
 // One CTA quantises one 128 x d block: x_sm = fl32(x - mu); amax; scale = fl32(amax/127);
 // inv = fl32(127/amax) (0 for an all-zero block, A3); q = clamp(RNE(fl32(x_sm*inv)), +-127).
-template <typename TI, int D, bool QKN>
-__global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T, IoLayout io) {
+template <typename TI, int D, bool QKN, bool RAG>
+__global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T, IoLayout io, int N) {
   // blockIdx.y selects the tensor (Q, K, V): one launch for all three psi passes
   const QuantJob& job = jobs.j[blockIdx.y];
   const TI* __restrict__ x = static_cast<const TI*>(job.x);
@@ -213,6 +219,7 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T,
   const int bh = (int)(blk / T), t = (int)(blk % T);
   const int g = threadIdx.x % kGroups, r0 = threadIdx.x / kGroups;
   const TI* xb = x + io.row(bh, (long long)t * kBlk);
+  const int nv = RAG ? min(kBlk, N - t * kBlk) : kBlk;  // rows this block holds (A33); the rest quantise to 0
   float m[kVec];
 #pragma unroll
   for (int e = 0; e < kVec; ++e) {
@@ -224,7 +231,8 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T,
   uint4 raw[kIters];
 #pragma unroll
   for (int it = 0; it < kIters; ++it)
-    raw[it] = *reinterpret_cast<const uint4*>(xb + (r0 + it * kRowsPerPass) * io.sn + g * kVec);
+    raw[it] = r0 + it * kRowsPerPass < nv ? *reinterpret_cast<const uint4*>(xb + (r0 + it * kRowsPerPass) * io.sn + g * kVec)
+                                          : make_uint4(0, 0, 0, 0);
   // QK-norm row statistics (A24), kept for the backward (QKN launches: every job with gamma)
   __shared__ double ssq[QKN ? nrm_smem_rows * kGroups : 1];
   __shared__ float rs_s[QKN ? kBlk : 1];
@@ -246,8 +254,10 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T,
       for (int e = 0; e < kVec; ++e) v[e] = qk_norm<TI>(v[e], rs, gam[e]);
       raw[it] = pack8<TI>(v);  // exact: qk_norm values are I/O-type values
     }
+    if (r0 + it * kRowsPerPass < nv) {
 #pragma unroll
-    for (int e = 0; e < kVec; ++e) amax = fmaxf(amax, fabsf(__fsub_rn(v[e], m[e])));
+      for (int e = 0; e < kVec; ++e) amax = fmaxf(amax, fabsf(__fsub_rn(v[e], m[e])));
+    }
   }
   amax = warp_max(amax);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
@@ -270,7 +280,9 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T,
 #pragma unroll
     for (int e = 0; e < kVec; ++e) v[e] = __fsub_rn(v[e], m[e]);
     uint32_t w[2];
-    if (job.fp8) {
+    if (r >= nv) {
+      w[0] = w[1] = 0u;
+    } else if (job.fp8) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const float* x = v + 4 * h;
@@ -292,7 +304,7 @@ __global__ void __launch_bounds__(256, 3) quantize_kernel(QuantJobs jobs, int T,
 // CTA = (bh, 128-key block, group of kBiasI query blocks); thread = key n holds its smoothed K row in
 // registers, the group's mu_Q rows are broadcast from shared memory.
 constexpr int kBiasI = 32;
-template <typename TI, int D>
+template <typename TI, int D, bool RAG>
 #ifndef SAGE_BIAS_MINB
 #define SAGE_BIAS_MINB 3  // 3 CTAs per SM (168 registers, 24 B prologue spill at D=128): C3 610.7 -> 612.8 TOPS
 #endif
@@ -301,11 +313,12 @@ __global__ void __launch_bounds__(128, SAGE_BIAS_MINB) qsmooth_bias_kernel(const
                                                            const float* __restrict__ mu_q, float* __restrict__ bias,
                                                            int N, NormIn nrm, IoLayout io) {
   __shared__ float4 mq[kBiasI][D / 4];
-  const int T = N / kBlk;
+  const int T = num_blocks(N), Np = T * kBlk;
   const long long blk = blockIdx.x;    // bh * T + jn
   const int bh = (int)(blk / T), jn = (int)(blk % T);
   const int i0 = blockIdx.y * kBiasI, ni = min(kBiasI, T - i0);
   const int n = threadIdx.x;
+  const bool valid = !RAG || jn * kBlk + n < N;  // a key the short last block lacks gets bias 0 (A33)
   for (int e = threadIdx.x; e < ni * (D / 4); e += blockDim.x)
     mq[e / (D / 4)][e % (D / 4)] = reinterpret_cast<const float4*>(mu_q + ((size_t)bh * T + i0) * D)[e];
   float ks[D];
@@ -314,7 +327,8 @@ __global__ void __launch_bounds__(128, SAGE_BIAS_MINB) qsmooth_bias_kernel(const
   const float rs = nrm.gamma ? nrm.rstd[blk * kBlk + n] : 1.f;  // written by K1's K job
   uint4 raw[D / kVec];  // the whole K row in flight before any use (the loads' latency dominates)
 #pragma unroll
-  for (int c8 = 0; c8 < D / kVec; ++c8) raw[c8] = *reinterpret_cast<const uint4*>(krow + c8 * kVec);
+  for (int c8 = 0; c8 < D / kVec; ++c8)
+    raw[c8] = valid ? *reinterpret_cast<const uint4*>(krow + c8 * kVec) : make_uint4(0, 0, 0, 0);
 #pragma unroll
   for (int c = 0; c < D; c += kVec) {
     float f[kVec];
@@ -326,10 +340,10 @@ __global__ void __launch_bounds__(128, SAGE_BIAS_MINB) qsmooth_bias_kernel(const
     const float4 m0 = *reinterpret_cast<const float4*>(mk + c), m1 = *reinterpret_cast<const float4*>(mk + c + 4);
     const float mm[kVec] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
 #pragma unroll
-    for (int e = 0; e < kVec; ++e) ks[c + e] = __fsub_rn(f[e], mm[e]);
+    for (int e = 0; e < kVec; ++e) ks[c + e] = valid ? __fsub_rn(f[e], mm[e]) : 0.f;
   }
   __syncthreads();
-  float* out = bias + ((size_t)bh * T + i0) * N + (size_t)jn * kBlk + n;
+  float* out = bias + ((size_t)bh * T + i0) * Np + (size_t)jn * kBlk + n;
   // FFMA2 over column pairs (c, c+1): mu_Q's float4 and the K row are already register pairs, so no
   // repacking; two query blocks per pass and two accumulator pairs each (8 partial sums) for ILP
 #pragma unroll 1
@@ -346,8 +360,8 @@ __global__ void __launch_bounds__(128, SAGE_BIAS_MINB) qsmooth_bias_kernel(const
       b1 = ffma2(make_float2(m1.z, m1.w), k23, b1);
     }
     const float2 sa = fadd2(a0, a1), sb = fadd2(b0, b1);
-    out[(size_t)ii * N] = sa.x + sa.y;
-    if (ii + 1 < ni) out[(size_t)(ii + 1) * N] = sb.x + sb.y;
+    out[(size_t)ii * Np] = sa.x + sa.y;
+    if (ii + 1 < ni) out[(size_t)(ii + 1) * Np] = sb.x + sb.y;
   }
 }
 
@@ -366,12 +380,12 @@ __device__ __forceinline__ void load_o8(const TO* p, float (&f)[8]) {
   }
 }
 
-template <typename T, typename TO, int D>
+template <typename T, typename TO, int D, bool RAG>
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const TO* __restrict__ o, const T* __restrict__ dO,
                                                        const float* __restrict__ lse, float* __restrict__ delta,
                                                        float* __restrict__ l2, int8_t* __restrict__ do_q,
                                                        float* __restrict__ do_scale, float* __restrict__ dq_acc,
-                                                       unsigned* __restrict__ dq_flags, IoLayout io, int nT) {
+                                                       unsigned* __restrict__ dq_flags, IoLayout io, int nT, int N) {
   constexpr int kGroups = D / kVec;            // threads per row
   constexpr int kRowsPerPass = 256 / kGroups;
   constexpr int kIters = kBlk / kRowsPerPass;
@@ -380,20 +394,27 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const TO* __restrict__ o,
   const int g = threadIdx.x % kGroups, r0 = threadIdx.x / kGroups;
   const size_t base = (size_t)blk * kBlk * D;                      // the contiguous buffers (dO^, dQ accumulator)
   const long long iob = io.row(blk / nT, (blk % nT) * (long long)kBlk);  // O and dO in the I/O layout
+  const int nv = RAG ? min(kBlk, N - (int)(blk % nT) * kBlk) : kBlk;  // rows this block holds (A33)
   float v[kIters][kVec];
   float amax = 0.f;
   // dO rows in flight before any arithmetic (kIters 16-byte loads per thread); O's alongside
   uint4 rdo[kIters];
 #pragma unroll
   for (int it = 0; it < kIters; ++it)
-    rdo[it] = *reinterpret_cast<const uint4*>(dO + iob + (r0 + it * kRowsPerPass) * io.sn + g * kVec);
+    rdo[it] = r0 + it * kRowsPerPass < nv ? *reinterpret_cast<const uint4*>(dO + iob + (r0 + it * kRowsPerPass) * io.sn + g * kVec)
+                                          : make_uint4(0, 0, 0, 0);
 #pragma unroll
   for (int it = 0; it < kIters; ++it) {
     const int r = r0 + it * kRowsPerPass;
     const size_t off = base + (size_t)r * D + g * kVec;
     float fo[kVec];
     unpack8<T>(rdo[it], v[it]);
-    load_o8<TO>(o + iob + r * io.sn + g * kVec, fo);
+    if (r < nv) {
+      load_o8<TO>(o + iob + r * io.sn + g * kVec, fo);
+    } else {
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) fo[e] = 0.f;
+    }
     double dot = 0.0;
 #pragma unroll
     for (int e = 0; e < kVec; ++e) {
@@ -403,9 +424,10 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const TO* __restrict__ o,
 #pragma unroll
     for (int s = kGroups / 2; s; s >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, s);
     if (g == 0) {
+      // padded rows (A33): delta 0 and L = +inf, so K4's P = 2^{t - L} and dS vanish on them
       const size_t row = (size_t)blk * kBlk + r;
       delta[row] = __double2float_rn(dot);
-      l2[row] = lse[row] * 1.4426950408889634f;
+      l2[row] = r < nv ? lse[(blk / nT) * (long long)N + (blk % nT) * kBlk + r] * 1.4426950408889634f : INFINITY;
     }
     *reinterpret_cast<float4*>(dq_acc + off) = make_float4(0.f, 0.f, 0.f, 0.f);
     *reinterpret_cast<float4*>(dq_acc + off + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -436,14 +458,16 @@ __global__ void fill_kernel(float* __restrict__ x, size_t n, float v) {
 }
 
 // 8 elements per thread, from the contiguous accumulator to dQ in the I/O layout (the I/O type, or fp32)
-template <typename T, bool F32>
+template <typename T, bool F32, bool RAG>
 __global__ void dq_finalize_kernel(const float* __restrict__ acc, void* __restrict__ dq, size_t n8, int N, int d,
                                    IoLayout io) {
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n8) return;
-  float4 a = reinterpret_cast<const float4*>(acc)[2 * i];
-  float4 b = reinterpret_cast<const float4*>(acc)[2 * i + 1];
   const size_t e = i * 8, row = e / d;
+  // the accumulator has Np rows per head (A33)
+  const size_t arow = RAG ? (row / N) * (size_t)padded_len(N) + row % N : row;
+  const float4* ap = reinterpret_cast<const float4*>(acc + arow * d + e % d);
+  const float4 a = ap[0], b = ap[1];
   const long long off = io.row((long long)(row / N), (long long)(row % N)) + (long long)(e % d);
   if constexpr (F32) {
     reinterpret_cast<float4*>(static_cast<float*>(dq) + off)[0] = a;
@@ -470,7 +494,8 @@ __global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__
   __shared__ float red[8][D];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const size_t blk = blockIdx.x;
-  const size_t row0 = blk * kBlk + warp * kRows;
+  const size_t row0 = blk * kBlk + warp * kRows;  // in the padded row space (Np rows per head, A33)
+  const int Np = padded_len(N);
   float gam[kPer], gacc[kPer];
 #pragma unroll
   for (int e = 0; e < kPer; ++e) {
@@ -481,8 +506,13 @@ __global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__
 #pragma unroll
   for (int rr = 0; rr < kRows; ++rr) {
     const size_t off = (row0 + rr) * D + lane * kPer;  // the contiguous fp32 dQ accumulator
-    const long long ioff = io.row((long long)((row0 + rr) / N), (long long)((row0 + rr) % N)) + lane * kPer;
+    const long long ioff = io.row((long long)((row0 + rr) / Np), (long long)((row0 + rr) % Np)) + lane * kPer;
     rs[rr] = rstd[row0 + rr];
+    if ((int)((row0 + rr) % Np) >= N) {  // a row the short last block lacks: no contribution
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) xv[rr][e] = dy[rr][e] = 0.f;
+      continue;
+    }
     if constexpr (kPer == 4) {
       const uint2 xu = *reinterpret_cast<const uint2*>(x + ioff);
       const float2 x0 = Io<T>::to2(*reinterpret_cast<const typename Io<T>::T2*>(&xu.x));
@@ -529,7 +559,8 @@ __global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__
   }
 #pragma unroll
   for (int rr = 0; rr < kRows; ++rr) {
-    const long long off = io.row((long long)((row0 + rr) / N), (long long)((row0 + rr) % N)) + lane * kPer;
+    if ((int)((row0 + rr) % Np) >= N) continue;
+    const long long off = io.row((long long)((row0 + rr) / Np), (long long)((row0 + rr) % Np)) + lane * kPer;
     const float mean = dot[rr] * (1.f / D);
     typename Io<T>::T2 h[kPer / 2];
 #pragma unroll
@@ -584,24 +615,35 @@ __global__ void dgamma_stage2_kernel(const double* __restrict__ part2, float* __
     }                                      \
   } while (0)
 
+#define SAGE_RAG_DISPATCH(N, ...)          \
+  do {                                     \
+    if ((N) % kBlk) {                      \
+      constexpr bool kRag = true;          \
+      __VA_ARGS__;                         \
+    } else {                               \
+      constexpr bool kRag = false;         \
+      __VA_ARGS__;                         \
+    }                                      \
+  } while (0)
+
 cudaError_t launch_colsum(const void* x, double* part, int BH, int N, int d, cudaStream_t s, NormIn nrm, bool fp16,
                           IoLayout io) {
-  const int nT = N / kBlk;
-  const unsigned grid = (unsigned)(BH * (N / kBlk));
-  SAGE_IO_DISPATCH(fp16, {
+  const int nT = num_blocks(N);
+  const unsigned grid = (unsigned)(BH * nT);
+  SAGE_IO_DISPATCH(fp16, SAGE_RAG_DISPATCH(N, {
     const IoT* xt = static_cast<const IoT*>(x);
     if (nrm.gamma) {
       if (d == 128)
-        colsum_kernel<IoT, 128, true><<<grid, 256, 0, s>>>(xt, part, nrm, io, nT);
+        colsum_kernel<IoT, 128, true, kRag><<<grid, 256, 0, s>>>(xt, part, nrm, io, nT, N);
       else
-        colsum_kernel<IoT, 64, true><<<grid, 256, 0, s>>>(xt, part, nrm, io, nT);
+        colsum_kernel<IoT, 64, true, kRag><<<grid, 256, 0, s>>>(xt, part, nrm, io, nT, N);
     } else {
       if (d == 128)
-        colsum_kernel<IoT, 128, false><<<grid, 256, 0, s>>>(xt, part, nrm, io, nT);
+        colsum_kernel<IoT, 128, false, kRag><<<grid, 256, 0, s>>>(xt, part, nrm, io, nT, N);
       else
-        colsum_kernel<IoT, 64, false><<<grid, 256, 0, s>>>(xt, part, nrm, io, nT);
+        colsum_kernel<IoT, 64, false, kRag><<<grid, 256, 0, s>>>(xt, part, nrm, io, nT, N);
     }
-  });
+  }));
   return cudaGetLastError();
 }
 
@@ -636,68 +678,68 @@ cudaError_t launch_colmean(const double* part, float* mu, int BH, int N, int d, 
 }
 
 cudaError_t launch_blockmean(const double* part, float* mu_q, int BH, int N, int d, cudaStream_t s) {
-  size_t n = (size_t)BH * (N / kBlk) * d;
-  blockmean_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(part, mu_q, n);
+  size_t n = (size_t)BH * num_blocks(N) * d;
+  blockmean_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(part, mu_q, n, d, N);
   return cudaGetLastError();
 }
 
 cudaError_t launch_quantize(const QuantJobs& jobs, int njobs, int BH, int N, int d, cudaStream_t s, bool fp16,
                             IoLayout io) {
-  int T = N / kBlk;
+  int T = num_blocks(N);
   dim3 grid((unsigned)(BH * T), (unsigned)njobs);
   bool qkn = false;
   for (int i = 0; i < njobs; ++i) qkn = qkn || jobs.j[i].gamma;
-  SAGE_IO_DISPATCH(fp16, {
+  SAGE_IO_DISPATCH(fp16, SAGE_RAG_DISPATCH(N, {
     if (qkn) {
       if (d == 128)
-        quantize_kernel<IoT, 128, true><<<grid, 256, 0, s>>>(jobs, T, io);
+        quantize_kernel<IoT, 128, true, kRag><<<grid, 256, 0, s>>>(jobs, T, io, N);
       else
-        quantize_kernel<IoT, 64, true><<<grid, 256, 0, s>>>(jobs, T, io);
+        quantize_kernel<IoT, 64, true, kRag><<<grid, 256, 0, s>>>(jobs, T, io, N);
     } else {
       if (d == 128)
-        quantize_kernel<IoT, 128, false><<<grid, 256, 0, s>>>(jobs, T, io);
+        quantize_kernel<IoT, 128, false, kRag><<<grid, 256, 0, s>>>(jobs, T, io, N);
       else
-        quantize_kernel<IoT, 64, false><<<grid, 256, 0, s>>>(jobs, T, io);
+        quantize_kernel<IoT, 64, false, kRag><<<grid, 256, 0, s>>>(jobs, T, io, N);
     }
-  });
+  }));
   return cudaGetLastError();
 }
 
 cudaError_t launch_qsmooth_bias(const void* k, const float* mu_k, const float* mu_q, float* bias, int BH, int N, int d,
                                 cudaStream_t s, NormIn nrm, bool fp16, IoLayout io) {
-  const int T = N / kBlk;
+  const int T = num_blocks(N);
   dim3 grid((unsigned)(BH * T), (unsigned)((T + kBiasI - 1) / kBiasI));
-  SAGE_IO_DISPATCH(fp16, {
+  SAGE_IO_DISPATCH(fp16, SAGE_RAG_DISPATCH(N, {
     const IoT* kt = static_cast<const IoT*>(k);
     if (d == 128)
-      qsmooth_bias_kernel<IoT, 128><<<grid, 128, 0, s>>>(kt, mu_k, mu_q, bias, N, nrm, io);
+      qsmooth_bias_kernel<IoT, 128, kRag><<<grid, 128, 0, s>>>(kt, mu_k, mu_q, bias, N, nrm, io);
     else
-      qsmooth_bias_kernel<IoT, 64><<<grid, 128, 0, s>>>(kt, mu_k, mu_q, bias, N, nrm, io);
-  });
+      qsmooth_bias_kernel<IoT, 64, kRag><<<grid, 128, 0, s>>>(kt, mu_k, mu_q, bias, N, nrm, io);
+  }));
   return cudaGetLastError();
 }
 
 cudaError_t launch_bwd_prep(const void* o, const void* dO, const float* lse, float* delta, float* l2, int8_t* do_q,
                             float* do_scale, float* dq_acc, int BH, int N, int d, cudaStream_t s, unsigned* dq_flags,
                             bool fp16, bool o_f32, IoLayout io) {
-  const int nT = N / kBlk;
-  unsigned grid = (unsigned)(BH * (N / kBlk));
-  SAGE_IO_DISPATCH(fp16, {
+  const int nT = num_blocks(N);
+  unsigned grid = (unsigned)(BH * nT);
+  SAGE_IO_DISPATCH(fp16, SAGE_RAG_DISPATCH(N, {
     const IoT* dot = static_cast<const IoT*>(dO);
     if (o_f32) {
       const float* ot = static_cast<const float*>(o);
       if (d == 128)
-        bwd_prep_kernel<IoT, float, 128><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags, io, nT);
+        bwd_prep_kernel<IoT, float, 128, kRag><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags, io, nT, N);
       else
-        bwd_prep_kernel<IoT, float, 64><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags, io, nT);
+        bwd_prep_kernel<IoT, float, 64, kRag><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags, io, nT, N);
     } else {
       const IoT* ot = static_cast<const IoT*>(o);
       if (d == 128)
-        bwd_prep_kernel<IoT, IoT, 128><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags, io, nT);
+        bwd_prep_kernel<IoT, IoT, 128, kRag><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags, io, nT, N);
       else
-        bwd_prep_kernel<IoT, IoT, 64><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags, io, nT);
+        bwd_prep_kernel<IoT, IoT, 64, kRag><<<grid, 256, 0, s>>>(ot, dot, lse, delta, l2, do_q, do_scale, dq_acc, dq_flags, io, nT, N);
     }
-  });
+  }));
   return cudaGetLastError();
 }
 
@@ -711,10 +753,10 @@ cudaError_t launch_dq_finalize(const float* dq_acc, void* dq, int BH, int N, int
   const size_t n8 = (size_t)BH * N * d / 8;
   const unsigned grid = (unsigned)((n8 + 255) / 256);
   if (f32) {
-    dq_finalize_kernel<float, true><<<grid, 256, 0, s>>>(dq_acc, dq, n8, N, d, io);
+    SAGE_RAG_DISPATCH(N, dq_finalize_kernel<float, true, kRag><<<grid, 256, 0, s>>>(dq_acc, dq, n8, N, d, io));
     return cudaGetLastError();
   }
-  SAGE_IO_DISPATCH(fp16, dq_finalize_kernel<IoT, false><<<grid, 256, 0, s>>>(dq_acc, dq, n8, N, d, io));
+  SAGE_IO_DISPATCH(fp16, SAGE_RAG_DISPATCH(N, dq_finalize_kernel<IoT, false, kRag><<<grid, 256, 0, s>>>(dq_acc, dq, n8, N, d, io)));
   return cudaGetLastError();
 }
 

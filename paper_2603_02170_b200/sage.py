@@ -189,11 +189,13 @@ class SageCtx:
         return torch.float16 if self.params.flags & SAGE_FP16 else torch.bfloat16
 
     def view(self):
-        """Device tensors of the context (Q^, K^, scales, mu_K, mu_Q, bias) -- no copies."""
+        """Device tensors of the context (Q^, K^, scales, mu_K, mu_Q, bias) -- no copies.  The per-row
+        buffers have Np = 128 ceil(N / 128) rows per head (N ragged: rows N.. are padding, reading A33)."""
         v = SageCtxView()
         _check(lib().sage_ctx_get_view(ctypes.byref(self.params), _ptr(self.buf), ctypes.byref(v)), "ctx_view")
         B, H, N, d = self.shape
-        T = N // 128
+        T = -(-N // 128)
+        N = T * 128
         base = self.buf.data_ptr()
 
         def sl(addr, n, dtype, shape):
@@ -270,7 +272,7 @@ def forward(q, k, v, causal=False, k_smooth=True, q_smooth=False, softmax_scale=
                     pv_fp8=pv_fp8, strides=strides)
     nctx = lib().sage_ctx_bytes(ctypes.byref(p))
     if nctx == 0:
-        raise SageError(f"unsupported shape/flags {tuple(q.shape)} (N % 128 == 0, d in {{64, 128}})")
+        raise SageError(f"unsupported shape/flags {tuple(q.shape)} (1 <= N <= 32768, d in {{64, 128}})")
     with torch.cuda.device(dev):
         o = torch.empty_strided(q.shape, q.stride(), dtype=_out_dtype(q.dtype, fp32_out), device=dev) \
             if out is None else out
@@ -451,6 +453,8 @@ def debug_dump(heads, N, device, d=None, acc=False):
         _check(lib().sage_debug_dump(None, None, None, None, None, 0), "sage_debug_dump")
         _check(lib().sage_debug_dump_acc(None, None, None, None, None), "sage_debug_dump_acc")
         return None
+    if N % 128:
+        raise SageError("the tile dumps need N % 128 == 0")
     T = N // 128
     bufs = dict(p_hat_t=torch.zeros((heads, N, N), dtype=torch.int8, device=device),
                 s_p=torch.zeros((heads, T, T), dtype=torch.float32, device=device),
@@ -478,6 +482,8 @@ def debug_fwd_dump(heads, N, d, device):
     if heads == 0:
         _check(lib().sage_debug_fwd_dump(None, None, None, None, 0), "sage_debug_fwd_dump")
         return None
+    if N % 128:
+        raise SageError("the tile dumps need N % 128 == 0")
     T = N // 128
     bufs = dict(s=torch.zeros((heads, N, N), dtype=torch.int32, device=device),
                 p_hat=torch.zeros((heads, N, N), dtype=torch.uint8, device=device),

@@ -36,10 +36,15 @@ def test_sizes_and_invalid_params(L):
     pq = make_params(2, 3, 256, 64, q_smooth=True)
     assert L.sage_ctx_bytes(ctypes.byref(pq)) > nctx  # + mu_Q and the bias
     assert L.sage_workspace_bytes(ctypes.byref(p), 1) >= 2 * 3 * 256 * 64 * 4  # fp32 dQ accumulator
-    for bad in (make_params(1, 1, 100, 64), make_params(1, 1, 128, 96), make_params(0, 1, 128, 64),
-                make_params(1, 1, 128, 64, softmax_scale=-1.0)):
+    for bad in (make_params(1, 1, 0, 64), make_params(1, 1, 32769, 64), make_params(1, 1, 128, 96),
+                make_params(0, 1, 128, 64), make_params(1, 1, 128, 64, softmax_scale=-1.0)):
         assert L.sage_ctx_bytes(ctypes.byref(bad)) == 0
         assert L.sage_workspace_bytes(ctypes.byref(bad), 0) == 0
+    # a ragged N (reading A33) is valid: the library's buffers pad each head to 128 ceil(N / 128) rows
+    pr, pp = make_params(2, 3, 200, 64, q_smooth=True), make_params(2, 3, 256, 64, q_smooth=True)
+    assert L.sage_ctx_bytes(ctypes.byref(pr)) == L.sage_ctx_bytes(ctypes.byref(pp))
+    assert L.sage_workspace_bytes(ctypes.byref(pr), 1) == L.sage_workspace_bytes(ctypes.byref(pp), 1)
+    assert L.sage_ctx_bytes(ctypes.byref(make_params(1, 1, 1, 128))) == L.sage_ctx_bytes(ctypes.byref(make_params(1, 1, 128, 128)))
     bad = make_params(1, 1, 128, 64)
     bad.flags = 1 << 12
     assert L.sage_ctx_bytes(ctypes.byref(bad)) == 0
@@ -64,7 +69,7 @@ def test_params_tag(L):
               make_params(2, 3, 256, 64, causal=True, strides=(256 * 3 * 64, 64, 3 * 64))]
     tags = {L.sage_params_tag(ctypes.byref(o)) for o in others}
     assert t0 not in tags and len(tags) == len(others)
-    assert L.sage_params_tag(ctypes.byref(make_params(1, 1, 100, 64))) == 0
+    assert L.sage_params_tag(ctypes.byref(make_params(1, 1, 128, 96))) == 0
 
 
 def test_stride_validation(L):
@@ -91,7 +96,7 @@ def test_error_paths_do_not_launch(L):
     mis = ctypes.c_void_p(0x10008)
     z = ctypes.c_void_p(0)
     S = ctypes.c_size_t
-    bad = make_params(1, 2, 200, 64)
+    bad = make_params(1, 2, 256, 96)
     C = _ctx(0x10000, nctx)
     assert L.sage_fwd(ctypes.byref(bad), A, A, A, A, A, C, A, S(nws), z) == 1
     assert L.sage_fwd(ctypes.byref(p), z, A, A, A, A, C, A, S(nws), z) == 1
