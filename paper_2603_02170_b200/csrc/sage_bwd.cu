@@ -108,6 +108,10 @@ struct BwdSmem {
 #define SAGE_K4_DVDP 0  // d=128: the dV tile on dP's columns, so S_{i+1} goes out as soon as S_i is in
                         // registers (1; C4 K4 +1.4%, C3 -1.6%: DESIGN.md 7.3), or on S's (0)
 #endif
+#ifndef SAGE_K4_EXPIPE
+#define SAGE_K4_EXPIPE 1  // P = 2^t for the first 32 columns before the tile-max barrier and the dP wait, the
+                          // second 32 interleaved with the first chunk's dS work (0: each chunk's 32 after its dP load)
+#endif
 #ifndef SAGE_TRACE
 #define SAGE_TRACE 0
 #endif
@@ -644,6 +648,12 @@ if (cm) {
 #pragma unroll
       for (int e = 0; e < 64; e += 4) tmax = fmaxf(tmax, fmax3(t[e], t[e + 1], fmaxf(t[e + 2], t[e + 3])));
       if (kv_missing) tmax = -INFINITY;
+      if constexpr (SAGE_K4_EXPIPE) {
+        // P = 2^t does not depend on the tile max: the first chunk's exponentials overlap the barrier below
+        // and the dP wait
+#pragma unroll
+        for (int u = 0; u < (SAGE_K4_EXPIPE == 2 ? 64 : 32); ++u) t[u] = ex2(t[u]);
+      }
 
       // -- step 2: psi(P) scale over the tile: amax = max P = 2^max(t)  (line 6, reading A11)
       if (threadIdx.x == 128) TR(19, it);
@@ -679,9 +689,11 @@ if (cm) {
       for (int cc = 0; cc < 2; ++cc) {
         uint32_t v[32];
         tmem_ld32(tDP + qc0 + cc * 32 + lane_off, v);
-        // the chunk's 32 exponentials first: back-to-back MUFU work while the TMEM load lands
+        if constexpr (!SAGE_K4_EXPIPE) {
+          // the chunk's 32 exponentials first: back-to-back MUFU work while the TMEM load lands
 #pragma unroll
-        for (int u = 0; u < 32; ++u) t[cc * 32 + u] = ex2(t[cc * 32 + u]);
+          for (int u = 0; u < 32; ++u) t[cc * 32 + u] = ex2(t[cc * 32 + u]);
+        }
         tmem_wait_ld();
         if (DUMPING && g_dacc.dp)
           dump_words(reinterpret_cast<int32_t*>(g_dacc.dp) + ((size_t)bh * N + j * kBlk + r) * N + i * kBlk + qc0 + cc * 32,
@@ -693,6 +705,10 @@ if (cm) {
           for (int e4 = 0; e4 < 4; ++e4) {
             const int ev = c16 * 16 + e4 * 4;  // index into v
             const int e = cc * 32 + ev;        // index into t
+            if (SAGE_K4_EXPIPE == 1 && cc == 0) {  // the second chunk's exponentials, 4 per group of this one
+#pragma unroll
+              for (int u = 0; u < 4; ++u) t[32 + ev + u] = ex2(t[32 + ev + u]);
+            }
             const float4 d4 = Ds4[e / 4];
             float2 qa = ffma2(make_float2(t[e], t[e + 1]), make_float2(inv_p, inv_p), make_float2(kMagic, kMagic));
             float2 qb = ffma2(make_float2(t[e + 2], t[e + 3]), make_float2(inv_p, inv_p), make_float2(kMagic, kMagic));

@@ -270,6 +270,11 @@ def forward(q, k, v, causal=False, k_smooth=True, q_smooth=False, softmax_scale=
     p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8, deterministic=deterministic,
                     p_colscale=p_colscale, fine_bwd=fine_bwd, fp16=q.dtype == torch.float16, fp32_out=fp32_out,
                     pv_fp8=pv_fp8, strides=strides)
+    if q.numel() == 0 and d in (64, 128):
+        # empty batch, heads or sequence: nothing to compute (the C ABI rejects empty shapes), empty results
+        o = torch.empty_strided(q.shape, q.stride(), dtype=_out_dtype(q.dtype, fp32_out), device=dev)
+        return o, torch.empty((B, H, N), dtype=torch.float32, device=dev), \
+            SageCtx(p, torch.empty(0, dtype=torch.uint8, device=dev), (B, H, N, d), q.stride())
     nctx = lib().sage_ctx_bytes(ctypes.byref(p))
     if nctx == 0:
         raise SageError(f"unsupported shape/flags {tuple(q.shape)} (1 <= N <= 32768, d in {{64, 128}})")
@@ -303,6 +308,9 @@ def backward(ctx, v, o, lse, do, dq=None, dk=None, dv=None, workspace=None, stre
     _check_out(o, ctx.shape, ctx.out_dtype, dev, "o", st)
     _check_out(lse, (B, H, N), torch.float32, dev, "lse")
     v, do = _to_layout(v, st), _to_layout(do, st)  # the forward's layout (a copy only if it differs)
+    if do.numel() == 0:  # the empty forward's context: empty gradients
+        mk = lambda: torch.empty_strided(ctx.shape, st, dtype=ctx.out_dtype, device=dev)
+        return mk(), mk(), mk()
     with torch.cuda.device(dev):
         mk = lambda: torch.empty_strided(ctx.shape, st, dtype=ctx.out_dtype, device=dev)
         dq = mk() if dq is None else dq

@@ -174,3 +174,18 @@ def test_ragged_degenerate_lengths():
             scale = max(np.abs(round_bf16(ref)).max(), 1e-3)
             assert np.abs(got - round_bf16(ref)).max() <= 2e-2 * scale, (N, name)
         assert np.abs(f64(gpu["lse"]).reshape(2, N) - f["lse"]).max() <= 1e-5
+
+
+@pytest.mark.parametrize("shape", [(0, 2, 256, 64), (1, 0, 256, 128), (1, 2, 0, 64)])
+def test_empty_inputs(shape):
+    """An empty batch, head count or sequence: empty results of the right shapes, forward and backward, and the
+    autograd path; nothing is launched (the C ABI rejects empty shapes, so the binding returns early)."""
+    q, k, v, do = (torch.zeros(shape, dtype=torch.bfloat16, device="cuda") for _ in range(4))
+    o, lse, ctx = sage.forward(q, k, v, causal=True)
+    assert o.shape == shape and lse.shape == shape[:3]
+    dq, dk, dv = sage.backward(ctx, v, o, lse, do)
+    assert dq.shape == dk.shape == dv.shape == shape
+    qa = q.clone().requires_grad_()
+    out = sage.sage_attention(qa, k, v, causal=True)
+    out.sum().backward()
+    assert out.shape == shape and qa.grad.shape == shape
