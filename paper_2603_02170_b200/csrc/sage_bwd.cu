@@ -18,14 +18,16 @@
 //                 tile (t -> P -> dS in place), so their TMEM columns free up immediately and
 //                 the next tile's MMAs overlap this tile's softmax / quantisation.
 //   warps 12-15   drain warpgroup: the per-tile scales forbid int32 accumulation across
-//                 tiles, so every dV/dK/dQ int32 tile is converted and scaled here while the
-//                 compute warpgroups already work on the next tile.  dK_j (and dV_j for d=64)
-//                 accumulate in fp32 registers; for d=128 dV_j accumulates in fp32 TMEM.
-//                 dQ_i is reduced across key blocks with a TMA reduce-add (cp.reduce.async.bulk.tensor
-//                 .add, fp32) per drain warp, finalised by K5.
-// TMEM (512 columns):  d=64 : S 0 | dP 128 | dV 256 | dK 320 | dQ 384
-//                      d=128: S/dV 0 | dP/dK 128 | dQ 256 | dV fp32 accumulator 384
-//   (d=128 aliases the dV tile onto S and the dK tile onto dP; the MMA issuer orders them.)
+//                 tiles, so every dK/dQ (and, for d=64, dV) int32 tile is converted and scaled
+//                 here while the compute warpgroups already work on the next tile.  dK_j (and
+//                 dV_j for d=64) accumulate in fp32 registers; for d=128 the compute warps drain
+//                 the dV tile into an fp32 accumulator in TMEM.  dQ_i is reduced across key blocks
+//                 with a TMA reduce-add (cp.reduce.async.bulk.tensor .add, fp32) per drain warp,
+//                 finalised by K5.
+// TMEM (512 columns):  d=64 : S 0 | dP 128 | dV 256 | dK 320 | dQ 384 | V_j (bf16) 448 | P^^T 480
+//                      d=128: S/dV 0 | dP 128 | dK, then dQ 256 | dV fp32 accumulator 384
+//   (d=128 aliases the dV tile onto S, and dK_i and dQ_i take turns in the third region
+//   (SAGE_K4_DKQ128); the MMA issuer orders them through the drain barriers.)
 #include "sage_internal.h"
 #include "sm100.cuh"
 
