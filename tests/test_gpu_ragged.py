@@ -189,3 +189,27 @@ def test_empty_inputs(shape):
     out = sage.sage_attention(qa, k, v, causal=True)
     out.sum().backward()
     assert out.shape == shape and qa.grad.shape == shape
+
+
+def test_ragged_max_length_sampled():
+    """N = 32767 (the largest ragged length: 256 blocks, the last one 127 rows) against the oracle on sampled
+    blocks of one head, with Q-smoothing: query blocks {0, 131, 255} (O, L, dQ; 255 is the short block) and
+    key blocks {254, 255} (dK, dV); the oracle's sampled mode runs the same tiles as a full run."""
+    B, H, N, d = 1, 1, 32767, 128
+    q, k, v, do = make_inputs(B, H, N, d, "outlier_kq", seed=2600)
+    gpu = _run(q, k, v, do, True, True, True)
+    qb, kb = [0, 131, 255], [254, 255]
+    need = sorted(set(qb) | set(range(254, 256)))
+    flat = lambda t: f64(t).reshape(1, N, d)
+    oracle.set_threads(8)
+    kw = dict(causal=True, k_smooth=True, q_smooth=True)
+    f = oracle.fwd(flat(q), flat(k), flat(v), q_blocks=need, **kw)
+    b = oracle.bwd(flat(q), flat(k), flat(v), round_bf16(f["o"]), flat(do), f["lse"], q_blocks=qb, k_blocks=kb, **kw)
+    rows = lambda bl: np.concatenate([np.arange(i * 128, min((i + 1) * 128, N)) for i in bl])
+    for name, ref, r in (("o", f["o"], rows(qb)), ("dq", b["dq"], rows(qb)), ("dk", b["dk"], rows(kb)),
+                         ("dv", b["dv"], rows(kb))):
+        got = flat(gpu[name])[0][r]
+        want = round_bf16(ref[0][r])
+        assert rel_l2(want, got) <= REL_TOL and cos_sim(want, got) >= COS_TOL, (name, rel_l2(want, got))
+    lse = f64(gpu["lse"]).reshape(N)[rows(qb)]
+    assert np.abs(lse - f["lse"][0][rows(qb)]).max() <= 1e-5
