@@ -213,3 +213,15 @@ def test_ragged_max_length_sampled():
         assert rel_l2(want, got) <= REL_TOL and cos_sim(want, got) >= COS_TOL, (name, rel_l2(want, got))
     lse = f64(gpu["lse"]).reshape(N)[rows(qb)]
     assert np.abs(lse - f["lse"][0][rows(qb)]).max() <= 1e-5
+
+
+def test_ragged_deterministic_noncausal():
+    """SAGE_DETERMINISTIC's rotated non-causal order (CTA j visits query blocks (j + it) mod T, T = ceil(N/128)) at
+    a ragged N: within the tolerance of the oracle, and dQ bitwise identical across two runs."""
+    B, H, N, d = 1, 2, 300, 64
+    q, k, v, do = make_inputs(B, H, N, d, "qknorm", seed=2700)
+    runs = [_run(q, k, v, do, False, True, False, deterministic=True) for _ in range(2)]
+    assert torch.equal(runs[0]["dq"], runs[1]["dq"])
+    heads = list(range(B * H))
+    f, b = _oracle(q, k, v, do, heads, False, True, False)
+    _assert_ok(_compare(runs[0], f, b, heads, B, H, N, d), "det ragged")

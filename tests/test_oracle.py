@@ -170,22 +170,27 @@ def test_tiled_quant_off_equals_fpa(orc, causal, smooth, N, blk):
 
 
 # --------------------------------------------------------------------------- ragged N (reading A33)
-@pytest.mark.parametrize("N,d", [(200, 64), (300, 128), (129, 64)])
-def test_ragged_causal_prefix(orc, N, d):
+@pytest.mark.parametrize("N,d,mode", [(200, 64, "int8"), (300, 128, "int8"), (129, 64, "int8"), (200, 64, "p_u8"),
+                                      (300, 64, "pv_fp8"), (200, 64, "p_col"), (300, 64, "ds_fine")])
+def test_ragged_causal_prefix(orc, N, d, mode):
     """A causal ragged-N run is the first N rows of the padded run: zero rows appended to Q, K, V and dO
     change no block's psi scale (amax over zeros), and causal rows never see the later keys, so O, L, dQ and
-    dK of the first N rows are bit-identical; dV only through the P^ tile scales (padded queries)."""
+    dK of the first N rows are bit-identical; dV only through the P^ tile scales (padded queries).  The same
+    holds in every variant mode (P_U8, PV_FP8, P_COL, DS_FINE: the padded queries' dS is 0)."""
     rng = np.random.default_rng(N)
     BH, Np = 2, -(-N // 128) * 128
     q, k, v, do = (_rand(rng, BH, N, d) for _ in range(4))
     pad = lambda x: np.concatenate([x, np.zeros((BH, Np - N, d))], 1)
-    f = orc.fwd(q, k, v, causal=True, k_smooth=False)
-    fp = orc.fwd(pad(q), pad(k), pad(v), causal=True, k_smooth=False)
+    fkw = dict(causal=True, k_smooth=False, p_u8=mode == "p_u8", pv_fp8=mode == "pv_fp8")
+    bkw = dict(causal=True, k_smooth=False, p_u8=mode == "p_u8", p_col=mode in ("p_col", "ds_fine"),
+               ds_fine=mode == "ds_fine")
+    f = orc.fwd(q, k, v, **fkw)
+    fp = orc.fwd(pad(q), pad(k), pad(v), **fkw)
     np.testing.assert_array_equal(f["o"], fp["o"][:, :N])
     np.testing.assert_array_equal(f["lse"], fp["lse"][:, :N])
     np.testing.assert_array_equal(f["sq"], fp["sq"])
-    b = orc.bwd(q, k, v, f["o"], do, f["lse"], causal=True, k_smooth=False)
-    bp = orc.bwd(pad(q), pad(k), pad(v), fp["o"], pad(do), fp["lse"], causal=True, k_smooth=False)
+    b = orc.bwd(q, k, v, f["o"], do, f["lse"], **bkw)
+    bp = orc.bwd(pad(q), pad(k), pad(v), fp["o"], pad(do), fp["lse"], **bkw)
     np.testing.assert_array_equal(b["dq"], bp["dq"][:, :N])
     np.testing.assert_array_equal(b["dk"], bp["dk"][:, :N])
     assert rel_l2(bp["dv"][:, :N], b["dv"]) < 2e-3
