@@ -114,6 +114,11 @@ struct BwdSmem {
 #define SAGE_K4_EXPIPE 1  // P = 2^t for the first 32 columns before the tile-max barrier and the dP wait, the
                           // second 32 interleaved with the first chunk's dS work (0: each chunk's 32 after its dP load)
 #endif
+#ifndef SAGE_K4_TAIL_MAXT
+#define SAGE_K4_TAIL_MAXT 32  // d=128, T <= this (N <= 4K): the TAIL instantiation (below), where the CTA's tail is a
+                              // large share of its time (measured: S1K K4 -3.7%, S2K -2.4%; at C4 its extra
+                              // register pressure costs +1%, so long sequences keep the plain kernel)
+#endif
 #ifndef SAGE_TRACE
 #define SAGE_TRACE 0
 #endif
@@ -164,7 +169,9 @@ __device__ __forceinline__ float compute_max(float v, int* red, int cw, int id) 
 // VAR: 0 the default path, 1 SAGE_DETERMINISTIC, 2 SAGE_P_COLSCALE, 3 SAGE_FINE_BWD (per-key psi(P),
 // per-key dS^ for dK, per-query dS^ for dQ) -- separate instantiations, because compiling the
 // variants' logic into the default kernel costs 2-8% (measured)
-template <int D, bool CAUSAL, bool QSMOOTH, int VAR>
+// TAIL: d=128, the compute warps, idle once their last tile is done, store dV_j and drain half of the last
+// dQ tile, shortening the CTA's tail (the drain warps keep dK_j and dQ's other half)
+template <int D, bool CAUSAL, bool QSMOOTH, int VAR, bool TAIL>
 __global__ void __launch_bounds__(kThreads, 1)
     sage_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_doq, const __grid_constant__ CUtensorMap tm_v,
@@ -290,6 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tS = tmem;
   const uint32_t tDP = tmem + 128;
   constexpr bool kDvDp = kAlias && SAGE_K4_DKQ128 && SAGE_K4_DVDP;
+  constexpr bool kTail = TAIL && kAlias && SAGE_K4_DKQ128 && !kDvDp && (VAR == 0 || VAR == 2);
   const uint32_t tDV = kAlias ? (kDvDp ? tmem + 128 : tmem) : tmem + 256;
   // d=128: dK_i and then dQ_i take turns in the third region, so dP_{i+1} never waits for the dK drain
   constexpr bool kDkQ = kAlias && SAGE_K4_DKQ128;
@@ -863,6 +871,62 @@ if (cm) {
         warp_arrive(dv_drained);
       }
     }
+    if constexpr (kTail) {
+      // the CTA's tail: this warpgroup's 64 columns of dV_j -> the output, from the fp32 TMEM accumulator
+      {
+        const long long orow = io.row(bh, (long long)j * kBlk + r) + qc0;
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t a[32];
+          tmem_ld32(tDVacc + qc0 + c0 + lane_off, a);
+          tmem_wait_ld();
+          if (r >= kv_valid) continue;  // a key the short last block lacks (A33)
+          if (f32out) {
+#pragma unroll
+            for (int e4 = 0; e4 < 32; e4 += 4)
+              *reinterpret_cast<uint4*>(static_cast<float*>(dv_out) + orow + c0 + e4) =
+                  make_uint4(a[e4], a[e4 + 1], a[e4 + 2], a[e4 + 3]);
+          } else {
+#pragma unroll
+            for (int e8 = 0; e8 < 32; e8 += 8) {
+              uint32_t hv[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                hv[e] = pack2_io(__uint_as_float(a[e8 + 2 * e]), __uint_as_float(a[e8 + 2 * e + 1]), fp16);
+              *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dv_out) + orow + c0 + e8) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+            }
+          }
+        }
+      }
+      // ... and columns 64 + 32 wg .. 64 + 32 wg + 31 of the last dQ tile (its 32 query rows): scaled into a 4 KB
+      // swizzled box in the P^^T / dS^^T buffers (free: their last readers, dV and dQ, have completed), then one
+      // TMA reduce-add, exactly as the drain warps do with columns 0..63
+      const int itl = n_it - 1, il = i_of(itl);
+      mbar_wait(dkq_full, itl & 1);
+      tc_fence_after();
+      const float s_ds = __fdiv_rn(scl[(itl & 3) * 2 + 1], 127.f);  // the tile's psi(dS) max, as the drain reads it
+      const float2 f = make_float2(s_ds * sk * tau, s_ds * sk * tau);
+      const int c0 = 64 + 32 * wg;
+      uint8_t* box = smem + (wg ? L::kDSt : L::kPt) + (warp % 4) * L::kDqBox;
+      uint32_t v[32];
+      tmem_ld32(tDQ + c0 + lane_off, v);
+      tmem_wait_ld();
+      if (DUMPING && g_dacc.dq) dump_words(g_dacc.dq + (((size_t)bh * T + j) * N + il * kBlk + r) * D + c0, v, 32);
+#pragma unroll
+      for (int e = 0; e < 32; e += 4) {
+        float2 a = fmul2(i2f2(v[e], v[e + 1], one), f);
+        float2 b = fmul2(i2f2(v[e + 2], v[e + 3], one), f);
+        *reinterpret_cast<float4*>(box + sw_offset(lane, e / 4, 128)) = make_float4(a.x, a.y, b.x, b.y);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_reduce_add_2d(&tm_dq, box, c0, bh * Np + il * kBlk + (warp % 4) * 32);
+        bulk_commit();
+        bulk_wait_all();  // the staging box must outlive the reduce
+      }
+      __syncwarp();
+    }
   } else {
     reg_set<kRegDrain, 65536 / kThreads>();
     // ------------------------------------------------------------ drain warpgroup (128 threads)
@@ -974,8 +1038,11 @@ if (cm) {
           if (lane == 0) flag_wait_geq(flag, (unsigned)((i - j + T) % T));
           __syncwarp();
         }
+        // SAGE_K4_TAIL: the compute warps take the last tile's columns 64..127
+        const int n_rounds = (kTail && it == n_it - 1) ? L::kDqRounds / 2 : L::kDqRounds;
 #pragma unroll
         for (int qq = 0; qq < L::kDqRounds; ++qq) {
+          if (qq >= n_rounds) break;
           const int rnd = it * L::kDqRounds + qq;
           uint8_t* stage = wstage + (rnd % L::kDqBufs) * L::kDqBoxes * L::kDqBox;
           if (lane == 0 && rnd >= L::kDqBufs) bulk_wait_read<L::kDqBufs - 1>();  // round rnd-kDqBufs has read `stage`
@@ -1021,10 +1088,29 @@ if (cm) {
       if (threadIdx.x == 384) TR(13, it);
     }
     if (lane == 0) bulk_wait_all();  // staging smem must outlive this warp's in-flight reduces
-    if constexpr (kAlias) {  // the compute warps' last dV accumulation
+    if constexpr (kAlias && !kTail) {  // the compute warps' last dV accumulation
       mbar_wait(dv_drained, (n_it - 1) & 1);
       tc_fence_after();
     }
+    if constexpr (kTail) {
+      // dK_j rows only: the compute warps store dV_j (SAGE_K4_TAIL)
+      if (r < kv_valid) {
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 8) {
+          if (f32out) {
+            *reinterpret_cast<float4*>(static_cast<float*>(dk_out) + orow + c0) =
+                make_float4(dk_acc[c0], dk_acc[c0 + 1], dk_acc[c0 + 2], dk_acc[c0 + 3]);
+            *reinterpret_cast<float4*>(static_cast<float*>(dk_out) + orow + c0 + 4) =
+                make_float4(dk_acc[c0 + 4], dk_acc[c0 + 5], dk_acc[c0 + 6], dk_acc[c0 + 7]);
+          } else {
+            uint32_t hk[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) hk[e] = pack2_io(dk_acc[c0 + 2 * e], dk_acc[c0 + 2 * e + 1], fp16);
+            *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dk_out) + orow + c0) = make_uint4(hk[0], hk[1], hk[2], hk[3]);
+          }
+        }
+      }
+    } else {
     // epilogue: dK_j, dV_j rows -> bf16 (not the rows a short last block lacks, A33)
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 32) {
@@ -1066,6 +1152,7 @@ if (cm) {
         *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dv_out) + orow + c0 + e8) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
       }
     }
+    }
   }
   __syncwarp();
   tc_fence_before();
@@ -1076,9 +1163,9 @@ if (cm) {
   }
 }
 
-template <int D, bool C, bool QS, int VAR>
-cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
-  auto kern = sage_bwd_kernel<D, C, QS, VAR>;
+template <int D, bool C, bool QS, int VAR, bool TAIL>
+cudaError_t launch_tt(const BwdArgs& a, cudaStream_t s) {
+  auto kern = sage_bwd_kernel<D, C, QS, VAR, TAIL>;
   constexpr int kSmem = BwdSmem<D, VAR == 3>::kAlloc;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
   if (e != cudaSuccess) return e;
@@ -1102,6 +1189,13 @@ cudaError_t set_bwd_dump_acc(int32_t* s_t, int32_t* dv_t, int32_t* dk_t, int32_t
 cudaError_t read_bwd_trace(void* host, size_t bytes) {
   if (bytes > sizeof(g_trace)) bytes = sizeof(g_trace);
   return cudaMemcpyFromSymbol(host, g_trace, bytes);
+}
+
+template <int D, bool C, bool QS, int VAR>
+cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
+  if constexpr (D == 128 && (VAR == 0 || VAR == 2))
+    if (num_blocks(a.N) <= SAGE_K4_TAIL_MAXT) return launch_tt<D, C, QS, VAR, true>(a, s);
+  return launch_tt<D, C, QS, VAR, false>(a, s);
 }
 
 template <int D, int VAR>
