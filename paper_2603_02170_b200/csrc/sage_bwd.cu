@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tS = tmem;
   const uint32_t tDP = tmem + 128;
   constexpr bool kDvDp = kAlias && SAGE_K4_DKQ128 && SAGE_K4_DVDP;
-  constexpr bool kTail = TAIL && kAlias && SAGE_K4_DKQ128 && !kDvDp && (VAR == 0 || VAR == 2);
+  constexpr bool kTail = TAIL && (VAR == 0 || VAR == 2) && (!kAlias || (SAGE_K4_DKQ128 && !kDvDp));
   const uint32_t tDV = kAlias ? (kDvDp ? tmem + 128 : tmem) : tmem + 256;
   // d=128: dK_i and then dQ_i take turns in the third region, so dP_{i+1} never waits for the dK drain
   constexpr bool kDkQ = kAlias && SAGE_K4_DKQ128;
@@ -872,8 +872,8 @@ if (cm) {
       }
     }
     if constexpr (kTail) {
-      // the CTA's tail: this warpgroup's 64 columns of dV_j -> the output, from the fp32 TMEM accumulator
-      {
+      // the CTA's tail: (d=128) this warpgroup's 64 columns of dV_j -> the output, from the fp32 TMEM accumulator
+      if constexpr (kAlias) {
         const long long orow = io.row(bh, (long long)j * kBlk + r) + qc0;
 #pragma unroll
         for (int c0 = 0; c0 < 64; c0 += 32) {
@@ -898,16 +898,18 @@ if (cm) {
           }
         }
       }
-      // ... and columns 64 + 32 wg .. 64 + 32 wg + 31 of the last dQ tile (its 32 query rows): scaled into a 4 KB
-      // swizzled box in the P^^T / dS^^T buffers (free: their last readers, dV and dQ, have completed), then one
-      // TMA reduce-add, exactly as the drain warps do with columns 0..63
+      // ... and the second half of the last dQ tile's columns (d=128: 64 + 32 wg .., both warpgroups; d=64: 32 ..,
+      // warpgroup 1) for this warp's 32 query rows: scaled into a 4 KB swizzled box in the P^^T / dS^^T buffers
+      // (free: their last readers, the dV / dK / dQ MMAs, have completed), then one TMA reduce-add, exactly as
+      // the drain warps do with the first half
+      if (kAlias || wg == 1) {
       const int itl = n_it - 1, il = i_of(itl);
       mbar_wait(dkq_full, itl & 1);
       tc_fence_after();
       const float s_ds = __fdiv_rn(scl[(itl & 3) * 2 + 1], 127.f);  // the tile's psi(dS) max, as the drain reads it
       const float2 f = make_float2(s_ds * sk * tau, s_ds * sk * tau);
-      const int c0 = 64 + 32 * wg;
-      uint8_t* box = smem + (wg ? L::kDSt : L::kPt) + (warp % 4) * L::kDqBox;
+      const int c0 = kAlias ? 64 + 32 * wg : 32;
+      uint8_t* box = smem + ((kAlias && !wg) ? L::kPt : L::kDSt) + (warp % 4) * L::kDqBox;
       uint32_t v[32];
       tmem_ld32(tDQ + c0 + lane_off, v);
       tmem_wait_ld();
@@ -926,6 +928,7 @@ if (cm) {
         bulk_wait_all();  // the staging box must outlive the reduce
       }
       __syncwarp();
+      }
     }
   } else {
     reg_set<kRegDrain, 65536 / kThreads>();
@@ -1092,8 +1095,8 @@ if (cm) {
       mbar_wait(dv_drained, (n_it - 1) & 1);
       tc_fence_after();
     }
-    if constexpr (kTail) {
-      // dK_j rows only: the compute warps store dV_j (SAGE_K4_TAIL)
+    if constexpr (kTail && kAlias) {
+      // dK_j rows only: the compute warps store dV_j (TAIL)
       if (r < kv_valid) {
 #pragma unroll
         for (int c0 = 0; c0 < D; c0 += 8) {
@@ -1193,6 +1196,8 @@ cudaError_t read_bwd_trace(void* host, size_t bytes) {
 
 template <int D, bool C, bool QS, int VAR>
 cudaError_t launch_t(const BwdArgs& a, cudaStream_t s) {
+  // (d=64 has the same tail path -- half of the last dQ tile by compute warpgroup 1 -- but measured neutral at
+  // C2, 0.495 vs 0.494-0.500 ms, so it is not instantiated)
   if constexpr (D == 128 && (VAR == 0 || VAR == 2))
     if (num_blocks(a.N) <= SAGE_K4_TAIL_MAXT) return launch_tt<D, C, QS, VAR, true>(a, s);
   return launch_tt<D, C, QS, VAR, false>(a, s);
