@@ -119,6 +119,12 @@ struct BwdSmem {
                               // large share of its time (measured: S1K K4 -3.7%, S2K -2.4%; at C4 its extra
                               // register pressure costs +1%, so long sequences keep the plain kernel)
 #endif
+#ifndef SAGE_K4_DETDEFER
+#define SAGE_K4_DETDEFER 1  // SAGE_DETERMINISTIC, causal: a drain warp hands on its dQ turn at its next tile (its reduce
+                            // has completed by then) instead of waiting for the reduce right after issuing it
+                            // (measured: C4 K4 15.14 -> 13.52 ms; the non-causal rotated order, where the next
+                            // contributor is exactly one tile behind, gets slower: C2 0.748 -> 0.774 ms, so off there)
+#endif
 #ifndef SAGE_TRACE
 #define SAGE_TRACE 0
 #endif
@@ -253,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // visits the query blocks rotated, i = (j + it) mod T, and dQ_i's contributions come in iteration
   // order; all T CTAs of a head are co-resident (the API requires T <= SM count).
   constexpr bool det = VAR == 1;
+  constexpr bool kDetDefer = det && CAUSAL && SAGE_K4_DETDEFER;
   const int j = (det && CAUSAL) ? T - 1 - tile % T : tile % T;
   const int i0 = CAUSAL ? j : 0;
   const int n_it = T - i0;
@@ -945,6 +952,7 @@ if (cm) {
 #pragma unroll
     for (int c = 0; c < kRegV; ++c) dv_acc[c] = 0.f;
 
+    unsigned* det_pending = nullptr;  // SAGE_DETERMINISTIC: the dQ turn this warp still has to hand on
     for (int it = 0; it < n_it; ++it) {
       const int i = i_of(it);
       const uint32_t ph = it & 1;
@@ -1038,7 +1046,13 @@ if (cm) {
         uint8_t* wstage = smem + L::kDq + (warp % 4) * L::kDqWarp;
         unsigned* flag = det ? dq_flags + ((size_t)bh * T + i) * kDrainWarps + (warp % 4) : nullptr;
         if (det) {  // wait for the contributions ordered before this one: (i - j) mod T of them
-          if (lane == 0) flag_wait_geq(flag, (unsigned)((i - j + T) % T));
+          if (lane == 0) {
+            if (kDetDefer && det_pending) {  // the previous tile's contribution, complete in L2 by now
+              bulk_wait_all();
+              flag_release_add(det_pending);
+            }
+            flag_wait_geq(flag, (unsigned)((i - j + T) % T));
+          }
           __syncwarp();
         }
         // SAGE_K4_TAIL: the compute warps take the last tile's columns 64..127
@@ -1078,7 +1092,9 @@ if (cm) {
             bulk_commit();
           }
         }
-        if (det) {  // this contribution complete in L2, then pass the turn on
+        if (kDetDefer) {
+          det_pending = flag;  // handed on at the next tile (or after the loop)
+        } else if (det) {  // this contribution complete in L2, then pass the turn on
           if (lane == 0) {
             bulk_wait_all();
             flag_release_add(flag);
@@ -1091,6 +1107,7 @@ if (cm) {
       if (threadIdx.x == 384) TR(13, it);
     }
     if (lane == 0) bulk_wait_all();  // staging smem must outlive this warp's in-flight reduces
+    if (kDetDefer && lane == 0 && det_pending) flag_release_add(det_pending);
     if constexpr (kAlias && !kTail) {  // the compute warps' last dV accumulation
       mbar_wait(dv_drained, (n_it - 1) & 1);
       tc_fence_after();
