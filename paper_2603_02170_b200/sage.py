@@ -343,6 +343,10 @@ def forward_qknorm(xq, xk, v, gamma_q, gamma_k, eps=1e-6, causal=False, k_smooth
     p = make_params(B, H, N, d, causal, k_smooth, q_smooth, softmax_scale, p_u8, qk_norm=True,
                     deterministic=deterministic, p_colscale=p_colscale, fine_bwd=fine_bwd,
                     fp16=xq.dtype == torch.float16, strides=strides)
+    if xq.numel() == 0 and d in (64, 128):  # empty batch, heads or sequence: empty results, nothing launched
+        return (torch.empty_strided(xq.shape, xq.stride(), dtype=xq.dtype, device=dev),
+                torch.empty((B, H, N), dtype=torch.float32, device=dev),
+                SageCtx(p, torch.empty(0, dtype=torch.uint8, device=dev), (B, H, N, d), xq.stride()))
     nctx = lib().sage_ctx_bytes(ctypes.byref(p))
     if nctx == 0:
         raise SageError(f"unsupported shape/flags {tuple(xq.shape)}")
@@ -375,6 +379,10 @@ def backward_qknorm(ctx, xq, xk, gamma_q, gamma_k, v, o, lse, do, out=None, work
     _check_gamma(gamma_k, d, dev)
     B, H, N, _ = ctx.shape
     _check_out(lse, (B, H, N), torch.float32, dev, "lse")
+    if do.numel() == 0:  # the empty forward's context: empty dX, dV and zero dgamma
+        mk = lambda: torch.empty_strided(ctx.shape, st, dtype=do.dtype, device=dev)
+        return (mk(), mk(), mk(), torch.zeros(d, dtype=torch.float32, device=dev),
+                torch.zeros(d, dtype=torch.float32, device=dev))
     with torch.cuda.device(dev):
         if out is None:
             mk = lambda: torch.empty_strided(ctx.shape, st, dtype=do.dtype, device=dev)

@@ -189,6 +189,10 @@ def test_empty_inputs(shape):
     out = sage.sage_attention(qa, k, v, causal=True)
     out.sum().backward()
     assert out.shape == shape and qa.grad.shape == shape
+    g = torch.ones(shape[3], dtype=torch.float32, device="cuda")
+    o, lse, ctx = sage.forward_qknorm(q, k, v, g, g, 1e-6, causal=True)
+    dxq, dxk, dv, dgq, dgk = sage.backward_qknorm(ctx, q, k, g, g, v, o, lse, do)
+    assert dxq.shape == shape and dgq.shape == (shape[3],) and not dgq.any()
 
 
 def test_ragged_max_length_sampled():
