@@ -125,6 +125,11 @@ struct BwdSmem {
                             // (measured: C4 K4 15.14 -> 13.52 ms; the non-causal rotated order, where the next
                             // contributor is exactly one tile behind, gets slower: C2 0.748 -> 0.774 ms, so off there)
 #endif
+#ifndef SAGE_K4_HGROUP
+#define SAGE_K4_HGROUP 4  // CTA order: groups of this many heads, within a group key block j major (all the
+                          // group's j = 0 CTAs, then j = 1, ...): longest-first across the group while only a few
+                          // heads' Q^/dO^/dO tiles are in flight (L2 reuse); 1 = head-major
+#endif
 #ifndef SAGE_TRACE
 #define SAGE_TRACE 0
 #endif
@@ -250,9 +255,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t one = blockDim.x / kThreads;  // a runtime 1 (i2f2 on the FMA pipe, SAGE_I2F_FMA)
   const int tile = blockIdx.x;
-  // head-major order: the T CTAs of one head run together and share its Q^/dO/dO^ tiles and
-  // its dQ accumulator through L2; within a head, low j (most query blocks when causal) first.
-  const int bh = tile / T;
+  // CTA order: heads in groups of SAGE_K4_HGROUP, within a group low j (most query blocks when causal) first
+  // across its heads, so the group's CTAs share its Q^/dO/dO^ tiles and dQ rows through L2 and the longest
+  // CTAs never start in the grid's last wave (SAGE_DETERMINISTIC keeps one head at a time, see below).
+  constexpr int kHG = VAR == 1 ? 1 : SAGE_K4_HGROUP;
+  const int grp = tile / (kHG * T), g_heads = min(kHG, BH - grp * kHG), within = tile - grp * kHG * T;
+  const int bh = grp * kHG + within % g_heads;
   // SAGE_DETERMINISTIC (dq_flags != null): dQ_i receives its key-block contributions in a fixed order,
   // enforced with per-(head, i, drain warp) flags.  Causal: descending j (j = i first), so the CTAs
   // launch high j first and every CTA only waits on CTAs launched before it.  Non-causal: CTA j
@@ -260,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // order; all T CTAs of a head are co-resident (the API requires T <= SM count).
   constexpr bool det = VAR == 1;
   constexpr bool kDetDefer = det && CAUSAL && SAGE_K4_DETDEFER;
-  const int j = (det && CAUSAL) ? T - 1 - tile % T : tile % T;
+  const int j = (det && CAUSAL) ? T - 1 - tile % T : (kHG == 1 ? tile % T : within / g_heads);
   const int i0 = CAUSAL ? j : 0;
   const int n_it = T - i0;
   auto i_of = [&](int it) { return (det && !CAUSAL) ? (j + it) % T : i0 + it; };

@@ -43,6 +43,10 @@ constexpr float kLog2_448 = 8.807354922057604f;
 #ifndef SAGE_K2_POLY
 #define SAGE_K2_POLY 1
 #endif
+#ifndef SAGE_K2_HGROUP
+#define SAGE_K2_HGROUP 4  // CTA order: groups of this many heads, within a group the longest query blocks first
+                          // across its heads (1 = head-major), as in K4
+#endif
 #ifndef SAGE_K2_P2DB
 #define SAGE_K2_P2DB 1  // pass 2 in 16-column pieces, the next piece's TMEM load in flight (0: 32-column chunks)
 #endif
@@ -116,10 +120,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int T = num_blocks(N), Np = T * kBlk;
   const int warp = threadIdx.x / 32;
   const uint32_t one = blockDim.x / kThreads;  // a runtime 1 (i2f2 on the FMA pipe, SAGE_I2F_FMA)
-  // head-major order (the CTAs of one head share K^/V^ through L2); causal: longest (high i) first
+  // heads in groups of SAGE_K2_HGROUP (the group's CTAs share its K^/V^ through L2); within a group, causal:
+  // longest (high i) first across its heads, so the longest CTAs never start in the grid's last wave
   const int tile = blockIdx.x;
-  const int bh = tile / T;
-  const int i = CAUSAL ? (T - 1 - tile % T) : (tile % T);
+  constexpr int kHG = SAGE_K2_HGROUP;
+  const int grp = tile / (kHG * T), g_heads = min(kHG, BH - grp * kHG), within = tile - grp * kHG * T;
+  const int bh = grp * kHG + within % g_heads, idx = within / g_heads;
+  const int i = CAUSAL ? (T - 1 - idx) : idx;
   const int nj = CAUSAL ? i + 1 : T;
   const int row0 = bh * Np + i * kBlk;  // first row of this q block in the padded int8 tiles
   const int kv_last = N - (T - 1) * kBlk;  // keys of the last kv block (128 unless N is ragged)
