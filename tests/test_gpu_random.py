@@ -66,3 +66,16 @@ def test_random_parity(seed):
                    p_col=var in ("p_colscale", "fine_bwd"), ds_fine=var == "fine_bwd", **okw)
     gpu = dict(o=o, lse=lse, dq=dq, dk=dk, dv=dv)
     _assert_ok(_compare(gpu, f, b, heads, B, H, N, d, out_round=rnd), c)
+
+
+@pytest.mark.parametrize("B,H,d,causal", [(1, 5, 64, True), (3, 1, 128, True), (1, 7, 128, False)])
+def test_head_counts_around_the_cta_groups(B, H, d, causal):
+    """K2 / K4 order their CTAs in groups of 4 heads (the last group short): head counts that leave a partial
+    group must still cover every (head, block) once."""
+    from tests.test_gpu import _oracle, _run
+    N = 384
+    q, k, v, do = make_inputs(B, H, N, d, "qknorm", seed=3100 + B * H + d)
+    gpu = _run(q, k, v, do, causal, True, False)
+    heads = list(range(B * H))
+    f, b = _oracle(q, k, v, do, heads, causal, True, False)
+    _assert_ok(_compare(gpu, f, b, heads, B, H, N, d), (B, H, d, causal))
