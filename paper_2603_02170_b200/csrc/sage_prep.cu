@@ -186,7 +186,16 @@ __global__ void colmean_kernel(const double* __restrict__ part, float* __restric
   int bh = item / d, c = item % d, T = num_blocks(N);
   const double* p = part + (size_t)bh * T * d + c;
   double total = 0.0;
-  for (int t = 0; t < T; ++t) total += p[(size_t)t * d];
+  // sequential in t (A17); the loads of 8 chunks are issued ahead of their adds
+  int t = 0;
+  for (; t + 8 <= T; t += 8) {
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = p[(size_t)(t + u) * d];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) total += x[u];
+  }
+  for (; t < T; ++t) total += p[(size_t)t * d];
   mu[item] = __double2float_rn(total / (double)N);
 }
 
